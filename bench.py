@@ -1,0 +1,432 @@
+"""Benchmark of the tet-walk track-length tally (BASELINE.json metric:
+tet-crossings/s and particle-moves/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Under torchrun (N > 1) there is one rank per GPU; every rank owns a shard of
+particles (weak scaling: the per-GPU particle count is fixed), a replica of
+the mesh and a private tally; once per batch the tallies are summed with one
+NCCL all-reduce before the on-device finalize.
+
+A step is one batch of the hot path over the whole synthetic workload:
+restore the localized start state (device-to-device), one
+move_to_next_location of every particle, tally reduce (N > 1), finalize.
+`e2e` repeats the batch through the public API with pinned HOST buffers:
+initialize_particle_location + move_to_next_location + finalize, H2D of the
+inputs and D2H of the TraceSummary inside the timed region.
+
+The CPU baseline is the oracle port of the reference's algorithm
+(oracle/walk_oracle.c, OpenMP, all host threads) timed on a bounded sample
+of the same workload on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+B_CROSSING = 133  # algorithmic bytes per tet-crossing
+B_MOVE = 100      # algorithmic bytes per particle-move
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--n", type=int, default=55, help="cube subdivisions (55 -> 998,250 tets)")
+    p.add_argument("--particles", type=int, default=10_000_000, help="particles per GPU")
+    p.add_argument("--sigma-t", type=float, default=2.0)
+    p.add_argument("--cpu-seconds", type=float, default=10.0,
+                   help="target CPU work for the bounded baseline sample")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--sort", type=int, default=1)
+    p.add_argument("--warp-agg", type=int, default=1)
+    p.add_argument("--blocks-per-sm", type=int, default=0)
+    return p.parse_args()
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def workload(n_particles, sigma_t, rank):
+    from paper_2504_19048_b200 import synth
+    gen = synth.rng(synth.SEED + 1000 * rank)
+    pos = synth.uniform_box(gen, n_particles)
+    dest = synth.flight_destinations(gen, pos, sigma_t)
+    return pos, dest
+
+
+def config(args, world, ne):
+    return {
+        "workload": (f"north-star point of configs[1]/[2]: unit cube n={args.n} "
+                     f"({ne:,} tets), {args.particles:,} particles per GPU uniform in "
+                     f"[0.05,0.95]^3, isotropic flights -ln(u)/{args.sigma_t} cm, weight 1, "
+                     "1 group, one move per batch"),
+        "mesh_elements": ne,
+        "particles_per_gpu": args.particles,
+        "global_particles": args.particles * world,
+        "sigma_t": args.sigma_t,
+        "parallelism": f"dp{world} (particle shards, mesh replicated, tally all-reduce)",
+        "l2": "particle state ~1 GB/GPU streamed per step (> 126 MB L2, no flush needed); "
+              "mesh 38 MB stays L2-resident by design",
+        "options": {"sort": bool(args.sort), "warp_agg": bool(args.warp_agg)},
+    }
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling during the timed region
+
+class Clocks:
+    def __init__(self, dev):
+        self.dev = dev
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        def run():
+            cmd = ["nvidia-smi", "-i", str(self.dev),
+                   "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                   "--format=csv,noheader,nounits"]
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(cmd, capture_output=True, text=True, timeout=5).stdout
+                    a = [x.strip() for x in out.strip().split(",")]
+                    self.samples.append((float(a[0]), float(a[1]), int(a[2], 16)))
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        names = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+                 0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+                 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+                 0x100: "display_clock_setting"}
+        bits = 0
+        for _, _, b in self.samples:
+            bits |= b
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": [v for k, v in names.items() if bits & k and k != 0x1],
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: oracle port, bounded sample
+
+def cpu_sample_rate(mesh, pos, dest, target_s, threads=None):
+    """Time the oracle's trace_and_score restatement on a sample sized for
+    ~target_s seconds; returns (crossings/s, moves/s, detail)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as orc
+    threads = threads or orc.max_threads()
+
+    def run(k):
+        t = orc.OracleTally(mesh, k, threads=threads)
+        t.initialize_particle_location(pos[:k])
+        fly = np.ones(k, np.int8)
+        w = np.ones(k)
+        t0 = time.perf_counter()
+        s = t.move_to_next_location(dest[:k], fly, w)
+        dt = time.perf_counter() - t0
+        return s, dt
+
+    k = min(20_000, pos.shape[0])
+    s, dt = run(k)
+    if dt < target_s / 4 and k < pos.shape[0]:
+        k = int(min(pos.shape[0], k * target_s / max(dt, 1e-3)))
+        s, dt = run(k)
+    detail = {"sample": f"first {k:,} particles of rank 0's workload, one move "
+                        f"({s.events:,} crossings), localization untimed",
+              "cores": threads, "seconds": round(dt, 3), "particles": k}
+    return s.events / dt, k / dt, detail, s, dt
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------------
+
+def run_reference(args):
+    rank, world, local = env_rank()
+    if rank != 0:
+        return
+    from paper_2504_19048_b200 import build_cube_mesh
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as orc
+    mesh = build_cube_mesh(args.n)
+    pos, dest = workload(args.particles, args.sigma_t, 0)
+    threads = orc.max_threads()
+    # size one step at ~2 s of CPU work so the whole run stays within minutes
+    per_step = float(os.environ.get("BENCH_REF_STEP_S", "2.0"))
+    _, _, detail, _, _ = cpu_sample_rate(mesh, pos, dest, per_step, threads)
+    k = detail["particles"]
+    t = orc.OracleTally(mesh, k, threads=threads)
+    t.initialize_particle_location(pos[:k])
+    snap = {f: getattr(t, f).copy() for f in ("position", "element", "alive", "entry_face",
+                                              "stuck", "outcome", "seg_total")}
+    fly = np.ones(k, np.int8)
+    w = np.ones(k)
+
+    def step():
+        for f, v in snap.items():
+            getattr(t, f)[:] = v
+        s = t.move_to_next_location(dest[:k], fly, w)
+        t.finalize_batch()
+        return s
+
+    for _ in range(args.warmup):
+        step()
+    ev = moves = 0
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        s = step()
+        ev += s.events
+        moves += k
+    dt = time.perf_counter() - t0
+    val = ev / dt
+    out = {
+        "impl": "reference",
+        "metric": "tet-crossings/s", "value": val, "unit": "crossings/s",
+        "particle_moves_per_s": moves / dt,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config(args, 1, mesh.num_elements),
+        "cpu_baseline": {"value": val, "unit": "crossings/s", "cores": threads, "kind": "port",
+                         "sample": f"first {k:,} of the {args.particles:,} particles per "
+                                   "step (same workload), oracle/walk_oracle.c (C "
+                                   "restatement of search.py:169-275, OpenMP)",
+                         "cpu": cpu_model()},
+        "e2e": {"value": val, "unit": "crossings/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def run_ours(args):
+    import torch
+    rank, world, local = env_rank()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    from paper_2504_19048_b200 import MeshTally, build_cube_mesh
+    from paper_2504_19048_b200 import _lib
+
+    mesh = build_cube_mesh(args.n)
+    P = args.particles
+    pos, dest = workload(P, args.sigma_t, rank)
+
+    mt = MeshTally(mesh, P, device=local, sort=bool(args.sort),
+                   warp_aggregate=bool(args.warp_agg))
+    if args.blocks_per_sm:
+        mt.set_option(_lib.BT_OPT_BLOCKS_PER_SM, args.blocks_per_sm)
+    d_pos = torch.from_numpy(pos).to(dev)
+    d_dest = torch.from_numpy(dest).to(dev)
+    d_fly = torch.ones(P, dtype=torch.int8, device=dev)
+    d_w = torch.ones(P, dtype=torch.float64, device=dev)
+    mt.initialize_particle_location(d_pos)
+    st = mt.read_particles(P)
+    lost = int((st.element < 0).sum())
+    mt.save_state()
+
+    nb = mesh.num_elements
+    tally_t = None
+    if dist is not None:
+        class _CAI:
+            def __init__(self, ptr, n):
+                self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8",
+                                                 "data": (ptr, False), "version": 3,
+                                                 "strides": None}
+        tally_t = torch.as_tensor(_CAI(mt.tally_device_ptr(), nb), device=dev)
+
+    stats = {"events": 0, "moves": 0, "walk_ms": 0.0, "kernels": 0}
+
+    def step(record):
+        mt.restore_state()
+        s = mt.move_to_next_location(d_dest, d_fly, d_w)
+        wk, _, kern = mt.last_timing()
+        if dist is not None:
+            dist.all_reduce(tally_t)
+            w = torch.tensor([mt.source_weight], dtype=torch.float64, device=dev)
+            dist.all_reduce(w)
+            mt.finalize_batch(float(w.item()))
+        else:
+            mt.finalize_batch()
+        if record:
+            stats["events"] += s.events
+            stats["moves"] += P - lost
+            stats["walk_ms"] += wk
+            stats["kernels"] += kern + 1
+        return s
+
+    for _ in range(args.warmup):
+        step(False)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    clocks = Clocks(local)
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with clocks:
+        e0.record()
+        for _ in range(args.steps):
+            step(True)
+        e1.record()
+        barrier()
+    ms = e0.elapsed_time(e1)
+    tot = torch.tensor([stats["events"], stats["moves"]], dtype=torch.float64, device=dev)
+    msmax = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(tot)
+        dist.all_reduce(msmax, op=dist.ReduceOp.MAX)
+    ms_total = float(msmax.item())
+    events_all, moves_all = float(tot[0].item()), float(tot[1].item())
+    value = events_all / (ms_total / 1e3)
+    moves_per_s = moves_all / (ms_total / 1e3)
+
+    # roofline of the walk kernel (rank-local, CUDA events on the library stream)
+    walk_s = stats["walk_ms"] / 1e3
+    alg_bytes = B_CROSSING * stats["events"] + B_MOVE * stats["moves"]
+    achieved = alg_bytes / walk_s / 1e9
+    peaks_p = ROOT / "MEASURED_PEAKS.json"
+    if peaks_p.exists():
+        peak = float(json.loads(peaks_p.read_text())["hbm_gbs"])
+        peak_src = "measured"
+    else:
+        peak, peak_src = 6650.0, "fallback"
+    traffic = None
+    tp = ROOT / "profiles" / "walk_dram_traffic.json"
+    if tp.exists():
+        try:
+            traffic = json.loads(tp.read_text()).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # e2e through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        h_pos = torch.from_numpy(pos).pin_memory().numpy()
+        h_dest = torch.from_numpy(dest).pin_memory().numpy()
+        h_fly = torch.ones(P, dtype=torch.int8).pin_memory().numpy()
+        h_w = torch.ones(P, dtype=torch.float64).pin_memory().numpy()
+        ev_e2e = 0
+
+        def e2e_step():
+            mt.initialize_particle_location(h_pos)
+            s = mt.move_to_next_location(h_dest, h_fly, h_w)
+            if dist is not None:
+                dist.all_reduce(tally_t)
+                w = torch.tensor([mt.source_weight], dtype=torch.float64, device=dev)
+                dist.all_reduce(w)
+                mt.finalize_batch(float(w.item()))
+            else:
+                mt.finalize_batch()
+            return s
+        e2e_step()
+        barrier()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(args.steps):
+            ev_e2e += e2e_step().events
+        f1.record()
+        barrier()
+        ms2 = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
+        ev2 = torch.tensor([float(ev_e2e)], dtype=torch.float64, device=dev)
+        if dist is not None:
+            dist.all_reduce(ms2, op=dist.ReduceOp.MAX)
+            dist.all_reduce(ev2)
+        e2e = {"value": float(ev2.item()) / (float(ms2.item()) / 1e3), "unit": "crossings/s",
+               "h2d_bytes_per_step": int(h_pos.nbytes + h_dest.nbytes + h_fly.nbytes
+                                         + h_w.nbytes) * world,
+               "d2h_bytes_per_step": 48 * world,
+               "ms_per_step": float(ms2.item()) / args.steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, mrate, detail, _, _ = cpu_sample_rate(mesh, pos, dest, args.cpu_seconds)
+        cpu = {"value": rate, "unit": "crossings/s", "cores": detail["cores"], "kind": "port",
+               "sample": detail["sample"], "particle_moves_per_s": mrate,
+               "seconds": detail["seconds"], "cpu": cpu_model()}
+
+    if rank == 0:
+        out = {
+            "metric": "tet-crossings/s", "value": value, "unit": "crossings/s",
+            "particle_moves_per_s": moves_per_s,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded numpy: uniform starts, isotropic exponential flights)",
+            "config": config(args, world, mesh.num_elements),
+            "crossings_per_move": events_all / max(moves_all, 1.0),
+            "e2e": e2e,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": peak_src,
+                         "kernel": "walk_kernel", "kernel_ms_per_step": stats["walk_ms"] / args.steps,
+                         "algorithmic_bytes": "133 B/crossing + 100 B/move (SURVEY.md §8d)"},
+            "cpu_baseline": cpu,
+            "clocks": clocks.summary(),
+            "gpu_launches": stats["kernels"],
+            "lost_at_localization": lost,
+        }
+        print(json.dumps(out), flush=True)
+    mt.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,164 @@
+/*
+ * b200tally.h -- C ABI of the B200-native PUMI-Tally hot path
+ * (libb200tally.so, built from paper_2504_19048_b200/csrc/).
+ *
+ * The boundary is the paper's PIMPL interface (Listing 2 at
+ * PAPER.md:265-270) as restated by the reference's Python facade
+ * meshtally.MeshTally (tally.py:203-286):
+ *
+ *   PumiTally(mesh, num_particles, ...)            -> bt_create
+ *   initialize_particle_location(double*, size)    -> bt_initialize_particle_location
+ *   move_to_next_location(double*, int8_t*, double*, size)
+ *                                                  -> bt_move_to_next_location
+ *   MeshTally.finalize_batch / flux / grid         -> bt_finalize_batch, bt_read_tally
+ *
+ * Plain pointers and sizes only.  Buffers are HOST memory when mem_kind ==
+ * BT_MEM_HOST (pinned or pageable; copied in and out on the handle's stream)
+ * or DEVICE memory on the handle's GPU when mem_kind == BT_MEM_DEVICE
+ * (zero-copy, e.g. a torch CUDA tensor's data_ptr()).  Caller buffers are never
+ * retained past the call.  Every function returns a bt_status; the message
+ * of the last failure on the calling thread is bt_last_error().
+ *
+ * A handle is not re-entrant; one host thread drives it.  All calls are
+ * synchronous with respect to the host unless documented otherwise.
+ */
+#ifndef B200TALLY_H
+#define B200TALLY_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bt_tally bt_tally;
+
+/* Status codes; the Python layer maps them to the reference's exception
+ * classes (tally.py:219-222, particles.py:65-73, search.py:513-516). */
+typedef enum {
+    BT_OK = 0,
+    BT_EINVAL = 1,    /* ValueError: bad size / count > capacity / bad argument */
+    BT_ERUNTIME = 2,  /* RuntimeError: sweep guard exceeded, no source weight */
+    BT_ECUDA = 3,     /* RuntimeError: CUDA failure (message names the call) */
+    BT_EINDEX = 4,    /* IndexError: group out of [0, num_groups) */
+    BT_ENOMEM = 5     /* MemoryError: device allocation failed */
+} bt_status;
+
+enum { BT_MEM_HOST = 0, BT_MEM_DEVICE = 1 };
+
+/* localization modes for bt_initialize_particle_location */
+enum {
+    BT_LOCATE_GRID = 0, /* uniform-grid candidate search, lowest containing id */
+    BT_LOCATE_WALK = 1  /* reference semantics: centroid-0 walk + tie-break
+                           (search.py:557-601), bit-exact incl. lost points */
+};
+
+/* tally arrays for bt_read_tally / bt_tally_device_ptr */
+enum {
+    BT_TALLY_BATCH = 0, /* unfinalized per-bin totals (tally.py:101-104) */
+    BT_TALLY_SUM = 1,   /* running sum of normalised batch tallies */
+    BT_TALLY_SUM_SQ = 2 /* running sum of squares */
+};
+
+/* options for bt_set_option */
+enum {
+    BT_OPT_MAX_SWEEPS = 0,   /* sweep guard; <0 -> 2*E + 1000 (search.py:449-450) */
+    BT_OPT_DIGEST = 1,       /* 1: record per-particle (element, face) digests */
+    BT_OPT_SORT = 2,         /* 1: hand particles to warps in element order */
+    BT_OPT_WARP_AGG = 3,     /* 1: __match_any_sync aggregation of tally atomics */
+    BT_OPT_BLOCKS_PER_SM = 4 /* persistent walk grid: CTAs per SM (0 = auto) */
+};
+
+/* Mirrors meshtally.search.TraceSummary (search.py:150-157). */
+typedef struct {
+    int64_t sweeps;
+    int64_t events;
+    int64_t reached;
+    int64_t boundary_exits;
+    int64_t stuck_recoveries;
+    int64_t stuck_terminations;
+} bt_summary;
+
+/*
+ * Upload a mesh and allocate a fixed-capacity particle batch + tally on
+ * `device` (MeshTally.__init__, tally.py:211-229; create_batch,
+ * create_workspace, create_grid).  Arrays are host memory in the reference
+ * layout (TetMesh, mesh.py:73-83): vertices (V,3) f64, elements (E,4) i32,
+ * adj_elem (E,4) i32 (-1 = boundary), adj_face (E,4) i8, bbox (2,3) f64,
+ * centroid0 = centroids[0] (3) f64 (the localization trial point).
+ */
+bt_status bt_create(const double *vertices, int64_t num_vertices, const int32_t *elements,
+                    const int32_t *adj_elem, const int8_t *adj_face, int64_t num_elements,
+                    const double *bbox, const double *centroid0, int64_t num_particles,
+                    int32_t num_groups, int32_t device, bt_tally **out);
+
+bt_status bt_destroy(bt_tally *h);
+
+/*
+ * initialize_particle_location(double* pos, int64_t size)
+ * (tally.py:239-245 -> search.py:557-601).  size = number of doubles
+ * (3 * count); size % 3 != 0 or count > capacity -> BT_EINVAL.  Resets the
+ * batch's recorded source weight.  `summary` (nullable) receives the trial
+ * walk's counters in BT_LOCATE_WALK mode, zeros in grid mode.
+ */
+bt_status bt_initialize_particle_location(bt_tally *h, const double *positions, int64_t size,
+                                          int32_t mem_kind, int32_t mode, bt_summary *summary);
+
+/*
+ * move_to_next_location(double* dest, int8_t* flying, double* weights,
+ * int64_t size) (tally.py:247-271; load_step particles.py:57-89;
+ * trace_and_score search.py:492-517).  size = count of particles; dest holds
+ * 3*count doubles (xyz interleaved); groups is nullable (keeps previous
+ * groups).  On the first move of a batch the source weight is recorded as the
+ * sum of weights of flying particles.  count == 0 -> BT_OK with an all-zero
+ * summary (the Python facade returns None).
+ */
+bt_status bt_move_to_next_location(bt_tally *h, const double *destinations, const int8_t *flying,
+                                   const double *weights, const int32_t *groups, int64_t size,
+                                   int32_t mem_kind, bt_summary *summary);
+
+/* finalize_batch (tally.py:273-279, _finalize tally.py:83-95).
+ * source_weight <= 0 -> use the recorded one (BT_ERUNTIME if none). */
+bt_status bt_finalize_batch(bt_tally *h, double source_weight);
+
+/* Copy a tally array (E*G doubles) to host `out` (n must equal E*G). */
+bt_status bt_read_tally(bt_tally *h, int32_t which, double *out, int64_t n);
+
+/* Device pointer of a tally array (for an NCCL reduce across GPUs). */
+bt_status bt_tally_device_ptr(bt_tally *h, int32_t which, void **ptr);
+
+/* Source weight recorded on the first move of the current batch. */
+bt_status bt_get_source_weight(bt_tally *h, double *w);
+bt_status bt_set_source_weight(bt_tally *h, double w);
+bt_status bt_batches_completed(bt_tally *h, int64_t *n);
+
+/* Particle state readout, [0, count); any output pointer may be NULL. */
+bt_status bt_read_particles(bt_tally *h, int64_t count, double *position, int32_t *element,
+                            int8_t *alive, int8_t *entry_face, int8_t *stuck, int8_t *outcome,
+                            double *seg_total);
+
+/* Per-particle digest + scored-event count of the LAST move (BT_OPT_DIGEST). */
+bt_status bt_read_digest(bt_tally *h, int64_t count, uint64_t *digest, int64_t *events);
+
+bt_status bt_set_option(bt_tally *h, int32_t key, int64_t value);
+
+/* Device time of the last call's walk kernel(s), CUDA events on the
+ * handle's stream, and the number of kernels the library launched. */
+bt_status bt_last_timing(bt_tally *h, float *walk_ms, float *call_ms, int64_t *kernels);
+
+/* Snapshot / restore of the per-particle state (device-to-device); used by
+ * the benchmark to replay one move over an identical start state. */
+bt_status bt_save_state(bt_tally *h);
+bt_status bt_restore_state(bt_tally *h);
+
+/* Device ordinal and sizes. */
+bt_status bt_info(bt_tally *h, int32_t *device, int64_t *num_elements, int64_t *capacity,
+                  int32_t *num_groups);
+
+const char *bt_last_error(void);
+const char *bt_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B200TALLY_H */

@@ -1,0 +1,105 @@
+"""ctypes binding of libb200tally.so (the C ABI in include/b200tally.h).
+
+The product path has no CPU fallback: if the shared library is missing or
+no CUDA device is visible, handle creation raises.  Status codes map onto
+the reference's exception classes (tally.py:219-222, particles.py:65-73,
+search.py:513-516, tally.py:275-277).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "libb200tally.so"
+
+BT_OK, BT_EINVAL, BT_ERUNTIME, BT_ECUDA, BT_EINDEX, BT_ENOMEM = range(6)
+BT_MEM_HOST, BT_MEM_DEVICE = 0, 1
+BT_LOCATE_GRID, BT_LOCATE_WALK = 0, 1
+BT_TALLY_BATCH, BT_TALLY_SUM, BT_TALLY_SUM_SQ = 0, 1, 2
+(BT_OPT_MAX_SWEEPS, BT_OPT_DIGEST, BT_OPT_SORT, BT_OPT_WARP_AGG,
+ BT_OPT_BLOCKS_PER_SM) = range(5)
+
+# every symbol declared in include/b200tally.h (checked by tests/test_abi.py)
+EXPORTS = (
+    "bt_create", "bt_destroy", "bt_initialize_particle_location",
+    "bt_move_to_next_location", "bt_finalize_batch", "bt_read_tally",
+    "bt_tally_device_ptr", "bt_get_source_weight", "bt_set_source_weight",
+    "bt_batches_completed", "bt_read_particles", "bt_read_digest", "bt_set_option",
+    "bt_last_timing", "bt_save_state", "bt_restore_state", "bt_info",
+    "bt_last_error", "bt_version",
+)
+
+
+class Summary(C.Structure):
+    _fields_ = [("sweeps", C.c_int64), ("events", C.c_int64), ("reached", C.c_int64),
+                ("boundary_exits", C.c_int64), ("stuck_recoveries", C.c_int64),
+                ("stuck_terminations", C.c_int64)]
+
+
+_P = C.c_void_p
+_I64 = C.c_int64
+_I32 = C.c_int32
+
+_SIGS = {
+    "bt_create": [_P, _I64, _P, _P, _P, _I64, _P, _P, _I64, _I32, _I32, C.POINTER(_P)],
+    "bt_destroy": [_P],
+    "bt_initialize_particle_location": [_P, _P, _I64, _I32, _I32, C.POINTER(Summary)],
+    "bt_move_to_next_location": [_P, _P, _P, _P, _P, _I64, _I32, C.POINTER(Summary)],
+    "bt_finalize_batch": [_P, C.c_double],
+    "bt_read_tally": [_P, _I32, _P, _I64],
+    "bt_tally_device_ptr": [_P, _I32, C.POINTER(_P)],
+    "bt_get_source_weight": [_P, C.POINTER(C.c_double)],
+    "bt_set_source_weight": [_P, C.c_double],
+    "bt_batches_completed": [_P, C.POINTER(_I64)],
+    "bt_read_particles": [_P, _I64, _P, _P, _P, _P, _P, _P, _P],
+    "bt_read_digest": [_P, _I64, _P, _P],
+    "bt_set_option": [_P, _I32, _I64],
+    "bt_last_timing": [_P, C.POINTER(C.c_float), C.POINTER(C.c_float), C.POINTER(_I64)],
+    "bt_save_state": [_P],
+    "bt_restore_state": [_P],
+    "bt_info": [_P, C.POINTER(_I32), C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I32)],
+    "bt_last_error": [],
+    "bt_version": [],
+}
+
+_lib = None
+
+
+class ExtensionMissing(RuntimeError):
+    pass
+
+
+def load(build_if_missing: bool = True):
+    """Load (building first if needed) the CUDA library."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists() and build_if_missing:
+        from . import build as _build
+        _build.build()
+    if not LIB_PATH.exists():
+        raise ExtensionMissing(
+            f"{LIB_PATH} is missing: run `python -m paper_2504_19048_b200.build` "
+            "(there is no CPU fallback)")
+    L = C.CDLL(str(LIB_PATH))
+    for name, args in _SIGS.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = C.c_char_p if name in ("bt_last_error", "bt_version") else C.c_int
+    _lib = L
+    return L
+
+
+def check(status: int) -> None:
+    if status == BT_OK:
+        return
+    msg = load().bt_last_error().decode(errors="replace")
+    if status == BT_EINVAL:
+        raise ValueError(msg)
+    if status == BT_EINDEX:
+        raise IndexError(msg)
+    if status == BT_ENOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(msg)

@@ -1,0 +1,1419 @@
+// b200tally.cu -- B200-native (sm_100a) tet-mesh walk with track-length
+// tallies behind the C ABI declared in include/b200tally.h.
+//
+// Replaces the reference's numba hot path:
+//   _sweep_fused + trace_and_score  search.py:169-275, 492-517 -> walk_kernel
+//   initialize_locations            search.py:557-601          -> locate_grid_kernel
+//                                                                 (or walk_kernel + tiebreak_kernel)
+//   _tie_break_faces                search.py:520-551          -> tiebreak_kernel
+//   _finalize                       tally.py:83-95              -> finalize_kernel
+//   load_step                       particles.py:57-89          -> fused into walk_kernel's fetch
+//
+// Design: persistent CTAs, one particle per lane run to
+// completion; idle lanes refill from a global work counter (warp-aggregated
+// atomicAdd) so lanes stay busy despite the exponential crossings-per-move
+// tail; the mesh is one 32-byte record per element (vertex ids + packed
+// neighbour/face) plus 32-byte padded fp64 vertices, L2-resident up to ~3M
+// tets; tallies are fp64 atomics into a private per-GPU grid, optionally
+// aggregated per warp with __match_any_sync.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "../../include/b200tally.h"
+#include "geometry.cuh"
+
+using namespace bt;
+
+// ---------------------------------------------------------------------------
+// errors
+
+static thread_local std::string g_err;
+
+static bt_status set_err(bt_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess) {                                                          \
+            bt_status s_ = (e_ == cudaErrorMemoryAllocation) ? BT_ENOMEM : BT_ECUDA;      \
+            return set_err(s_, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_),    \
+                           __FILE__, __LINE__);                                           \
+        }                                                                                 \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// device data layout
+
+struct __align__(32) ElemRec {
+    int v[4];   // global vertex ids, reference local order (mesh.py:126-132)
+    int nb[4];  // (neighbour << 2) | neighbour's local face, -1 on the boundary
+};
+static_assert(sizeof(ElemRec) == 32, "one 32-byte sector per element");
+
+struct __align__(32) Vtx {
+    double x, y, z, pad;
+};
+static_assert(sizeof(Vtx) == 32, "one 32-byte sector per vertex");
+
+enum { C_EVENTS = 0, C_REACHED, C_BOUNDARY, C_RECOV, C_KILLED, C_SWEEPS, C_ERR, C_NCOUNTERS };
+
+struct WalkArgs {
+    const ElemRec* __restrict__ rec;
+    const Vtx* __restrict__ vtx;
+    double* __restrict__ pos;            // (N,3) persistent
+    const double* __restrict__ dest;     // (count,3) this move's destinations
+    const int8_t* __restrict__ fly_in;   // (count) this move's flying flags
+    const double* __restrict__ weight;   // (count) this move's weights (nullable if !score)
+    const int32_t* __restrict__ group;   // (N) persistent groups
+    int32_t* __restrict__ element;
+    int8_t* __restrict__ alive;
+    int8_t* __restrict__ entry;
+    int8_t* __restrict__ stuck;
+    int8_t* __restrict__ outcome;
+    double* __restrict__ seg_total;
+    double* __restrict__ tally;          // (E*G)
+    uint64_t* __restrict__ digest;       // (N) nullable
+    int64_t* __restrict__ dcount;        // (N) nullable
+    const int32_t* __restrict__ order;   // (count) nullable: hand-out permutation
+    unsigned long long* queue;
+    unsigned long long* counters;        // C_NCOUNTERS
+    int64_t count;
+    int64_t max_sweeps;
+    int32_t ngroups;
+    int32_t score;
+};
+
+__device__ __forceinline__ void load_tet(const WalkArgs& a, const ElemRec& r, Tet& T) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const double2* p = reinterpret_cast<const double2*>(a.vtx + r.v[j]);
+        const double2 xy = __ldg(p);
+        const double2 zw = __ldg(p + 1);
+        T.x[j] = xy.x;
+        T.y[j] = xy.y;
+        T.z[j] = zw.x;
+    }
+}
+
+__device__ __forceinline__ ElemRec load_rec(const ElemRec* __restrict__ rec, int e) {
+    const int4* p = reinterpret_cast<const int4*>(rec + e);
+    const int4 a = __ldg(p);
+    const int4 b = __ldg(p + 1);
+    ElemRec r;
+    r.v[0] = a.x; r.v[1] = a.y; r.v[2] = a.z; r.v[3] = a.w;
+    r.nb[0] = b.x; r.nb[1] = b.y; r.nb[2] = b.z; r.nb[3] = b.w;
+    return r;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// ---------------------------------------------------------------------------
+// walk kernel: the fused sweep (search.py:169-275) run to completion per lane
+
+constexpr int WALK_THREADS = 256;
+
+template <bool DIGEST, bool WAGG>
+__global__ void __launch_bounds__(WALK_THREADS) walk_kernel(const WalkArgs a) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+
+    int64_t idx = -1;
+    bool drained = false;
+    // particle state in registers
+    double px = 0, py = 0, pz = 0, dx = 0, dy = 0, dz = 0, w = 0, seg_acc = 0;
+    int e = 0, g = 0, entry = -1, st = 0, iters = 0;
+    uint64_t dig = DIGEST_INIT;
+    int dcnt = 0;
+    // per-lane counters (TraceSummary)
+    unsigned n_events = 0, n_reached = 0, n_boundary = 0, n_recov = 0, n_killed = 0;
+    int max_iters = 0;
+    int err = 0;
+
+    while (true) {
+        // ---- refill idle lanes from the global queue (one atomic per warp)
+        if (!drained) {
+            const unsigned idle = __ballot_sync(FULL, idx < 0);
+            if (idle) {
+                const unsigned nidle = __popc(idle);
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(a.queue, (unsigned long long)nidle);
+                base = __shfl_sync(FULL, base, 0);
+                if (base + nidle >= (unsigned long long)a.count) drained = true;
+                if (idx < 0) {
+                    const unsigned long long q = base + __popc(idle & lanemask_lt());
+                    if (q < (unsigned long long)a.count) {
+                        const int64_t i = a.order ? (int64_t)a.order[q] : (int64_t)q;
+                        if (a.fly_in[i] != 0) {
+                            idx = i;
+                            e = a.element[i];
+                            px = a.pos[3 * i];
+                            py = a.pos[3 * i + 1];
+                            pz = a.pos[3 * i + 2];
+                            dx = a.dest[3 * i];
+                            dy = a.dest[3 * i + 1];
+                            dz = a.dest[3 * i + 2];
+                            entry = a.entry[i];
+                            st = a.stuck[i];
+                            seg_acc = a.seg_total[i];
+                            if (a.score) {
+                                w = a.weight[i];
+                                g = a.group[i];
+                            }
+                            iters = 0;
+                            dig = DIGEST_INIT;
+                            dcnt = 0;
+                        }
+                    }
+                }
+            }
+        }
+        if (!__any_sync(FULL, idx >= 0)) {
+            if (drained) break;
+            continue;
+        }
+
+        bool has_score = false;
+        int64_t bin = 0;
+        double val = 0.0;
+        if (idx >= 0) {
+            const ElemRec r = load_rec(a.rec, e);
+            Tet T;
+            load_tet(a, r, T);
+            double ox = px, oy = py, oz = pz;
+            if (st == 1) {  // search.py:190-196
+                const double sx = __dsub_rn(dx, px), sy = __dsub_rn(dy, py),
+                             sz = __dsub_rn(dz, pz);
+                const double ln = __dsqrt_rn(__dadd_rn(
+                    __dadd_rn(__dmul_rn(sx, sx), __dmul_rn(sy, sy)), __dmul_rn(sz, sz)));
+                if (ln > 0.0) {
+                    ox = __dadd_rn(ox, __ddiv_rn(__dmul_rn(NUDGE, sx), ln));
+                    oy = __dadd_rn(oy, __ddiv_rn(__dmul_rn(NUDGE, sy), ln));
+                    oz = __dadd_rn(oz, __ddiv_rn(__dmul_rn(NUDGE, sz), ln));
+                }
+            }
+            int face;
+            double t;
+            int kind = exit_search(T, ox, oy, oz, dx, dy, dz, entry, &face, &t);
+            bool done = false;
+            bool event = true;
+            if (kind == 2) {  // stuck ladder, search.py:199-235
+                if (contains(T, dx, dy, dz, STUCK_TOL)) {
+                    kind = 0;
+                    ++n_recov;
+                } else if (st == 0) {
+                    st = 1;
+                    ++n_recov;
+                    event = false;
+                } else if (st == 1) {
+                    int hop = -1;
+                    for (int f = 0; f < 4; ++f) {
+                        const int nbp = r.nb[f];
+                        if (nbp >= 0) {
+                            const int nb = nbp >> 2;
+                            const ElemRec rn = load_rec(a.rec, nb);
+                            Tet Tn;
+                            load_tet(a, rn, Tn);
+                            if (contains(Tn, ox, oy, oz, EPS_BARY)) {
+                                hop = nb;
+                                break;
+                            }
+                        }
+                    }
+                    event = false;
+                    if (hop >= 0) {
+                        e = hop;
+                        entry = -1;
+                        st = 2;
+                        ++n_recov;
+                    } else {
+                        a.outcome[idx] = OUT_STUCK_KILLED;
+                        a.alive[idx] = 0;
+                        ++n_killed;
+                        done = true;
+                    }
+                } else {
+                    a.outcome[idx] = OUT_STUCK_KILLED;
+                    a.alive[idx] = 0;
+                    ++n_killed;
+                    event = false;
+                    done = true;
+                }
+            }
+            if (event) {  // search.py:236-274
+                ++n_events;
+                st = 0;
+                if (DIGEST) {
+                    dig = (dig ^ (uint64_t)((int64_t)e * 8 + face + 1)) * DIGEST_PRIME;
+                    ++dcnt;
+                }
+                double qx, qy, qz;
+                if (kind == 0) {
+                    qx = dx;
+                    qy = dy;
+                    qz = dz;
+                } else {
+                    qx = __dadd_rn(ox, __dmul_rn(t, __dsub_rn(dx, ox)));
+                    qy = __dadd_rn(oy, __dmul_rn(t, __dsub_rn(dy, oy)));
+                    qz = __dadd_rn(oz, __dmul_rn(t, __dsub_rn(dz, oz)));
+                }
+                const double ax = __dsub_rn(qx, px), ay = __dsub_rn(qy, py),
+                             az = __dsub_rn(qz, pz);
+                const double seg = __dsqrt_rn(__dadd_rn(
+                    __dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)), __dmul_rn(az, az)));
+                if (a.score) {
+                    has_score = true;
+                    bin = (int64_t)e * a.ngroups + g;
+                    val = __dmul_rn(w, seg);
+                }
+                seg_acc = __dadd_rn(seg_acc, seg);
+                px = qx;
+                py = qy;
+                pz = qz;
+                if (kind == 0) {
+                    entry = -1;
+                    a.outcome[idx] = OUT_REACHED;
+                    a.alive[idx] = 1;
+                    ++n_reached;
+                    done = true;
+                } else {
+                    const int nbp = r.nb[face];
+                    if (nbp < 0) {
+                        a.outcome[idx] = OUT_LEAKED;
+                        a.alive[idx] = 0;
+                        ++n_boundary;
+                        done = true;
+                    } else {
+                        e = nbp >> 2;
+                        entry = nbp & 3;
+                    }
+                }
+            }
+            ++iters;
+            if (!done && iters > a.max_sweeps) {  // sweep guard, search.py:513-516
+                err = 1;
+                a.alive[idx] = 1;
+                done = true;
+            }
+            if (done) {
+                a.pos[3 * idx] = px;
+                a.pos[3 * idx + 1] = py;
+                a.pos[3 * idx + 2] = pz;
+                a.element[idx] = e;
+                a.entry[idx] = (int8_t)entry;
+                a.stuck[idx] = (int8_t)st;
+                a.seg_total[idx] = seg_acc;
+                if (DIGEST) {
+                    a.digest[idx] = dig;
+                    a.dcount[idx] = dcnt;
+                }
+                max_iters = max(max_iters, iters);
+                idx = -1;
+            }
+        }
+
+        // ---- tally: fp64 atomics, optionally aggregated over equal bins
+        if (WAGG) {
+            const unsigned m = __ballot_sync(FULL, has_score);
+            if (has_score) {
+                const unsigned peers = __match_any_sync(m, (unsigned long long)bin);
+                const int leader = __ffs(peers) - 1;
+                double sum = val;
+                if (peers != (1u << lane)) {
+                    sum = 0.0;
+                    unsigned rest = peers;
+                    while (rest) {
+                        const int src = __ffs(rest) - 1;
+                        rest &= rest - 1;
+                        sum = __dadd_rn(sum, __shfl_sync(peers, val, src));
+                    }
+                }
+                if (lane == leader) atomicAdd(a.tally + bin, sum);
+            }
+        } else if (has_score) {
+            atomicAdd(a.tally + bin, val);
+        }
+    }
+
+    // ---- counters: warp reduce, one atomic per warp
+    n_events = __reduce_add_sync(FULL, n_events);
+    n_reached = __reduce_add_sync(FULL, n_reached);
+    n_boundary = __reduce_add_sync(FULL, n_boundary);
+    n_recov = __reduce_add_sync(FULL, n_recov);
+    n_killed = __reduce_add_sync(FULL, n_killed);
+    max_iters = __reduce_max_sync(FULL, max_iters);
+    err = __reduce_or_sync(FULL, err);
+    if (lane == 0) {
+        if (n_events) atomicAdd(a.counters + C_EVENTS, (unsigned long long)n_events);
+        if (n_reached) atomicAdd(a.counters + C_REACHED, (unsigned long long)n_reached);
+        if (n_boundary) atomicAdd(a.counters + C_BOUNDARY, (unsigned long long)n_boundary);
+        if (n_recov) atomicAdd(a.counters + C_RECOV, (unsigned long long)n_recov);
+        if (n_killed) atomicAdd(a.counters + C_KILLED, (unsigned long long)n_killed);
+        if (max_iters) atomicMax(a.counters + C_SWEEPS, (unsigned long long)max_iters);
+        if (err) atomicOr(a.counters + C_ERR, 1ull);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// localization: uniform grid of element bounding boxes
+
+struct GridDev {
+    double org[3];
+    double cs[3];
+    int dims[3];
+    const int* cell_start;  // ncells + 1
+    const int* cand;        // element ids, ascending within a cell
+};
+
+__device__ __forceinline__ int grid_axis(double p, double org, double cs, int dim) {
+    double f = floor((p - org) / cs);
+    int i = (f < 0.0) ? 0 : (f >= (double)dim ? dim - 1 : (int)f);
+    return i;
+}
+
+__global__ void elem_cells_count_kernel(const ElemRec* __restrict__ rec,
+                                        const Vtx* __restrict__ vtx, int64_t ne, GridDev G,
+                                        int* __restrict__ counts, int4* __restrict__ ranges_lo,
+                                        int4* __restrict__ ranges_hi) {
+    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= ne) return;
+    const ElemRec r = rec[e];
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int j = 0; j < 4; ++j) {
+        const Vtx v = vtx[r.v[j]];
+        const double c[3] = {v.x, v.y, v.z};
+        for (int k = 0; k < 3; ++k) {
+            lo[k] = fmin(lo[k], c[k]);
+            hi[k] = fmax(hi[k], c[k]);
+        }
+    }
+    double ext = fmax(fmax(hi[0] - lo[0], hi[1] - lo[1]), hi[2] - lo[2]);
+    double delta = 1e-7 * ext + 1e-300;
+    int a[3], b[3];
+    for (int k = 0; k < 3; ++k) {
+        a[k] = grid_axis(lo[k] - delta, G.org[k], G.cs[k], G.dims[k]);
+        b[k] = grid_axis(hi[k] + delta, G.org[k], G.cs[k], G.dims[k]);
+    }
+    counts[e] = (b[0] - a[0] + 1) * (b[1] - a[1] + 1) * (b[2] - a[2] + 1);
+    ranges_lo[e] = make_int4(a[0], a[1], a[2], 0);
+    ranges_hi[e] = make_int4(b[0], b[1], b[2], 0);
+}
+
+__global__ void elem_cells_emit_kernel(int64_t ne, GridDev G, const int* __restrict__ offs,
+                                       const int4* __restrict__ ranges_lo,
+                                       const int4* __restrict__ ranges_hi,
+                                       unsigned long long* __restrict__ keys) {
+    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= ne) return;
+    const int4 a = ranges_lo[e], b = ranges_hi[e];
+    int k = offs[e];
+    for (int i = a.x; i <= b.x; ++i)
+        for (int j = a.y; j <= b.y; ++j)
+            for (int l = a.z; l <= b.z; ++l) {
+                const unsigned long long cell =
+                    ((unsigned long long)i * G.dims[1] + j) * G.dims[2] + l;
+                keys[k++] = (cell << 32) | (unsigned long long)e;
+            }
+}
+
+__global__ void cell_start_kernel(const unsigned long long* __restrict__ keys, int64_t m,
+                                  int64_t ncells, int* __restrict__ start,
+                                  int* __restrict__ cand) {
+    int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c < m) cand[c] = (int)(keys[c] & 0xffffffffull);
+    if (c > ncells) return;
+    // lower_bound of (c << 32)
+    const unsigned long long target = (unsigned long long)c << 32;
+    int64_t lo = 0, hi = m;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (keys[mid] < target) lo = mid + 1;
+        else hi = mid;
+    }
+    start[c] = (int)lo;
+}
+
+struct LocateArgs {
+    const ElemRec* __restrict__ rec;
+    const Vtx* __restrict__ vtx;
+    GridDev G;
+    const double* __restrict__ target;  // (count,3)
+    double* __restrict__ pos;
+    int32_t* __restrict__ element;
+    int8_t* __restrict__ alive;
+    int8_t* __restrict__ entry;
+    int8_t* __restrict__ stuck;
+    int8_t* __restrict__ outcome;
+    double* __restrict__ seg_total;
+    double bbox[6];
+    double c0[3];
+    int64_t count;
+};
+
+// One warp per particle: 32 candidates tested at a time; candidates are in
+// ascending element order, so the lowest set ballot bit is the lowest-id
+// containing element (pkg/tests/oracles.py:36-57 semantics).
+__global__ void __launch_bounds__(256) locate_grid_kernel(const LocateArgs a) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < a.count; i += nwarps) {
+        const double p0 = a.target[3 * i], p1 = a.target[3 * i + 1], p2 = a.target[3 * i + 2];
+        const bool inside = p0 >= a.bbox[0] && p0 <= a.bbox[3] && p1 >= a.bbox[1] &&
+                            p1 <= a.bbox[4] && p2 >= a.bbox[2] && p2 <= a.bbox[5];
+        int found = -1;
+        if (inside) {
+            const int ci = grid_axis(p0, a.G.org[0], a.G.cs[0], a.G.dims[0]);
+            const int cj = grid_axis(p1, a.G.org[1], a.G.cs[1], a.G.dims[1]);
+            const int ck = grid_axis(p2, a.G.org[2], a.G.cs[2], a.G.dims[2]);
+            const int64_t cell = ((int64_t)ci * a.G.dims[1] + cj) * a.G.dims[2] + ck;
+            const int s0 = a.G.cell_start[cell], s1 = a.G.cell_start[cell + 1];
+            for (int base = s0; base < s1 && found < 0; base += 32) {
+                bool ok = false;
+                int cand = -1;
+                if (base + lane < s1) {
+                    cand = a.G.cand[base + lane];
+                    const ElemRec r = load_rec(a.rec, cand);
+                    Tet T;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const Vtx v = a.vtx[r.v[j]];
+                        T.x[j] = v.x;
+                        T.y[j] = v.y;
+                        T.z[j] = v.z;
+                    }
+                    ok = contains(T, p0, p1, p2, EPS_BARY);
+                }
+                const unsigned hit = __ballot_sync(FULL, ok);
+                if (hit) found = __shfl_sync(FULL, cand, __ffs(hit) - 1);
+            }
+        }
+        if (lane == 0) {
+            a.element[i] = found;
+            a.alive[i] = found >= 0 ? 1 : 0;
+            if (found >= 0 || inside) {
+                a.pos[3 * i] = p0;
+                a.pos[3 * i + 1] = p1;
+                a.pos[3 * i + 2] = p2;
+            } else {  // outside the bbox: the reference leaves centroid 0
+                a.pos[3 * i] = a.c0[0];
+                a.pos[3 * i + 1] = a.c0[1];
+                a.pos[3 * i + 2] = a.c0[2];
+            }
+            a.entry[i] = -1;
+            a.stuck[i] = 0;
+            a.outcome[i] = found >= 0 ? OUT_REACHED : (inside ? OUT_LEAKED : OUT_NONE);
+            a.seg_total[i] = 0.0;
+        }
+    }
+}
+
+// walk-mode localization, step 1: search.py:577-591
+__global__ void init_walk_prep_kernel(LocateArgs a, int8_t* __restrict__ fly) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= a.count) return;
+    const double p0 = a.target[3 * i], p1 = a.target[3 * i + 1], p2 = a.target[3 * i + 2];
+    const bool inside = p0 >= a.bbox[0] && p0 <= a.bbox[3] && p1 >= a.bbox[1] &&
+                        p1 <= a.bbox[4] && p2 >= a.bbox[2] && p2 <= a.bbox[5];
+    a.pos[3 * i] = a.c0[0];
+    a.pos[3 * i + 1] = a.c0[1];
+    a.pos[3 * i + 2] = a.c0[2];
+    a.element[i] = inside ? 0 : -1;
+    a.alive[i] = inside ? 1 : 0;
+    fly[i] = inside ? 1 : 0;
+    a.entry[i] = -1;
+    a.stuck[i] = 0;
+    a.outcome[i] = OUT_NONE;
+    a.seg_total[i] = 0.0;
+}
+
+// walk-mode localization, step 2: lost reset + _tie_break_faces (search.py:595-600)
+__global__ void tiebreak_kernel(LocateArgs a) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= a.count) return;
+    const int8_t oc = a.outcome[i];
+    if (oc == OUT_LEAKED || oc == OUT_STUCK_KILLED) a.element[i] = -1;
+    if (a.alive[i] == 0 || a.element[i] < 0) return;
+    const double px = a.pos[3 * i], py = a.pos[3 * i + 1], pz = a.pos[3 * i + 2];
+    int e = a.element[i];
+    bool moved = true;
+    while (moved) {
+        moved = false;
+        const ElemRec r = load_rec(a.rec, e);
+        Tet T;
+        for (int j = 0; j < 4; ++j) {
+            const Vtx v = a.vtx[r.v[j]];
+            T.x[j] = v.x;
+            T.y[j] = v.y;
+            T.z[j] = v.z;
+        }
+        double l[4];
+        if (bary(T, px, py, pz, l) == 0.0) break;
+        for (int f = 0; f < 4; ++f) {
+            if (l[f] <= EPS_BARY) {
+                const int nbp = r.nb[f];
+                const int nb = nbp >> 2;
+                if (nbp >= 0 && nb < e) {
+                    const ElemRec rn = load_rec(a.rec, nb);
+                    Tet Tn;
+                    for (int j = 0; j < 4; ++j) {
+                        const Vtx v = a.vtx[rn.v[j]];
+                        Tn.x[j] = v.x;
+                        Tn.y[j] = v.y;
+                        Tn.z[j] = v.z;
+                    }
+                    if (contains(Tn, px, py, pz, EPS_BARY)) {
+                        e = nb;
+                        moved = true;
+                        break;
+                    }
+                }
+            }
+        }
+    }
+    a.element[i] = e;
+}
+
+// ---------------------------------------------------------------------------
+// move preparation: localization check (+ group range + source weight for
+// device-resident inputs)
+
+__global__ void prepare_kernel(const int8_t* __restrict__ fly, const int32_t* __restrict__ element,
+                               const int32_t* __restrict__ groups, int32_t ngroups,
+                               const double* __restrict__ weight, int64_t count,
+                               unsigned long long* __restrict__ flags,
+                               double* __restrict__ wsum) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    bool unloc = false, badg = false;
+    double wv = 0.0;
+    if (i < count) {
+        const bool f = fly[i] != 0;
+        unloc = f && element[i] < 0;
+        if (groups) badg = groups[i] < 0 || groups[i] >= ngroups;
+        if (wsum && f) wv = weight[i];
+    }
+    if (__any_sync(0xffffffffu, unloc) && (threadIdx.x & 31) == 0) atomicOr(flags, 1ull);
+    if (__any_sync(0xffffffffu, badg) && (threadIdx.x & 31) == 0) atomicOr(flags, 2ull);
+    if (wsum) {
+        for (int o = 16; o > 0; o >>= 1) wv += __shfl_xor_sync(0xffffffffu, wv, o);
+        if ((threadIdx.x & 31) == 0 && wv != 0.0) atomicAdd(wsum, wv);
+    }
+}
+
+__global__ void finalize_kernel(double* __restrict__ acc, double* __restrict__ sum,
+                                double* __restrict__ sum_sq, int64_t nbins, double w) {
+    int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= nbins) return;
+    const double x = __ddiv_rn(acc[b], w);
+    acc[b] = 0.0;
+    sum[b] = __dadd_rn(sum[b], x);
+    sum_sq[b] = __dadd_rn(sum_sq[b], __dmul_rn(x, x));
+}
+
+__global__ void iota_keys_kernel(const int32_t* __restrict__ element, int64_t count,
+                                 unsigned* __restrict__ keys, int32_t* __restrict__ vals) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    keys[i] = (unsigned)(element[i] + 1);
+    vals[i] = (int32_t)i;
+}
+
+// ---------------------------------------------------------------------------
+// handle
+
+struct bt_tally {
+    int dev = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+    int64_t nv = 0, ne = 0, cap = 0;
+    int32_t ngroups = 1;
+    double bbox[6];
+    double c0[3];
+    // mesh
+    ElemRec* rec = nullptr;
+    Vtx* vtx = nullptr;
+    // grid
+    GridDev grid{};
+    int* cell_start = nullptr;
+    int* cand = nullptr;
+    int64_t grid_m = 0;
+    // particles (persistent)
+    double* pos = nullptr;
+    int32_t* element = nullptr;
+    int8_t* alive = nullptr;
+    int8_t* entry = nullptr;
+    int8_t* stuck = nullptr;
+    int8_t* outcome = nullptr;
+    double* seg_total = nullptr;
+    int32_t* group = nullptr;
+    // per-move staging
+    double* dest = nullptr;
+    int8_t* fly = nullptr;
+    double* weight = nullptr;
+    uint64_t* digest = nullptr;
+    int64_t* dcount = nullptr;
+    // ordering
+    int32_t* order = nullptr;
+    unsigned* sort_keys_in = nullptr;
+    unsigned* sort_keys_out = nullptr;
+    int32_t* sort_vals_in = nullptr;
+    void* sort_tmp = nullptr;
+    size_t sort_tmp_bytes = 0;
+    // tallies
+    double* tally = nullptr;
+    double* sum = nullptr;
+    double* sum_sq = nullptr;
+    int64_t batches = 0;
+    double source_weight = 0.0;
+    // counters
+    unsigned long long* dcounters = nullptr;  // queue + counters + flags
+    double* dwsum = nullptr;
+    unsigned long long* hcounters = nullptr;  // pinned
+    // snapshot
+    double* snap_pos = nullptr;
+    int32_t* snap_element = nullptr;
+    int8_t* snap_flags = nullptr;  // alive, entry, stuck, outcome (4 x cap)
+    double* snap_seg = nullptr;
+    bool have_snapshot = false;
+    // options
+    int64_t max_sweeps = -1;
+    bool opt_digest = false;
+    bool opt_sort = false;
+    bool opt_wagg = true;
+    int blocks_per_sm = 0;
+    // timing
+    float walk_ms = 0.f, call_ms = 0.f;
+    int64_t kernels = 0;
+};
+
+static bt_status ensure_device(bt_tally* h) {
+    CK(cudaSetDevice(h->dev));
+    return BT_OK;
+}
+
+#define TRY(x)                         \
+    do {                               \
+        bt_status s__ = (x);           \
+        if (s__ != BT_OK) return s__;  \
+    } while (0)
+
+static bt_status free_all(bt_tally* h) {
+    void* ptrs[] = {h->rec, h->vtx, h->cell_start, h->cand, h->pos, h->element, h->alive,
+                    h->entry, h->stuck, h->outcome, h->seg_total, h->group, h->dest, h->fly,
+                    h->weight, h->digest, h->dcount, h->order, h->sort_keys_in,
+                    h->sort_keys_out, h->sort_vals_in, h->sort_tmp, h->tally, h->sum,
+                    h->sum_sq, h->dcounters, h->dwsum, h->snap_pos, h->snap_element,
+                    h->snap_flags, h->snap_seg};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (h->hcounters) cudaFreeHost(h->hcounters);
+    if (h->ev0) cudaEventDestroy(h->ev0);
+    if (h->ev1) cudaEventDestroy(h->ev1);
+    if (h->ev2) cudaEventDestroy(h->ev2);
+    if (h->ev3) cudaEventDestroy(h->ev3);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    return BT_OK;
+}
+
+template <typename T>
+static bt_status dalloc(T** p, int64_t n) {
+    CK(cudaMalloc((void**)p, sizeof(T) * (size_t)std::max<int64_t>(n, 1)));
+    return BT_OK;
+}
+
+static inline unsigned grid_for(int64_t n, int threads) {
+    return (unsigned)std::max<int64_t>(1, (n + threads - 1) / threads);
+}
+
+static bt_status build_grid(bt_tally* h) {
+    // cells ~ E/6 over the bounding box, per-axis counts proportional to extent
+    double ext[3];
+    double vol = 1.0;
+    for (int k = 0; k < 3; ++k) {
+        ext[k] = h->bbox[3 + k] - h->bbox[k];
+        if (!(ext[k] > 0.0)) ext[k] = 1e-300;
+    }
+    double maxext = std::max(ext[0], std::max(ext[1], ext[2]));
+    for (int k = 0; k < 3; ++k) vol *= std::max(ext[k], 1e-6 * maxext);
+    double target = std::max(1.0, (double)h->ne / 6.0);
+    target = std::min(target, (double)(1 << 26));
+    double cell = std::cbrt(vol / target);
+    GridDev G{};
+    int64_t ncells = 1;
+    for (int k = 0; k < 3; ++k) {
+        int d = (int)std::max(1.0, std::min(4096.0, std::round(ext[k] / cell)));
+        if (ext[k] <= 1e-300) d = 1;
+        G.dims[k] = d;
+        G.org[k] = h->bbox[k];
+        G.cs[k] = (ext[k] > 1e-300) ? ext[k] / d : 1.0;
+        ncells *= d;
+    }
+    int* counts = nullptr;
+    int* offs = nullptr;
+    int4 *rlo = nullptr, *rhi = nullptr;
+    TRY(dalloc(&counts, h->ne + 1));
+    TRY(dalloc(&offs, h->ne + 1));
+    TRY(dalloc(&rlo, h->ne));
+    TRY(dalloc(&rhi, h->ne));
+    CK(cudaMemsetAsync(counts + h->ne, 0, sizeof(int), h->stream));
+    elem_cells_count_kernel<<<grid_for(h->ne, 256), 256, 0, h->stream>>>(h->rec, h->vtx, h->ne,
+                                                                         G, counts, rlo, rhi);
+    CK(cudaGetLastError());
+    size_t tmp_bytes = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, offs, (int)(h->ne + 1),
+                                     h->stream));
+    void* tmp = nullptr;
+    CK(cudaMalloc(&tmp, tmp_bytes));
+    CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, offs, (int)(h->ne + 1), h->stream));
+    int m = 0;
+    CK(cudaMemcpyAsync(&m, offs + h->ne, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    cudaFree(tmp);
+    unsigned long long *keys = nullptr, *keys_out = nullptr;
+    TRY(dalloc(&keys, m));
+    TRY(dalloc(&keys_out, m));
+    elem_cells_emit_kernel<<<grid_for(h->ne, 256), 256, 0, h->stream>>>(h->ne, G, offs, rlo, rhi,
+                                                                        keys);
+    CK(cudaGetLastError());
+    int cell_bits = 1;
+    while ((1ll << cell_bits) < ncells + 1) ++cell_bits;
+    tmp_bytes = 0;
+    CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys, keys_out, m, 0, 32 + cell_bits,
+                                      h->stream));
+    CK(cudaMalloc(&tmp, tmp_bytes));
+    CK(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, keys, keys_out, m, 0, 32 + cell_bits,
+                                      h->stream));
+    TRY(dalloc(&h->cell_start, ncells + 1));
+    TRY(dalloc(&h->cand, m));
+    int64_t nthreads = std::max<int64_t>(m, ncells + 1);
+    cell_start_kernel<<<grid_for(nthreads, 256), 256, 0, h->stream>>>(keys_out, m, ncells,
+                                                                      h->cell_start, h->cand);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->stream));
+    cudaFree(tmp);
+    cudaFree(keys);
+    cudaFree(keys_out);
+    cudaFree(counts);
+    cudaFree(offs);
+    cudaFree(rlo);
+    cudaFree(rhi);
+    G.cell_start = h->cell_start;
+    G.cand = h->cand;
+    h->grid = G;
+    h->grid_m = m;
+    return BT_OK;
+}
+
+// numpy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src,
+// pairwise_sum_DOUBLE), so the recorded source weight equals the reference's
+// `weight[:count][flying].sum()` (tally.py:267-269) bit for bit.
+static double pairwise_sum(const double* a, int64_t n) {
+    if (n < 8) {
+        double res = -0.0;
+        for (int64_t i = 0; i < n; ++i) res += a[i];
+        return res;
+    } else if (n <= 128) {
+        double r[8];
+        for (int k = 0; k < 8; ++k) r[k] = a[k];
+        int64_t i;
+        for (i = 8; i < n - (n % 8); i += 8)
+            for (int k = 0; k < 8; ++k) r[k] += a[i + k];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; ++i) res += a[i];
+        return res;
+    } else {
+        int64_t n2 = n / 2;
+        n2 -= n2 % 8;
+        return pairwise_sum(a, n2) + pairwise_sum(a + n2, n - n2);
+    }
+}
+
+static bool is_device_ptr(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+extern "C" {
+
+const char* bt_last_error(void) { return g_err.c_str(); }
+const char* bt_version(void) { return "b200tally 0.1 (sm_100a)"; }
+
+bt_status bt_create(const double* vertices, int64_t num_vertices, const int32_t* elements,
+                    const int32_t* adj_elem, const int8_t* adj_face, int64_t num_elements,
+                    const double* bbox, const double* centroid0, int64_t num_particles,
+                    int32_t num_groups, int32_t device, bt_tally** out) {
+    if (!out) return set_err(BT_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (num_particles <= 0) return set_err(BT_EINVAL, "num_particles must be positive");
+    if (num_groups <= 0) return set_err(BT_EINVAL, "grid sizes must be positive");
+    if (num_elements <= 0) return set_err(BT_EINVAL, "grid sizes must be positive");
+    if (num_elements >= (1ll << 29)) return set_err(BT_EINVAL, "mesh too large (>= 2^29 tets)");
+    if (num_particles >= (1ll << 31)) return set_err(BT_EINVAL, "capacity must be < 2^31");
+    if (num_elements * (int64_t)num_groups >= (1ll << 40))
+        return set_err(BT_EINVAL, "tally too large");
+    if (!vertices || !elements || !adj_elem || !adj_face || !bbox || !centroid0)
+        return set_err(BT_EINVAL, "NULL mesh array");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev)
+        return set_err(BT_EINVAL, "device %d out of range (%d visible)", device, ndev);
+
+    bt_tally* h = new bt_tally();
+    h->dev = device;
+    h->nv = num_vertices;
+    h->ne = num_elements;
+    h->cap = num_particles;
+    h->ngroups = num_groups;
+    memcpy(h->bbox, bbox, sizeof h->bbox);
+    memcpy(h->c0, centroid0, sizeof h->c0);
+    auto fail = [&](bt_status s) {
+        std::string keep = g_err;
+        free_all(h);
+        delete h;
+        g_err = keep;
+        return s;
+    };
+    bt_status s = ensure_device(h);
+    if (s) return fail(s);
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return fail(set_err(BT_ECUDA, "cudaGetDeviceProperties"));
+    h->num_sms = prop.multiProcessorCount;
+#define CKF(call)                                                                        \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            return fail(set_err(e_ == cudaErrorMemoryAllocation ? BT_ENOMEM : BT_ECUDA,  \
+                                "%s failed: %s", #call, cudaGetErrorString(e_)));        \
+    } while (0)
+#define TRYF(x)                        \
+    do {                               \
+        bt_status s__ = (x);           \
+        if (s__ != BT_OK) return fail(s__); \
+    } while (0)
+    CKF(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    CKF(cudaEventCreate(&h->ev0));
+    CKF(cudaEventCreate(&h->ev1));
+    CKF(cudaEventCreate(&h->ev2));
+    CKF(cudaEventCreate(&h->ev3));
+
+    // ---- mesh records (host packing, one upload)
+    {
+        std::vector<ElemRec> hr((size_t)num_elements);
+        for (int64_t e = 0; e < num_elements; ++e) {
+            for (int j = 0; j < 4; ++j) {
+                const int v = elements[4 * e + j];
+                if (v < 0 || v >= num_vertices)
+                    return fail(set_err(BT_EINVAL, "element vertex id out of range"));
+                hr[e].v[j] = v;
+                const int nb = adj_elem[4 * e + j];
+                const int nf = adj_face[4 * e + j];
+                if (nb >= num_elements || (nb >= 0 && (nf < 0 || nf > 3)))
+                    return fail(set_err(BT_EINVAL, "adjacency out of range"));
+                hr[e].nb[j] = nb < 0 ? -1 : ((nb << 2) | nf);
+            }
+        }
+        std::vector<Vtx> hv((size_t)num_vertices);
+        for (int64_t v = 0; v < num_vertices; ++v)
+            hv[v] = Vtx{vertices[3 * v], vertices[3 * v + 1], vertices[3 * v + 2], 0.0};
+        TRYF(dalloc(&h->rec, num_elements));
+        TRYF(dalloc(&h->vtx, num_vertices));
+        CKF(cudaMemcpy(h->rec, hr.data(), sizeof(ElemRec) * hr.size(), cudaMemcpyHostToDevice));
+        CKF(cudaMemcpy(h->vtx, hv.data(), sizeof(Vtx) * hv.size(), cudaMemcpyHostToDevice));
+    }
+    // ---- particles / staging / tallies
+    const int64_t n = num_particles;
+    TRYF(dalloc(&h->pos, 3 * n));
+    TRYF(dalloc(&h->element, n));
+    TRYF(dalloc(&h->alive, n));
+    TRYF(dalloc(&h->entry, n));
+    TRYF(dalloc(&h->stuck, n));
+    TRYF(dalloc(&h->outcome, n));
+    TRYF(dalloc(&h->seg_total, n));
+    TRYF(dalloc(&h->group, n));
+    TRYF(dalloc(&h->dest, 3 * n));
+    TRYF(dalloc(&h->fly, n));
+    TRYF(dalloc(&h->weight, n));
+    const int64_t nbins = num_elements * num_groups;
+    TRYF(dalloc(&h->tally, nbins));
+    TRYF(dalloc(&h->sum, nbins));
+    TRYF(dalloc(&h->sum_sq, nbins));
+    TRYF(dalloc(&h->dcounters, 16));
+    TRYF(dalloc(&h->dwsum, 1));
+    CKF(cudaMallocHost((void**)&h->hcounters, 16 * sizeof(unsigned long long)));
+    CKF(cudaMemset(h->pos, 0, sizeof(double) * 3 * n));
+    CKF(cudaMemset(h->element, 0xff, sizeof(int32_t) * n));  // -1: unlocalized
+    CKF(cudaMemset(h->alive, 0, n));
+    CKF(cudaMemset(h->entry, 0xff, n));  // -1
+    CKF(cudaMemset(h->stuck, 0, n));
+    CKF(cudaMemset(h->outcome, 0, n));
+    CKF(cudaMemset(h->seg_total, 0, sizeof(double) * n));
+    CKF(cudaMemset(h->group, 0, sizeof(int32_t) * n));
+    CKF(cudaMemset(h->tally, 0, sizeof(double) * nbins));
+    CKF(cudaMemset(h->sum, 0, sizeof(double) * nbins));
+    CKF(cudaMemset(h->sum_sq, 0, sizeof(double) * nbins));
+    TRYF(build_grid(h));
+    CKF(cudaStreamSynchronize(h->stream));
+    *out = h;
+    return BT_OK;
+#undef CKF
+#undef TRYF
+}
+
+bt_status bt_destroy(bt_tally* h) {
+    if (!h) return BT_OK;
+    cudaSetDevice(h->dev);
+    cudaStreamSynchronize(h->stream);
+    free_all(h);
+    delete h;
+    return BT_OK;
+}
+
+bt_status bt_set_option(bt_tally* h, int32_t key, int64_t value) {
+    if (!h) return set_err(BT_EINVAL, "NULL handle");
+    switch (key) {
+        case BT_OPT_MAX_SWEEPS: h->max_sweeps = value; break;
+        case BT_OPT_DIGEST:
+            h->opt_digest = value != 0;
+            if (h->opt_digest && !h->digest) {
+                TRY(ensure_device(h));
+                TRY(dalloc(&h->digest, h->cap));
+                TRY(dalloc(&h->dcount, h->cap));
+                CK(cudaMemset(h->dcount, 0, sizeof(int64_t) * h->cap));
+            }
+            break;
+        case BT_OPT_SORT:
+            h->opt_sort = value != 0;
+            if (h->opt_sort && !h->order) {
+                TRY(ensure_device(h));
+                TRY(dalloc(&h->order, h->cap));
+                TRY(dalloc(&h->sort_keys_in, h->cap));
+                TRY(dalloc(&h->sort_keys_out, h->cap));
+                TRY(dalloc(&h->sort_vals_in, h->cap));
+                size_t b = 0;
+                CK(cub::DeviceRadixSort::SortPairs(nullptr, b, h->sort_keys_in, h->sort_keys_out,
+                                                   h->sort_vals_in, h->order, (int)h->cap));
+                CK(cudaMalloc(&h->sort_tmp, b));
+                h->sort_tmp_bytes = b;
+            }
+            break;
+        case BT_OPT_WARP_AGG: h->opt_wagg = value != 0; break;
+        case BT_OPT_BLOCKS_PER_SM: h->blocks_per_sm = (int)value; break;
+        default: return set_err(BT_EINVAL, "unknown option %d", key);
+    }
+    return BT_OK;
+}
+
+static bt_status run_walk(bt_tally* h, const double* dest, const int8_t* fly, const double* w,
+                          int64_t count, bool score, bt_summary* summary) {
+    WalkArgs a;
+    a.rec = h->rec;
+    a.vtx = h->vtx;
+    a.pos = h->pos;
+    a.dest = dest;
+    a.fly_in = fly;
+    a.weight = w;
+    a.group = h->group;
+    a.element = h->element;
+    a.alive = h->alive;
+    a.entry = h->entry;
+    a.stuck = h->stuck;
+    a.outcome = h->outcome;
+    a.seg_total = h->seg_total;
+    a.tally = h->tally;
+    const bool dig = h->opt_digest && score;
+    a.digest = dig ? h->digest : nullptr;
+    a.dcount = dig ? h->dcount : nullptr;
+    a.order = nullptr;
+    a.queue = h->dcounters;
+    a.counters = h->dcounters + 1;
+    a.count = count;
+    a.max_sweeps = h->max_sweeps >= 0 ? h->max_sweeps : 2 * h->ne + 1000;
+    a.ngroups = h->ngroups;
+    a.score = score ? 1 : 0;
+    CK(cudaMemsetAsync(h->dcounters, 0, sizeof(unsigned long long) * 16, h->stream));
+    if (dig) {
+        // particles not flying this move report zero events
+        CK(cudaMemsetAsync(h->dcount, 0, sizeof(int64_t) * count, h->stream));
+        h->kernels += 1;
+    }
+    if (h->opt_sort && score) {
+        iota_keys_kernel<<<grid_for(count, 256), 256, 0, h->stream>>>(
+            h->element, count, h->sort_keys_in, h->sort_vals_in);
+        CK(cudaGetLastError());
+        size_t b = h->sort_tmp_bytes;
+        CK(cub::DeviceRadixSort::SortPairs(h->sort_tmp, b, h->sort_keys_in, h->sort_keys_out,
+                                           h->sort_vals_in, h->order, (int)count, 0, 32,
+                                           h->stream));
+        a.order = h->order;
+        h->kernels += 5;
+    }
+    int bps = h->blocks_per_sm;
+    auto kern = dig ? (h->opt_wagg ? walk_kernel<true, true> : walk_kernel<true, false>)
+                    : (h->opt_wagg ? walk_kernel<false, true> : walk_kernel<false, false>);
+    if (bps <= 0) {
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WALK_THREADS, 0));
+        bps = std::max(1, occ);
+    }
+    const int64_t want = (count + WALK_THREADS - 1) / WALK_THREADS;
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)bps * h->num_sms));
+    CK(cudaEventRecord(h->ev0, h->stream));
+    kern<<<blocks, WALK_THREADS, 0, h->stream>>>(a);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(h->ev1, h->stream));
+    h->kernels += 1;
+    CK(cudaMemcpyAsync(h->hcounters, h->dcounters, sizeof(unsigned long long) * 16,
+                       cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    h->walk_ms += ms;
+    const unsigned long long* c = h->hcounters + 1;
+    if (summary) {
+        summary->sweeps = (int64_t)c[C_SWEEPS];
+        summary->events = (int64_t)c[C_EVENTS];
+        summary->reached = (int64_t)c[C_REACHED];
+        summary->boundary_exits = (int64_t)c[C_BOUNDARY];
+        summary->stuck_recoveries = (int64_t)c[C_RECOV];
+        summary->stuck_terminations = (int64_t)c[C_KILLED];
+    }
+    if (c[C_ERR])
+        return set_err(BT_ERUNTIME, "trace did not terminate within %lld sweeps",
+                       (long long)a.max_sweeps);
+    return BT_OK;
+}
+
+static LocateArgs locate_args(bt_tally* h, const double* target, int64_t count) {
+    LocateArgs a;
+    a.rec = h->rec;
+    a.vtx = h->vtx;
+    a.G = h->grid;
+    a.target = target;
+    a.pos = h->pos;
+    a.element = h->element;
+    a.alive = h->alive;
+    a.entry = h->entry;
+    a.stuck = h->stuck;
+    a.outcome = h->outcome;
+    a.seg_total = h->seg_total;
+    memcpy(a.bbox, h->bbox, sizeof a.bbox);
+    memcpy(a.c0, h->c0, sizeof a.c0);
+    a.count = count;
+    return a;
+}
+
+bt_status bt_initialize_particle_location(bt_tally* h, const double* positions, int64_t size,
+                                          int32_t mem_kind, int32_t mode, bt_summary* summary) {
+    if (!h) return set_err(BT_EINVAL, "NULL handle");
+    if (summary) memset(summary, 0, sizeof *summary);
+    if (size < 0 || size % 3 != 0)
+        return set_err(BT_EINVAL, "positions must hold 3*count floats, got %lld",
+                       (long long)size);
+    const int64_t count = size / 3;
+    if (count > h->cap)
+        return set_err(BT_EINVAL, "count %lld exceeds capacity %lld", (long long)count,
+                       (long long)h->cap);
+    if (mode != BT_LOCATE_GRID && mode != BT_LOCATE_WALK)
+        return set_err(BT_EINVAL, "unknown localization mode %d", mode);
+    TRY(ensure_device(h));
+    h->walk_ms = 0.f;
+    h->kernels = 0;
+    h->source_weight = 0.0;
+    if (count == 0) return BT_OK;
+    if (!positions) return set_err(BT_EINVAL, "positions is NULL");
+    CK(cudaEventRecord(h->ev2, h->stream));
+    const double* target = positions;
+    if (mem_kind == BT_MEM_HOST) {
+        CK(cudaMemcpyAsync(h->dest, positions, sizeof(double) * 3 * count,
+                           cudaMemcpyHostToDevice, h->stream));
+        target = h->dest;
+    }
+    LocateArgs la = locate_args(h, target, count);
+    if (mode == BT_LOCATE_GRID) {
+        const int64_t blocks = std::min<int64_t>((count + 7) / 8, (int64_t)h->num_sms * 64);
+        locate_grid_kernel<<<(unsigned)blocks, 256, 0, h->stream>>>(la);
+        CK(cudaGetLastError());
+        h->kernels += 1;
+    } else {
+        init_walk_prep_kernel<<<grid_for(count, 256), 256, 0, h->stream>>>(la, h->fly);
+        CK(cudaGetLastError());
+        h->kernels += 1;
+        TRY(run_walk(h, target, h->fly, nullptr, count, false, summary));
+        tiebreak_kernel<<<grid_for(count, 128), 128, 0, h->stream>>>(la);
+        CK(cudaGetLastError());
+        h->kernels += 1;
+    }
+    CK(cudaEventRecord(h->ev3, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    CK(cudaEventElapsedTime(&h->call_ms, h->ev2, h->ev3));
+    return BT_OK;
+}
+
+bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, const int8_t* flying,
+                                   const double* weights, const int32_t* groups, int64_t size,
+                                   int32_t mem_kind, bt_summary* summary) {
+    if (!h) return set_err(BT_EINVAL, "NULL handle");
+    if (summary) memset(summary, 0, sizeof *summary);
+    const int64_t count = size;
+    if (count < 0 || count > h->cap)
+        return set_err(BT_EINVAL, "count %lld outside [0, %lld]", (long long)count,
+                       (long long)h->cap);
+    TRY(ensure_device(h));
+    h->walk_ms = 0.f;
+    h->kernels = 0;
+    if (count == 0) return BT_OK;
+    if (!destinations || !flying || !weights)
+        return set_err(BT_EINVAL, "NULL move array");
+    const bool host = mem_kind == BT_MEM_HOST;
+    // host-side checks and the recorded source weight (tally.py:262-269)
+    bool need_w = h->source_weight == 0.0;
+    double hw = 0.0;
+    if (host) {
+        if (groups) {
+            for (int64_t i = 0; i < count; ++i)
+                if (groups[i] < 0 || groups[i] >= h->ngroups)
+                    return set_err(BT_EINDEX, "group %d out of range [0, %d)", groups[i],
+                                   h->ngroups);
+        }
+        if (need_w) {
+            std::vector<double> sel;
+            sel.reserve((size_t)count);
+            for (int64_t i = 0; i < count; ++i)
+                if (flying[i] != 0) sel.push_back(weights[i]);
+            hw = pairwise_sum(sel.data(), (int64_t)sel.size());
+        }
+    }
+    CK(cudaEventRecord(h->ev2, h->stream));
+    const double* d_dest = destinations;
+    const int8_t* d_fly = flying;
+    const double* d_w = weights;
+    if (host) {
+        CK(cudaMemcpyAsync(h->dest, destinations, sizeof(double) * 3 * count,
+                           cudaMemcpyHostToDevice, h->stream));
+        CK(cudaMemcpyAsync(h->fly, flying, count, cudaMemcpyHostToDevice, h->stream));
+        CK(cudaMemcpyAsync(h->weight, weights, sizeof(double) * count, cudaMemcpyHostToDevice,
+                           h->stream));
+        d_dest = h->dest;
+        d_fly = h->fly;
+        d_w = h->weight;
+    }
+    const int32_t* d_groups_in = nullptr;
+    if (groups) {
+        CK(cudaMemcpyAsync(h->group, groups, sizeof(int32_t) * count,
+                           host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, h->stream));
+        if (!host) d_groups_in = h->group;
+    }
+    // device-side checks: unlocalized flying particles (+ groups, weight sum)
+    CK(cudaMemsetAsync(h->dcounters + 15, 0, sizeof(unsigned long long), h->stream));
+    const bool dev_w = !host && need_w;
+    if (dev_w) CK(cudaMemsetAsync(h->dwsum, 0, sizeof(double), h->stream));
+    prepare_kernel<<<grid_for(count, 256), 256, 0, h->stream>>>(
+        d_fly, h->element, d_groups_in, h->ngroups, d_w, count, h->dcounters + 15,
+        dev_w ? h->dwsum : nullptr);
+    CK(cudaGetLastError());
+    h->kernels += 1;
+    unsigned long long flags = 0;
+    double dw = 0.0;
+    CK(cudaMemcpyAsync(&flags, h->dcounters + 15, sizeof flags, cudaMemcpyDeviceToHost,
+                       h->stream));
+    if (dev_w) CK(cudaMemcpyAsync(&dw, h->dwsum, sizeof dw, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (flags & 2ull) return set_err(BT_EINDEX, "group out of range [0, %d)", h->ngroups);
+    if (flags & 1ull)
+        return set_err(BT_EINVAL,
+                       "a flying particle is not localized (element = -1); call "
+                       "initialize_particle_location first");
+    if (need_w) h->source_weight = host ? hw : dw;
+    bt_status s = run_walk(h, d_dest, d_fly, d_w, count, true, summary);
+    CK(cudaEventRecord(h->ev3, h->stream));
+    CK(cudaEventSynchronize(h->ev3));
+    CK(cudaEventElapsedTime(&h->call_ms, h->ev2, h->ev3));
+    return s;
+}
+
+bt_status bt_finalize_batch(bt_tally* h, double source_weight) {
+    if (!h) return set_err(BT_EINVAL, "NULL handle");
+    double w = source_weight > 0.0 ? source_weight : h->source_weight;
+    if (!(w > 0.0))
+        return set_err(BT_ERUNTIME, "no source weight recorded for this batch; pass source_weight");
+    TRY(ensure_device(h));
+    const int64_t nb = h->ne * h->ngroups;
+    finalize_kernel<<<grid_for(nb, 256), 256, 0, h->stream>>>(h->tally, h->sum, h->sum_sq, nb, w);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->stream));
+    h->batches += 1;
+    h->source_weight = 0.0;
+    return BT_OK;
+}
+
+static double* tally_ptr(bt_tally* h, int32_t which) {
+    switch (which) {
+        case BT_TALLY_BATCH: return h->tally;
+        case BT_TALLY_SUM: return h->sum;
+        case BT_TALLY_SUM_SQ: return h->sum_sq;
+        default: return nullptr;
+    }
+}
+
+bt_status bt_read_tally(bt_tally* h, int32_t which, double* out, int64_t n) {
+    if (!h) return set_err(BT_EINVAL, "NULL handle");
+    double* p = tally_ptr(h, which);
+    if (!p) return set_err(BT_EINVAL, "unknown tally array %d", which);
+    if (n != h->ne * h->ngroups) return set_err(BT_EINVAL, "n must be E*G");
+    TRY(ensure_device(h));
+    CK(cudaMemcpyAsync(out, p, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return BT_OK;
+}
+
+bt_status bt_tally_device_ptr(bt_tally* h, int32_t which, void** ptr) {
+    if (!h || !ptr) return set_err(BT_EINVAL, "NULL argument");
+    double* p = tally_ptr(h, which);
+    if (!p) return set_err(BT_EINVAL, "unknown tally array %d", which);
+    *ptr = p;
+    return BT_OK;
+}
+
+bt_status bt_get_source_weight(bt_tally* h, double* w) {
+    if (!h || !w) return set_err(BT_EINVAL, "NULL argument");
+    *w = h->source_weight;
+    return BT_OK;
+}
+
+bt_status bt_set_source_weight(bt_tally* h, double w) {
+    if (!h) return set_err(BT_EINVAL, "NULL handle");
+    h->source_weight = w;
+    return BT_OK;
+}
+
+bt_status bt_batches_completed(bt_tally* h, int64_t* n) {
+    if (!h || !n) return set_err(BT_EINVAL, "NULL argument");
+    *n = h->batches;
+    return BT_OK;
+}
+
+bt_status bt_read_particles(bt_tally* h, int64_t count, double* position, int32_t* element,
+                            int8_t* alive, int8_t* entry_face, int8_t* stuck, int8_t* outcome,
+                            double* seg_total) {
+    if (!h) return set_err(BT_EINVAL, "NULL handle");
+    if (count < 0 || count > h->cap) return set_err(BT_EINVAL, "count out of range");
+    TRY(ensure_device(h));
+    auto cp = [&](void* dst, const void* src, size_t bytes) -> bt_status {
+        if (dst && bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, h->stream));
+        return BT_OK;
+    };
+    TRY(cp(position, h->pos, sizeof(double) * 3 * count));
+    TRY(cp(element, h->element, sizeof(int32_t) * count));
+    TRY(cp(alive, h->alive, count));
+    TRY(cp(entry_face, h->entry, count));
+    TRY(cp(stuck, h->stuck, count));
+    TRY(cp(outcome, h->outcome, count));
+    TRY(cp(seg_total, h->seg_total, sizeof(double) * count));
+    CK(cudaStreamSynchronize(h->stream));
+    return BT_OK;
+}
+
+bt_status bt_read_digest(bt_tally* h, int64_t count, uint64_t* digest, int64_t* events) {
+    if (!h) return set_err(BT_EINVAL, "NULL handle");
+    if (!h->digest) return set_err(BT_EINVAL, "digests are off (BT_OPT_DIGEST)");
+    if (count < 0 || count > h->cap) return set_err(BT_EINVAL, "count out of range");
+    TRY(ensure_device(h));
+    if (digest)
+        CK(cudaMemcpyAsync(digest, h->digest, sizeof(uint64_t) * count, cudaMemcpyDeviceToHost,
+                           h->stream));
+    if (events)
+        CK(cudaMemcpyAsync(events, h->dcount, sizeof(int64_t) * count, cudaMemcpyDeviceToHost,
+                           h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return BT_OK;
+}
+
+bt_status bt_last_timing(bt_tally* h, float* walk_ms, float* call_ms, int64_t* kernels) {
+    if (!h) return set_err(BT_EINVAL, "NULL handle");
+    if (walk_ms) *walk_ms = h->walk_ms;
+    if (call_ms) *call_ms = h->call_ms;
+    if (kernels) *kernels = h->kernels;
+    return BT_OK;
+}
+
+bt_status bt_save_state(bt_tally* h) {
+    if (!h) return set_err(BT_EINVAL, "NULL handle");
+    TRY(ensure_device(h));
+    const int64_t n = h->cap;
+    if (!h->snap_pos) {
+        TRY(dalloc(&h->snap_pos, 3 * n));
+        TRY(dalloc(&h->snap_element, n));
+        TRY(dalloc(&h->snap_flags, 4 * n));
+        TRY(dalloc(&h->snap_seg, n));
+    }
+    auto d2d = cudaMemcpyDeviceToDevice;
+    CK(cudaMemcpyAsync(h->snap_pos, h->pos, sizeof(double) * 3 * n, d2d, h->stream));
+    CK(cudaMemcpyAsync(h->snap_element, h->element, sizeof(int32_t) * n, d2d, h->stream));
+    CK(cudaMemcpyAsync(h->snap_flags, h->alive, n, d2d, h->stream));
+    CK(cudaMemcpyAsync(h->snap_flags + n, h->entry, n, d2d, h->stream));
+    CK(cudaMemcpyAsync(h->snap_flags + 2 * n, h->stuck, n, d2d, h->stream));
+    CK(cudaMemcpyAsync(h->snap_flags + 3 * n, h->outcome, n, d2d, h->stream));
+    CK(cudaMemcpyAsync(h->snap_seg, h->seg_total, sizeof(double) * n, d2d, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    h->have_snapshot = true;
+    return BT_OK;
+}
+
+bt_status bt_restore_state(bt_tally* h) {
+    if (!h) return set_err(BT_EINVAL, "NULL handle");
+    if (!h->have_snapshot) return set_err(BT_EINVAL, "no snapshot saved");
+    TRY(ensure_device(h));
+    const int64_t n = h->cap;
+    auto d2d = cudaMemcpyDeviceToDevice;
+    CK(cudaMemcpyAsync(h->pos, h->snap_pos, sizeof(double) * 3 * n, d2d, h->stream));
+    CK(cudaMemcpyAsync(h->element, h->snap_element, sizeof(int32_t) * n, d2d, h->stream));
+    CK(cudaMemcpyAsync(h->alive, h->snap_flags, n, d2d, h->stream));
+    CK(cudaMemcpyAsync(h->entry, h->snap_flags + n, n, d2d, h->stream));
+    CK(cudaMemcpyAsync(h->stuck, h->snap_flags + 2 * n, n, d2d, h->stream));
+    CK(cudaMemcpyAsync(h->outcome, h->snap_flags + 3 * n, n, d2d, h->stream));
+    CK(cudaMemcpyAsync(h->seg_total, h->snap_seg, sizeof(double) * n, d2d, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return BT_OK;
+}
+
+bt_status bt_info(bt_tally* h, int32_t* device, int64_t* num_elements, int64_t* capacity,
+                  int32_t* num_groups) {
+    if (!h) return set_err(BT_EINVAL, "NULL handle");
+    if (device) *device = h->dev;
+    if (num_elements) *num_elements = h->ne;
+    if (capacity) *capacity = h->cap;
+    if (num_groups) *num_groups = h->ngroups;
+    return BT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,429 @@
+"""Drop-in ``MeshTally`` facade over the CUDA library (C ABI, ctypes).
+
+Mirrors the reference's tally API (meshtally/tally.py):
+
+* ``MeshTally(mesh, num_particles, num_groups=1, threads=1)`` -- tally.py:211-229
+* ``.initialize_particle_location(positions)``                 -- tally.py:239-245
+* ``.move_to_next_location(destinations, flying, weights, groups=None)``
+  -> ``TraceSummary | None``                                    -- tally.py:247-271
+* ``.finalize_batch(source_weight=None)``                       -- tally.py:273-279
+* ``.flux() -> FluxResult``, ``.write(filename)``, ``.mesh``, ``.grid``
+* module functions ``batch_totals``, ``finalize_batch``, ``flux`` over a grid
+  view (tally.py:101-152) and the VTK/CSV writers (tally.py:159-200).
+
+Arguments accept host arrays (anything ``numpy.asarray`` takes, converted
+exactly as the reference converts them) or CUDA tensors that expose
+``data_ptr()`` and live on the handle's GPU (zero-copy).
+
+Documented deviations from the reference:
+
+* ``threads`` is accepted and ignored (there are no CPU slabs; the
+  reference's slab/thread mismatch bug, cannot occur).
+* ``groups`` values outside ``[0, num_groups)`` raise ``IndexError`` instead
+  of silently scoring into another element's bin (tally.py:262-266).
+* A flying particle with ``element == -1`` raises ``ValueError`` before any
+  work (the reference's fused path reads element -1 with numba wraparound).
+* Localization defaults to the grid search (``localize="grid"``): it returns
+  the lowest-id element containing the point (pkg/tests/oracles.py:36-57),
+  which equals the reference's centroid-0 walk + tie-break on every generic
+  point and also finds the points that walk loses.
+  ``localize="walk"`` reproduces the reference bit for bit, losses included.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+from . import _lib
+from .mesh import TetMesh, read_tetmesh
+
+OUTCOME_NONE, OUTCOME_REACHED, OUTCOME_LEAKED, OUTCOME_STUCK_KILLED = 0, 1, 2, 3
+
+
+@dataclass(frozen=True)
+class TraceSummary:
+    """search.py:150-157."""
+
+    sweeps: int
+    events: int
+    reached: int
+    boundary_exits: int
+    stuck_recoveries: int
+    stuck_terminations: int
+
+    @classmethod
+    def _from(cls, s: _lib.Summary) -> "TraceSummary":
+        return cls(int(s.sweeps), int(s.events), int(s.reached), int(s.boundary_exits),
+                   int(s.stuck_recoveries), int(s.stuck_terminations))
+
+
+@dataclass(frozen=True)
+class FluxResult:
+    """tally.py:115-120."""
+
+    mean: np.ndarray       # (E, G)
+    rel_error: np.ndarray  # (E, G)
+
+
+@dataclass(frozen=True)
+class ParticleState:
+    position: np.ndarray
+    element: np.ndarray
+    alive: np.ndarray
+    entry_face: np.ndarray
+    stuck: np.ndarray
+    outcome: np.ndarray
+    seg_total: np.ndarray
+
+
+def _is_device(x) -> bool:
+    return hasattr(x, "data_ptr") and getattr(x, "is_cuda", False)
+
+
+class TallyGrid:
+    """Read-through view of the device tally (tally.py:21-44 field names)."""
+
+    def __init__(self, owner: "MeshTally"):
+        self._owner = owner
+        self.num_elements = owner.mesh.num_elements
+        self.num_groups = owner.num_groups
+
+    def _read(self, which):
+        return self._owner._read_tally(which)
+
+    @property
+    def partials(self) -> np.ndarray:
+        return self._read(_lib.BT_TALLY_BATCH)[None, :]
+
+    @property
+    def batch_accum(self) -> np.ndarray:
+        return np.zeros(self.num_elements * self.num_groups)
+
+    @property
+    def sum(self) -> np.ndarray:
+        return self._read(_lib.BT_TALLY_SUM)
+
+    @property
+    def sum_sq(self) -> np.ndarray:
+        return self._read(_lib.BT_TALLY_SUM_SQ)
+
+    @property
+    def batches_completed(self) -> int:
+        return self._owner.batches_completed
+
+
+def batch_totals(grid: TallyGrid) -> np.ndarray:
+    """tally.py:101-104."""
+    return grid.partials.sum(axis=0).reshape(grid.num_elements, grid.num_groups)
+
+
+def finalize_batch(grid: TallyGrid, batch_source_weight: float) -> None:
+    """tally.py:107-112."""
+    if not batch_source_weight > 0.0:
+        raise ValueError(
+            f"batch_source_weight must be positive, got {batch_source_weight!r}")
+    grid._owner.finalize_batch(float(batch_source_weight))
+
+
+def flux(grid: TallyGrid, volumes) -> FluxResult:
+    """tally.py:123-152 (same formula, evaluated on the read-back moments)."""
+    n = grid.batches_completed
+    if n == 0:
+        raise RuntimeError("no batches completed; nothing to normalize")
+    volumes = np.asarray(volumes, dtype=np.float64)
+    if volumes.shape != (grid.num_elements,):
+        raise ValueError(f"volumes must be ({grid.num_elements},), got {volumes.shape}")
+    if not (volumes > 0.0).all():
+        raise ValueError("volumes must be positive")
+    shape = (grid.num_elements, grid.num_groups)
+    s = grid.sum.reshape(shape)
+    sq = grid.sum_sq.reshape(shape)
+    batch_mean = s / n
+    mean = batch_mean / volumes[:, None]
+    rel = np.zeros(shape)
+    if n >= 2:
+        var = (sq - s * s / n) / (n - 1)
+        np.clip(var, 0.0, None, out=var)
+        se = np.sqrt(var / n)
+        nz = batch_mean > 0.0
+        rel[nz] = se[nz] / batch_mean[nz]
+    return FluxResult(mean=mean, rel_error=rel)
+
+
+def _fmt(v: float) -> str:
+    return repr(float(v))
+
+
+def write_vtk(mesh, flux_result: FluxResult, filename) -> None:
+    """Legacy ASCII VTK unstructured grid, one flux and one rel_error cell
+    field per group (tally.py:159-189 file layout)."""
+    mean = np.atleast_2d(flux_result.mean)
+    rel = np.atleast_2d(flux_result.rel_error)
+    if mean.shape[0] != mesh.num_elements:
+        raise ValueError(f"flux has {mean.shape[0]} elements, mesh has {mesh.num_elements}")
+    ne, nv = mesh.num_elements, mesh.num_vertices
+    with open(filename, "w") as fh:
+        fh.write("# vtk DataFile Version 3.0\ntetrahedral mesh flux tally\nASCII\n"
+                 "DATASET UNSTRUCTURED_GRID\n")
+        fh.write(f"POINTS {nv} double\n")
+        fh.writelines(f"{_fmt(x)} {_fmt(y)} {_fmt(z)}\n" for x, y, z in mesh.vertices.tolist())
+        fh.write(f"CELLS {ne} {5 * ne}\n")
+        fh.writelines(f"4 {a} {b} {c} {d}\n" for a, b, c, d in mesh.elements.tolist())
+        fh.write(f"CELL_TYPES {ne}\n")
+        fh.write("10\n" * ne)
+        fh.write(f"CELL_DATA {ne}\n")
+        for g in range(mean.shape[1]):
+            fh.write(f"SCALARS flux_g{g} double 1\nLOOKUP_TABLE default\n")
+            fh.writelines(_fmt(x) + "\n" for x in mean[:, g].tolist())
+            fh.write(f"SCALARS rel_error_g{g} double 1\nLOOKUP_TABLE default\n")
+            fh.writelines(_fmt(x) + "\n" for x in rel[:, g].tolist())
+
+
+def write_flux_csv(flux_result: FluxResult, filename) -> None:
+    """tally.py:192-200 row layout."""
+    mean = np.atleast_2d(flux_result.mean)
+    rel = np.atleast_2d(flux_result.rel_error)
+    with open(filename, "w") as fh:
+        fh.write("element,group,mean,rel_error\n")
+        for e in range(mean.shape[0]):
+            for g in range(mean.shape[1]):
+                fh.write(f"{e},{g},{_fmt(mean[e, g])},{_fmt(rel[e, g])}\n")
+
+
+class MeshTally:
+    """Batched track-length tally on a tet mesh, computed on one B200."""
+
+    def __init__(self, mesh, num_particles: int, num_groups: int = 1, threads: int = 1, *,
+                 device: int = 0, localize: str = "grid", digest: bool = False,
+                 sort: bool = False, warp_aggregate: bool = True):
+        if isinstance(mesh, (str, Path)):
+            mesh = read_tetmesh(mesh)
+        if not all(hasattr(mesh, a) for a in ("vertices", "elements", "adj_elem", "adj_face",
+                                              "volumes", "centroids", "bounding_box")):
+            raise TypeError("mesh must be a TetMesh or a path to one")
+        if int(num_particles) <= 0:
+            raise ValueError("num_particles must be positive")
+        if int(num_groups) <= 0:
+            raise ValueError(f"grid sizes must be positive, got ({mesh.num_elements}, "
+                             f"{num_groups})")
+        if localize not in ("grid", "walk"):
+            raise ValueError("localize must be 'grid' or 'walk'")
+        self._mesh = mesh
+        self.threads = max(1, int(threads))  # accepted for API compatibility
+        self.num_groups = int(num_groups)
+        self.capacity = int(num_particles)
+        self.device = int(device)
+        self.localize = localize
+        self._count = 0
+        L = _lib.load()
+        v = np.ascontiguousarray(mesh.vertices, dtype=np.float64)
+        e = np.ascontiguousarray(mesh.elements, dtype=np.int32)
+        ae = np.ascontiguousarray(mesh.adj_elem, dtype=np.int32)
+        af = np.ascontiguousarray(mesh.adj_face, dtype=np.int8)
+        bbox = np.ascontiguousarray(mesh.bounding_box, dtype=np.float64)
+        c0 = np.ascontiguousarray(mesh.centroids[0], dtype=np.float64)
+        h = C.c_void_p()
+        _lib.check(L.bt_create(v.ctypes.data, v.shape[0], e.ctypes.data, ae.ctypes.data,
+                               af.ctypes.data, e.shape[0], bbox.ctypes.data, c0.ctypes.data,
+                               self.capacity, self.num_groups, self.device, C.byref(h)))
+        self._h = h
+        self._L = L
+        self.set_option(_lib.BT_OPT_DIGEST, int(digest))
+        self.set_option(_lib.BT_OPT_SORT, int(sort))
+        self.set_option(_lib.BT_OPT_WARP_AGG, int(warp_aggregate))
+        self._grid = TallyGrid(self)
+
+    # ------------------------------------------------------------------ props
+    @property
+    def mesh(self) -> TetMesh:
+        return self._mesh
+
+    @property
+    def grid(self) -> TallyGrid:
+        return self._grid
+
+    @property
+    def batches_completed(self) -> int:
+        n = C.c_int64()
+        _lib.check(self._L.bt_batches_completed(self._h, C.byref(n)))
+        return int(n.value)
+
+    @property
+    def source_weight(self) -> float:
+        w = C.c_double()
+        _lib.check(self._L.bt_get_source_weight(self._h, C.byref(w)))
+        return float(w.value)
+
+    @source_weight.setter
+    def source_weight(self, w: float) -> None:
+        _lib.check(self._L.bt_set_source_weight(self._h, float(w)))
+
+    def set_option(self, key: int, value: int) -> None:
+        _lib.check(self._L.bt_set_option(self._h, int(key), int(value)))
+
+    # ------------------------------------------------------------------ API
+    def initialize_particle_location(self, positions, *, mode: str | None = None) -> None:
+        """tally.py:239-245; `mode` overrides the constructor's `localize`."""
+        mode = self.localize if mode is None else mode
+        m = _lib.BT_LOCATE_WALK if mode == "walk" else _lib.BT_LOCATE_GRID
+        s = _lib.Summary()
+        if _is_device(positions):
+            self._check_tensor(positions, 8)
+            size = positions.numel()
+            _lib.check(self._L.bt_initialize_particle_location(
+                self._h, positions.data_ptr(), size, _lib.BT_MEM_DEVICE, m, C.byref(s)))
+        else:
+            pos = np.ascontiguousarray(np.asarray(positions, dtype=np.float64).reshape(-1))
+            size = pos.size
+            count = size // 3
+            if count > self.capacity:
+                raise ValueError(f"count {count} exceeds capacity {self.capacity}")
+            if size != 3 * count:
+                raise ValueError(f"positions must hold 3*count = {3 * count} floats, "
+                                 f"got {size}")
+            _lib.check(self._L.bt_initialize_particle_location(
+                self._h, pos.ctypes.data, size, _lib.BT_MEM_HOST, m, C.byref(s)))
+        self._count = size // 3
+        self.last_init_summary = TraceSummary._from(s)
+
+    def move_to_next_location(self, destinations, flying, weights, groups=None):
+        """tally.py:247-271. Returns TraceSummary, or None when count == 0."""
+        s = _lib.Summary()
+        if _is_device(flying):
+            count = flying.numel()
+            for t, isz in ((destinations, 8), (flying, 1), (weights, 8)):
+                self._check_tensor(t, isz)
+            if destinations.numel() != 3 * count or weights.numel() != count:
+                raise ValueError(
+                    f"array sizes ({destinations.numel()}, {count}, {weights.numel()}) do not "
+                    f"match count {count} (need 3*count, count, count)")
+            if count > self.capacity:
+                raise ValueError(f"count {count} outside [0, {self.capacity}]")
+            gp = None
+            if groups is not None:
+                self._check_tensor(groups, 4)
+                if groups.numel() != count:
+                    raise ValueError("groups size mismatch")
+                gp = groups.data_ptr()
+            if count == 0:
+                return None
+            _lib.check(self._L.bt_move_to_next_location(
+                self._h, destinations.data_ptr(), flying.data_ptr(), weights.data_ptr(), gp,
+                count, _lib.BT_MEM_DEVICE, C.byref(s)))
+            return TraceSummary._from(s)
+        fly = np.ascontiguousarray(np.asarray(flying).reshape(-1).astype(np.int8, copy=False))
+        count = fly.size
+        dest = np.ascontiguousarray(np.asarray(destinations, dtype=np.float64).reshape(-1))
+        w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64).reshape(-1))
+        if count > self.capacity:
+            raise ValueError(f"count {count} outside [0, {self.capacity}]")
+        if dest.size != 3 * count or w.size != count:
+            raise ValueError(
+                f"array sizes ({dest.size}, {fly.size}, {w.size}) do not match "
+                f"count {count} (need 3*count, count, count)")
+        if count == 0:
+            return None
+        gp = None
+        if groups is not None:
+            g = np.ascontiguousarray(np.asarray(groups, dtype=np.int32).reshape(-1))
+            if g.size != count:
+                raise ValueError("groups size mismatch")
+            gp = g.ctypes.data
+        _lib.check(self._L.bt_move_to_next_location(
+            self._h, dest.ctypes.data, fly.ctypes.data, w.ctypes.data, gp, count,
+            _lib.BT_MEM_HOST, C.byref(s)))
+        return TraceSummary._from(s)
+
+    def finalize_batch(self, source_weight: float | None = None) -> None:
+        """tally.py:273-279."""
+        w = self.source_weight if source_weight is None else source_weight
+        if not w or w <= 0.0:
+            raise RuntimeError("no source weight recorded for this batch; pass source_weight")
+        _lib.check(self._L.bt_finalize_batch(self._h, float(w)))
+
+    def flux(self) -> FluxResult:
+        return flux(self._grid, self._mesh.volumes)
+
+    def write(self, filename) -> None:
+        write_vtk(self._mesh, self.flux(), filename)
+
+    # ------------------------------------------------------------------ extras
+    def _check_tensor(self, t, itemsize):
+        if not t.is_contiguous():
+            raise ValueError("device arrays must be contiguous")
+        if t.element_size() != itemsize:
+            raise ValueError(f"device array has element size {t.element_size()}, "
+                             f"expected {itemsize}")
+        if t.device.index is not None and t.device.index != self.device:
+            raise ValueError(f"tensor on cuda:{t.device.index}, handle on cuda:{self.device}")
+
+    def _read_tally(self, which) -> np.ndarray:
+        n = self._mesh.num_elements * self.num_groups
+        out = np.empty(n)
+        _lib.check(self._L.bt_read_tally(self._h, which, out.ctypes.data, n))
+        return out
+
+    def batch_totals(self) -> np.ndarray:
+        return batch_totals(self._grid)
+
+    def tally_device_ptr(self, which=_lib.BT_TALLY_BATCH) -> int:
+        p = C.c_void_p()
+        _lib.check(self._L.bt_tally_device_ptr(self._h, which, C.byref(p)))
+        return int(p.value)
+
+    def read_particles(self, count: int | None = None) -> ParticleState:
+        n = self._count if count is None else int(count)
+        pos = np.empty((n, 3))
+        el = np.empty(n, np.int32)
+        al = np.empty(n, np.int8)
+        ef = np.empty(n, np.int8)
+        st = np.empty(n, np.int8)
+        oc = np.empty(n, np.int8)
+        sg = np.empty(n)
+        _lib.check(self._L.bt_read_particles(self._h, n, pos.ctypes.data, el.ctypes.data,
+                                             al.ctypes.data, ef.ctypes.data, st.ctypes.data,
+                                             oc.ctypes.data, sg.ctypes.data))
+        return ParticleState(pos, el, al, ef, st, oc, sg)
+
+    def read_digest(self, count: int | None = None):
+        n = self._count if count is None else int(count)
+        d = np.empty(n, np.uint64)
+        c = np.empty(n, np.int64)
+        _lib.check(self._L.bt_read_digest(self._h, n, d.ctypes.data, c.ctypes.data))
+        return d, c
+
+    def last_timing(self):
+        """(walk kernel ms, whole call ms, kernels launched) of the last call."""
+        w = C.c_float()
+        c = C.c_float()
+        k = C.c_int64()
+        _lib.check(self._L.bt_last_timing(self._h, C.byref(w), C.byref(c), C.byref(k)))
+        return float(w.value), float(c.value), int(k.value)
+
+    def save_state(self) -> None:
+        _lib.check(self._L.bt_save_state(self._h))
+
+    def restore_state(self) -> None:
+        _lib.check(self._L.bt_restore_state(self._h))
+
+    def close(self) -> None:
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._L.bt_destroy(h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

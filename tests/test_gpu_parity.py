@@ -1,0 +1,207 @@
+"""CUDA path (libb200tally.so through the MeshTally facade / C ABI) vs the
+reference's golden outputs and the CPU oracle.
+
+Bars (BASELINE.json north_star): element sequences, exit faces, positions,
+outcomes, flags and event counts BIT-EXACT; per-bin tallies within 1e-9
+relative (fp64 atomics reorder the sums).
+"""
+
+import numpy as np
+import pytest
+
+import oracle as orc
+from golden_cases import GOLDEN, STATE_KEYS, WALK_CASES, load_walk_case, rel_close
+from paper_2504_19048_b200 import MeshTally, build_cube_mesh, synth
+
+pytestmark = pytest.mark.gpu
+
+TALLY_RTOL = 1e-9
+
+
+def _run(case, localize, **kw):
+    mt = MeshTally(case.mesh, case.capacity, case.num_groups, localize=localize,
+                   digest=True, **kw)
+    for b in case.batches:
+        mt.initialize_particle_location(b.init_positions)
+        n = b.init_positions.shape[0]
+        st = mt.read_particles(n)
+        yield "init", mt, b, None, None, st
+        for mv in b.moves:
+            seg0 = st.seg_total.copy()
+            s = mt.move_to_next_location(mv.dest, mv.flying, mv.weights, mv.groups)
+            st = mt.read_particles(n)
+            yield "move", mt, b, mv, s, (st, st.seg_total - seg0)
+        yield "finalize", mt, b, None, None, None
+        mt.finalize_batch()
+
+
+def _check_case(case, localize, **kw):
+    for kind, mt, b, mv, s, st in _run(case, localize, **kw):
+        if kind == "init":
+            if localize == "walk" or case.name != "torus_small":
+                assert np.array_equal(st.element, b.init_element)
+                assert np.array_equal(st.alive, b.init_alive)
+        elif kind == "move":
+            st, seg = st
+            e = mv.expect
+            got = np.array([s.sweeps, s.events, s.reached, s.boundary_exits,
+                            s.stuck_recoveries, s.stuck_terminations])
+            assert np.array_equal(got, e["summary"]), (got, e["summary"])
+            for k in STATE_KEYS:
+                if k == "flying":
+                    assert not e[k].any()
+                    continue
+                assert np.array_equal(getattr(st, k), e[k]), k
+            d, c = mt.read_digest(len(st.element))
+            assert np.array_equal(c, e["count"])
+            assert np.array_equal(d, e["digest"])
+            assert np.array_equal(seg, e["seg_delta"])
+            ok, worst = rel_close(mt.batch_totals().reshape(-1), e["tally"], TALLY_RTOL)
+            assert ok, worst
+        else:
+            pass
+    assert rel_close(mt.grid.sum, case.batches[-1].sum, TALLY_RTOL)[0]
+    assert rel_close(mt.grid.sum_sq, case.batches[-1].sum_sq, TALLY_RTOL)[0]
+    fl = mt.flux()
+    assert rel_close(fl.mean, case.flux_mean, TALLY_RTOL)[0]
+    # rel_error cancels catastrophically between near-equal batches; see
+    # tests/test_oracle_golden.py
+    assert np.abs(fl.rel_error - case.flux_rel).max() < 1e-5
+    mt.close()
+
+
+@pytest.mark.parametrize("name", WALK_CASES)
+def test_walk_matches_reference_walk_localize(name):
+    _check_case(load_walk_case(name), "walk")
+
+
+@pytest.mark.parametrize("name", [c for c in WALK_CASES if c != "torus_small"])
+def test_walk_matches_reference_grid_localize(name):
+    _check_case(load_walk_case(name), "grid")
+
+
+@pytest.mark.parametrize("opts", [dict(sort=True), dict(warp_aggregate=False),
+                                  dict(sort=True, warp_aggregate=False)])
+def test_walk_options_keep_parity(opts):
+    _check_case(load_walk_case("c1_point_s2"), "grid", **opts)
+    _check_case(load_walk_case("n6_uniform_g3"), "grid", **opts)
+
+
+def test_localize_pathologies():
+    d = np.load(GOLDEN / "localize_ref.npz")
+    m = build_cube_mesh(10)
+    pts = d["points"]
+    mt = MeshTally(m, pts.shape[0], localize="walk")
+    mt.initialize_particle_location(pts)
+    st = mt.read_particles()
+    # walk mode reproduces the reference bit for bit, lost points included
+    assert np.array_equal(st.element, d["element"])
+    assert np.array_equal(st.alive, d["alive"])
+    assert np.array_equal(st.outcome, d["outcome"])
+    assert np.array_equal(st.position, d["position"])
+    # grid mode: lowest-id containing element everywhere (finds what the walk loses)
+    mt.initialize_particle_location(pts, mode="grid")
+    st = mt.read_particles()
+    low = orc.locate_exhaustive(m, pts)
+    assert np.array_equal(st.element, low)
+    assert np.array_equal(st.alive, (low >= 0).astype(np.int8))
+    found = low >= 0
+    assert np.array_equal(st.position[found], pts[found])
+
+
+def test_grid_localize_random_meshes():
+    gen = np.random.default_rng(5)
+    for n in (1, 3, 7, 16):
+        m = build_cube_mesh(n)
+        pts = gen.uniform(-0.1, 1.1, (5000, 3))
+        mt = MeshTally(m, pts.shape[0])
+        mt.initialize_particle_location(pts)
+        st = mt.read_particles()
+        assert np.array_equal(st.element, orc.locate_exhaustive(m, pts))
+
+
+@pytest.mark.parametrize("sigma_t", [2.0, 100.0])
+def test_full_size_c2_against_oracle(sigma_t):
+    """C2 mesh (998,250 tets); 2e5 particles checked exhaustively against the
+    multi-threaded oracle: digests, states bit-exact; tallies <= 1e-9."""
+    m = build_cube_mesh(55)
+    gen = synth.rng(synth.SEED + 10)
+    n = 200_000
+    pos = synth.uniform_box(gen, n)
+    dest = synth.flight_destinations(gen, pos, sigma_t)
+    w = 0.5 + gen.random(n)
+    fly = np.ones(n, np.int8)
+    mt = MeshTally(m, n, digest=True, sort=True)
+    mt.initialize_particle_location(pos)
+    s = mt.move_to_next_location(dest, fly, w)
+    st = mt.read_particles()
+    ref = orc.OracleTally(m, n, threads=orc.max_threads())
+    ref.initialize_particle_location(pos)
+    assert np.array_equal(st.element, ref.element)
+    r = ref.move_to_next_location(dest, fly, w)
+    assert tuple(r) == (s.sweeps, s.events, s.reached, s.boundary_exits, s.stuck_recoveries,
+                        s.stuck_terminations)
+    for k in ("position", "element", "alive", "entry_face", "stuck", "outcome", "seg_total"):
+        assert np.array_equal(getattr(st, k), getattr(ref, k)[:n]), k
+    d, c = mt.read_digest()
+    assert np.array_equal(d, ref.digest) and np.array_equal(c, ref.count)
+    ok, worst = rel_close(mt.batch_totals().reshape(-1), ref.batch_totals(), TALLY_RTOL)
+    assert ok, worst
+    # size-independent property: path-length conservation
+    tot = mt.batch_totals().sum()
+    assert abs(tot - float((w * st.seg_total).sum())) <= 1e-9 * tot
+
+
+def test_device_pointer_path_equals_host_path():
+    torch = pytest.importorskip("torch")
+    case = load_walk_case("n6_uniform_g3")
+    b = case.batches[0]
+    mv = b.moves[0]
+    host = MeshTally(case.mesh, case.capacity, case.num_groups, digest=True)
+    dev = MeshTally(case.mesh, case.capacity, case.num_groups, digest=True)
+    host.initialize_particle_location(b.init_positions)
+    dev.initialize_particle_location(torch.from_numpy(b.init_positions).cuda())
+    s1 = host.move_to_next_location(mv.dest, mv.flying, mv.weights, mv.groups)
+    s2 = dev.move_to_next_location(torch.from_numpy(mv.dest).cuda(),
+                                   torch.from_numpy(mv.flying).cuda(),
+                                   torch.from_numpy(mv.weights).cuda(),
+                                   torch.from_numpy(mv.groups).cuda())
+    assert s1 == s2
+    a, c = host.read_particles(), dev.read_particles()
+    for k in ("position", "element", "alive", "entry_face", "stuck", "outcome"):
+        assert np.array_equal(getattr(a, k), getattr(c, k))
+    assert rel_close(host.batch_totals(), dev.batch_totals(), TALLY_RTOL)[0]
+    assert host.source_weight == pytest.approx(dev.source_weight, rel=1e-14)
+
+
+def test_error_behaviour():
+    m = build_cube_mesh(4)
+    mt = MeshTally(m, 10)
+    with pytest.raises(ValueError):
+        mt.initialize_particle_location(np.zeros(33))      # count 11 > capacity
+    with pytest.raises(ValueError):
+        mt.initialize_particle_location(np.zeros(7))       # not 3*count
+    pos = np.full((4, 3), 0.3123)
+    mt.initialize_particle_location(pos)
+    with pytest.raises(ValueError):
+        mt.move_to_next_location(np.zeros(11), np.ones(4), np.ones(4))
+    with pytest.raises(IndexError):
+        mt.move_to_next_location(pos + 0.1, np.ones(4), np.ones(4), groups=[0, 0, 0, 5])
+    assert mt.move_to_next_location(np.zeros(0), np.zeros(0, np.int8), np.zeros(0)) is None
+    with pytest.raises(RuntimeError):
+        mt.flux()
+    with pytest.raises(RuntimeError):
+        mt.finalize_batch()
+    # unlocalized flying particle
+    mt2 = MeshTally(m, 4)
+    with pytest.raises(ValueError):
+        mt2.move_to_next_location(pos, np.ones(4), np.ones(4))
+    # sweep guard
+    mt.set_option(0, 1)
+    mt.initialize_particle_location(np.array([[0.05, 0.05, 0.05]]))
+    with pytest.raises(RuntimeError):
+        mt.move_to_next_location([0.95, 0.95, 0.9], [1], [1.0])
+    with pytest.raises(TypeError):
+        MeshTally(object(), 4)
+    with pytest.raises(ValueError):
+        MeshTally(m, 0)
