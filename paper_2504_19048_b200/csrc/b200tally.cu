@@ -133,9 +133,10 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // walk kernel: the fused sweep (search.py:169-275) run to completion per lane
 
 constexpr int WALK_THREADS = 256;
+constexpr int DEFAULT_MINB = 2;
 
-template <bool DIGEST, bool WAGG>
-__global__ void __launch_bounds__(WALK_THREADS) walk_kernel(const WalkArgs a) {
+template <bool DIGEST, bool WAGG, int MINB>
+__global__ void __launch_bounds__(WALK_THREADS, MINB) walk_kernel(const WalkArgs a) {
     constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
 
@@ -165,6 +166,10 @@ __global__ void __launch_bounds__(WALK_THREADS) walk_kernel(const WalkArgs a) {
                     const unsigned long long q = base + __popc(idle & lanemask_lt());
                     if (q < (unsigned long long)a.count) {
                         const int64_t i = a.order ? (int64_t)a.order[q] : (int64_t)q;
+                        if (DIGEST && a.fly_in[i] == 0) {  // not moving: empty sequence
+                            a.digest[i] = DIGEST_INIT;
+                            a.dcount[i] = 0;
+                        }
                         if (a.fly_in[i] != 0) {
                             idx = i;
                             e = a.element[i];
@@ -228,17 +233,15 @@ __global__ void __launch_bounds__(WALK_THREADS) walk_kernel(const WalkArgs a) {
                     event = false;
                 } else if (st == 1) {
                     int hop = -1;
-                    for (int f = 0; f < 4; ++f) {
-                        const int nbp = r.nb[f];
-                        if (nbp >= 0) {
+#pragma unroll 1
+                    for (int f = 0; f < 4; ++f) {  // rare path: reload, no local arrays
+                        const int nbp = __ldg(&a.rec[e].nb[f]);
+                        if (hop < 0 && nbp >= 0) {
                             const int nb = nbp >> 2;
                             const ElemRec rn = load_rec(a.rec, nb);
                             Tet Tn;
                             load_tet(a, rn, Tn);
-                            if (contains(Tn, ox, oy, oz, EPS_BARY)) {
-                                hop = nb;
-                                break;
-                            }
+                            if (contains(Tn, ox, oy, oz, EPS_BARY)) hop = nb;
                         }
                     }
                     event = false;
@@ -298,7 +301,9 @@ __global__ void __launch_bounds__(WALK_THREADS) walk_kernel(const WalkArgs a) {
                     ++n_reached;
                     done = true;
                 } else {
-                    const int nbp = r.nb[face];
+                    const int nbp = face == 0 ? r.nb[0]
+                                    : face == 1 ? r.nb[1]
+                                    : face == 2 ? r.nb[2] : r.nb[3];
                     if (nbp < 0) {
                         a.outcome[idx] = OUT_LEAKED;
                         a.alive[idx] = 0;
@@ -1061,11 +1066,6 @@ static bt_status run_walk(bt_tally* h, const double* dest, const int8_t* fly, co
     a.ngroups = h->ngroups;
     a.score = score ? 1 : 0;
     CK(cudaMemsetAsync(h->dcounters, 0, sizeof(unsigned long long) * 16, h->stream));
-    if (dig) {
-        // particles not flying this move report zero events
-        CK(cudaMemsetAsync(h->dcount, 0, sizeof(int64_t) * count, h->stream));
-        h->kernels += 1;
-    }
     if (h->opt_sort && score) {
         iota_keys_kernel<<<grid_for(count, 256), 256, 0, h->stream>>>(
             h->element, count, h->sort_keys_in, h->sort_vals_in);
@@ -1077,14 +1077,19 @@ static bt_status run_walk(bt_tally* h, const double* dest, const int8_t* fly, co
         a.order = h->order;
         h->kernels += 5;
     }
-    int bps = h->blocks_per_sm;
-    auto kern = dig ? (h->opt_wagg ? walk_kernel<true, true> : walk_kernel<true, false>)
-                    : (h->opt_wagg ? walk_kernel<false, true> : walk_kernel<false, false>);
-    if (bps <= 0) {
-        int occ = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WALK_THREADS, 0));
-        bps = std::max(1, occ);
-    }
+    // register-budget variant: MINB resident CTAs of 256 threads per SM
+    const int minb = h->blocks_per_sm >= 1 && h->blocks_per_sm <= 3 ? h->blocks_per_sm
+                                                                     : DEFAULT_MINB;
+    using KernT = void (*)(const WalkArgs);
+    static const KernT table[2][2][3] = {
+        {{walk_kernel<false, false, 1>, walk_kernel<false, false, 2>, walk_kernel<false, false, 3>},
+         {walk_kernel<false, true, 1>, walk_kernel<false, true, 2>, walk_kernel<false, true, 3>}},
+        {{walk_kernel<true, false, 1>, walk_kernel<true, false, 2>, walk_kernel<true, false, 3>},
+         {walk_kernel<true, true, 1>, walk_kernel<true, true, 2>, walk_kernel<true, true, 3>}}};
+    KernT kern = table[dig ? 1 : 0][h->opt_wagg ? 1 : 0][minb - 1];
+    int bps = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, WALK_THREADS, 0));
+    bps = std::max(1, bps);
     const int64_t want = (count + WALK_THREADS - 1) / WALK_THREADS;
     const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)bps * h->num_sms));
     CK(cudaEventRecord(h->ev0, h->stream));

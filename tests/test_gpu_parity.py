@@ -55,7 +55,12 @@ def _check_case(case, localize, **kw):
             d, c = mt.read_digest(len(st.element))
             assert np.array_equal(c, e["count"])
             assert np.array_equal(d, e["digest"])
-            assert np.array_equal(seg, e["seg_delta"])
+            if localize == "walk":
+                assert np.array_equal(seg, e["seg_delta"])
+            else:
+                # the reference's seg_total also holds the centroid-0 trial walk
+                # length, so its per-move delta carries that sum's rounding
+                assert rel_close(seg, e["seg_delta"], 1e-12)[0]
             ok, worst = rel_close(mt.batch_totals().reshape(-1), e["tally"], TALLY_RTOL)
             assert ok, worst
         else:
@@ -133,11 +138,13 @@ def test_full_size_c2_against_oracle(sigma_t):
     fly = np.ones(n, np.int8)
     mt = MeshTally(m, n, digest=True, sort=True)
     mt.initialize_particle_location(pos)
+    st0 = mt.read_particles()
     s = mt.move_to_next_location(dest, fly, w)
     st = mt.read_particles()
     ref = orc.OracleTally(m, n, threads=orc.max_threads())
     ref.initialize_particle_location(pos)
-    assert np.array_equal(st.element, ref.element)
+    assert np.array_equal(st0.element, ref.element)
+    ref.seg_total[:] = 0.0  # grid localization has no trial-walk length
     r = ref.move_to_next_location(dest, fly, w)
     assert tuple(r) == (s.sweeps, s.events, s.reached, s.boundary_exits, s.stuck_recoveries,
                         s.stuck_terminations)
