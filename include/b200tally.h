@@ -66,7 +66,8 @@ enum {
     BT_OPT_DIGEST = 1,       /* 1: record per-particle (element, face) digests */
     BT_OPT_SORT = 2,         /* 1: hand particles to warps in element order */
     BT_OPT_WARP_AGG = 3,     /* 1: __match_any_sync aggregation of tally atomics */
-    BT_OPT_BLOCKS_PER_SM = 4 /* persistent walk grid: CTAs per SM (0 = auto) */
+    BT_OPT_BLOCKS_PER_SM = 4, /* walk register budget: 1..3 resident 256-thread CTAs/SM */
+    BT_OPT_STAGED = 5         /* 1: compact flying particles + cp.async-prefetched refill */
 };
 
 /* Mirrors meshtally.search.TraceSummary (search.py:150-157). */

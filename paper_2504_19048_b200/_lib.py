@@ -19,7 +19,7 @@ BT_MEM_HOST, BT_MEM_DEVICE = 0, 1
 BT_LOCATE_GRID, BT_LOCATE_WALK = 0, 1
 BT_TALLY_BATCH, BT_TALLY_SUM, BT_TALLY_SUM_SQ = 0, 1, 2
 (BT_OPT_MAX_SWEEPS, BT_OPT_DIGEST, BT_OPT_SORT, BT_OPT_WARP_AGG,
- BT_OPT_BLOCKS_PER_SM) = range(5)
+ BT_OPT_BLOCKS_PER_SM, BT_OPT_STAGED) = range(6)
 
 # every symbol declared in include/b200tally.h (checked by tests/test_abi.py)
 EXPORTS = (

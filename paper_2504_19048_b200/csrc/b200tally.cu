@@ -130,39 +130,244 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 }
 
 // ---------------------------------------------------------------------------
-// walk kernel: the fused sweep (search.py:169-275) run to completion per lane
+// walk kernels: the fused sweep (search.py:169-275) run to completion per lane
 
 constexpr int WALK_THREADS = 256;
 constexpr int DEFAULT_MINB = 2;
 
+// one particle's walk state, held in registers while it flies
+struct Lane {
+    double px, py, pz, dx, dy, dz, w, seg;
+    int64_t idx;  // -1: lane idle
+    int e, g, entry, st, iters;
+    int outcome, alive;
+    uint64_t dig;
+    int dcnt;
+};
+
+struct Counters {
+    unsigned events = 0, reached = 0, boundary = 0, recov = 0, killed = 0;
+    int max_iters = 0;
+    int err = 0;
+};
+
+// One step of search.py:183-274 for a flying lane.  Returns true when the
+// particle stops (reached, leaked, stuck-killed or sweep guard); sets
+// has_score/bin/val when the step scores a segment.
+template <bool DIGEST>
+__device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& C,
+                                          bool& has_score, int64_t& bin, double& val) {
+    const ElemRec r = load_rec(a.rec, L.e);
+    Tet T;
+    load_tet(a, r, T);
+    double ox = L.px, oy = L.py, oz = L.pz;
+    if (L.st == 1) {  // search.py:190-196
+        const double sx = __dsub_rn(L.dx, L.px), sy = __dsub_rn(L.dy, L.py),
+                     sz = __dsub_rn(L.dz, L.pz);
+        const double ln = __dsqrt_rn(
+            __dadd_rn(__dadd_rn(__dmul_rn(sx, sx), __dmul_rn(sy, sy)), __dmul_rn(sz, sz)));
+        if (ln > 0.0) {
+            ox = __dadd_rn(ox, __ddiv_rn(__dmul_rn(NUDGE, sx), ln));
+            oy = __dadd_rn(oy, __ddiv_rn(__dmul_rn(NUDGE, sy), ln));
+            oz = __dadd_rn(oz, __ddiv_rn(__dmul_rn(NUDGE, sz), ln));
+        }
+    }
+    int face;
+    double t;
+    bool exact_used;
+    int kind = exit_search_fast(T, ox, oy, oz, L.dx, L.dy, L.dz, L.entry, &face, &t, &exact_used);
+    bool done = false;
+    bool event = true;
+    if (kind == 2) {  // stuck ladder, search.py:199-235
+        if (contains(T, L.dx, L.dy, L.dz, STUCK_TOL)) {
+            kind = 0;
+            ++C.recov;
+        } else if (L.st == 0) {
+            L.st = 1;
+            ++C.recov;
+            event = false;
+        } else if (L.st == 1) {
+            int hop = -1;
+#pragma unroll 1
+            for (int f = 0; f < 4; ++f) {  // rare path: reload, no local arrays
+                const int nbp = __ldg(&a.rec[L.e].nb[f]);
+                if (hop < 0 && nbp >= 0) {
+                    const int nb = nbp >> 2;
+                    const ElemRec rn = load_rec(a.rec, nb);
+                    Tet Tn;
+                    load_tet(a, rn, Tn);
+                    if (contains(Tn, ox, oy, oz, EPS_BARY)) hop = nb;
+                }
+            }
+            event = false;
+            if (hop >= 0) {
+                L.e = hop;
+                L.entry = -1;
+                L.st = 2;
+                ++C.recov;
+            } else {
+                L.outcome = OUT_STUCK_KILLED;
+                L.alive = 0;
+                ++C.killed;
+                done = true;
+            }
+        } else {
+            L.outcome = OUT_STUCK_KILLED;
+            L.alive = 0;
+            ++C.killed;
+            event = false;
+            done = true;
+        }
+    }
+    if (event) {  // search.py:236-274
+        ++C.events;
+        L.st = 0;
+        if (DIGEST) {
+            L.dig = (L.dig ^ (uint64_t)((int64_t)L.e * 8 + face + 1)) * DIGEST_PRIME;
+            ++L.dcnt;
+        }
+        double qx, qy, qz;
+        if (kind == 0) {
+            qx = L.dx;
+            qy = L.dy;
+            qz = L.dz;
+        } else {
+            qx = __dadd_rn(ox, __dmul_rn(t, __dsub_rn(L.dx, ox)));
+            qy = __dadd_rn(oy, __dmul_rn(t, __dsub_rn(L.dy, oy)));
+            qz = __dadd_rn(oz, __dmul_rn(t, __dsub_rn(L.dz, oz)));
+        }
+        const double ax = __dsub_rn(qx, L.px), ay = __dsub_rn(qy, L.py), az = __dsub_rn(qz, L.pz);
+        const double seg = __dsqrt_rn(
+            __dadd_rn(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)), __dmul_rn(az, az)));
+        if (a.score) {
+            has_score = true;
+            bin = (int64_t)L.e * a.ngroups + L.g;
+            val = __dmul_rn(L.w, seg);
+        }
+        L.seg = __dadd_rn(L.seg, seg);
+        L.px = qx;
+        L.py = qy;
+        L.pz = qz;
+        if (kind == 0) {
+            L.entry = -1;
+            L.outcome = OUT_REACHED;
+            ++C.reached;
+            done = true;
+        } else {
+            const int nbp = face == 0 ? r.nb[0] : face == 1 ? r.nb[1] : face == 2 ? r.nb[2] : r.nb[3];
+            if (nbp < 0) {
+                L.outcome = OUT_LEAKED;
+                L.alive = 0;
+                ++C.boundary;
+                done = true;
+            } else {
+                L.e = nbp >> 2;
+                L.entry = nbp & 3;
+            }
+        }
+    }
+    ++L.iters;
+    if (!done && L.iters > a.max_sweeps) {  // sweep guard, search.py:513-516
+        C.err = 1;
+        done = true;
+    }
+    return done;
+}
+
+template <bool DIGEST>
+__device__ __forceinline__ void finish(const WalkArgs& a, Lane& L, Counters& C) {
+    const int64_t i = L.idx;
+    a.pos[3 * i] = L.px;
+    a.pos[3 * i + 1] = L.py;
+    a.pos[3 * i + 2] = L.pz;
+    a.element[i] = L.e;
+    a.entry[i] = (int8_t)L.entry;
+    a.stuck[i] = (int8_t)L.st;
+    a.outcome[i] = (int8_t)L.outcome;
+    a.alive[i] = (int8_t)L.alive;
+    a.seg_total[i] = L.seg;
+    if (DIGEST) {
+        a.digest[i] = L.dig;
+        a.dcount[i] = L.dcnt;
+    }
+    C.max_iters = max(C.max_iters, L.iters);
+    L.idx = -1;
+}
+
+__device__ __forceinline__ void begin(Lane& L) {
+    L.iters = 0;
+    L.dig = DIGEST_INIT;
+    L.dcnt = 0;
+    L.alive = 1;          // load_step: alive |= flying
+    L.outcome = OUT_NONE;
+}
+
+template <bool WAGG>
+__device__ __forceinline__ void score(const WalkArgs& a, bool has_score, int64_t bin, double val) {
+    constexpr unsigned FULL = 0xffffffffu;
+    if (WAGG) {
+        const int lane = threadIdx.x & 31;
+        const unsigned m = __ballot_sync(FULL, has_score);
+        if (has_score) {
+            const unsigned peers = __match_any_sync(m, (unsigned long long)bin);
+            const int leader = __ffs(peers) - 1;
+            double sum = val;
+            if (peers != (1u << lane)) {
+                sum = 0.0;
+                unsigned rest = peers;
+                while (rest) {
+                    const int src = __ffs(rest) - 1;
+                    rest &= rest - 1;
+                    sum = __dadd_rn(sum, __shfl_sync(peers, val, src));
+                }
+            }
+            if (lane == leader) atomicAdd(a.tally + bin, sum);
+        }
+    } else if (has_score) {
+        atomicAdd(a.tally + bin, val);
+    }
+}
+
+__device__ __forceinline__ void flush_counters(const WalkArgs& a, Counters& C) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const unsigned ev = __reduce_add_sync(FULL, C.events);
+    const unsigned re = __reduce_add_sync(FULL, C.reached);
+    const unsigned bd = __reduce_add_sync(FULL, C.boundary);
+    const unsigned rv = __reduce_add_sync(FULL, C.recov);
+    const unsigned kl = __reduce_add_sync(FULL, C.killed);
+    const int mi = __reduce_max_sync(FULL, C.max_iters);
+    const int er = __reduce_or_sync(FULL, C.err);
+    if ((threadIdx.x & 31) == 0) {
+        if (ev) atomicAdd(a.counters + C_EVENTS, (unsigned long long)ev);
+        if (re) atomicAdd(a.counters + C_REACHED, (unsigned long long)re);
+        if (bd) atomicAdd(a.counters + C_BOUNDARY, (unsigned long long)bd);
+        if (rv) atomicAdd(a.counters + C_RECOV, (unsigned long long)rv);
+        if (kl) atomicAdd(a.counters + C_KILLED, (unsigned long long)kl);
+        if (mi) atomicMax(a.counters + C_SWEEPS, (unsigned long long)mi);
+        if (er) atomicOr(a.counters + C_ERR, 1ull);
+    }
+}
+
+// v1: idle lanes refill straight from the particle arrays (one atomicAdd per
+// warp per refill); the fetch's global loads sit on the step's critical path.
 template <bool DIGEST, bool WAGG, int MINB>
 __global__ void __launch_bounds__(WALK_THREADS, MINB) walk_kernel(const WalkArgs a) {
     constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
-
-    int64_t idx = -1;
+    Lane L;
+    L.idx = -1;
+    Counters C;
     bool drained = false;
-    // particle state in registers
-    double px = 0, py = 0, pz = 0, dx = 0, dy = 0, dz = 0, w = 0, seg_acc = 0;
-    int e = 0, g = 0, entry = -1, st = 0, iters = 0;
-    uint64_t dig = DIGEST_INIT;
-    int dcnt = 0;
-    // per-lane counters (TraceSummary)
-    unsigned n_events = 0, n_reached = 0, n_boundary = 0, n_recov = 0, n_killed = 0;
-    int max_iters = 0;
-    int err = 0;
-
     while (true) {
-        // ---- refill idle lanes from the global queue (one atomic per warp)
         if (!drained) {
-            const unsigned idle = __ballot_sync(FULL, idx < 0);
+            const unsigned idle = __ballot_sync(FULL, L.idx < 0);
             if (idle) {
                 const unsigned nidle = __popc(idle);
                 unsigned long long base = 0;
                 if (lane == 0) base = atomicAdd(a.queue, (unsigned long long)nidle);
                 base = __shfl_sync(FULL, base, 0);
                 if (base + nidle >= (unsigned long long)a.count) drained = true;
-                if (idx < 0) {
+                if (L.idx < 0) {
                     const unsigned long long q = base + __popc(idle & lanemask_lt());
                     if (q < (unsigned long long)a.count) {
                         const int64_t i = a.order ? (int64_t)a.order[q] : (int64_t)q;
@@ -171,213 +376,206 @@ __global__ void __launch_bounds__(WALK_THREADS, MINB) walk_kernel(const WalkArgs
                             a.dcount[i] = 0;
                         }
                         if (a.fly_in[i] != 0) {
-                            idx = i;
-                            e = a.element[i];
-                            px = a.pos[3 * i];
-                            py = a.pos[3 * i + 1];
-                            pz = a.pos[3 * i + 2];
-                            dx = a.dest[3 * i];
-                            dy = a.dest[3 * i + 1];
-                            dz = a.dest[3 * i + 2];
-                            entry = a.entry[i];
-                            st = a.stuck[i];
-                            seg_acc = a.seg_total[i];
-                            if (a.score) {
-                                w = a.weight[i];
-                                g = a.group[i];
-                            }
-                            iters = 0;
-                            dig = DIGEST_INIT;
-                            dcnt = 0;
+                            L.idx = i;
+                            L.e = a.element[i];
+                            L.px = a.pos[3 * i];
+                            L.py = a.pos[3 * i + 1];
+                            L.pz = a.pos[3 * i + 2];
+                            L.dx = a.dest[3 * i];
+                            L.dy = a.dest[3 * i + 1];
+                            L.dz = a.dest[3 * i + 2];
+                            L.entry = a.entry[i];
+                            L.st = a.stuck[i];
+                            L.seg = a.seg_total[i];
+                            L.w = a.score ? a.weight[i] : 0.0;
+                            L.g = a.score ? a.group[i] : 0;
+                            begin(L);
                         }
                     }
                 }
             }
         }
-        if (!__any_sync(FULL, idx >= 0)) {
+        if (!__any_sync(FULL, L.idx >= 0)) {
             if (drained) break;
             continue;
         }
-
         bool has_score = false;
         int64_t bin = 0;
         double val = 0.0;
-        if (idx >= 0) {
-            const ElemRec r = load_rec(a.rec, e);
-            Tet T;
-            load_tet(a, r, T);
-            double ox = px, oy = py, oz = pz;
-            if (st == 1) {  // search.py:190-196
-                const double sx = __dsub_rn(dx, px), sy = __dsub_rn(dy, py),
-                             sz = __dsub_rn(dz, pz);
-                const double ln = __dsqrt_rn(__dadd_rn(
-                    __dadd_rn(__dmul_rn(sx, sx), __dmul_rn(sy, sy)), __dmul_rn(sz, sz)));
-                if (ln > 0.0) {
-                    ox = __dadd_rn(ox, __ddiv_rn(__dmul_rn(NUDGE, sx), ln));
-                    oy = __dadd_rn(oy, __ddiv_rn(__dmul_rn(NUDGE, sy), ln));
-                    oz = __dadd_rn(oz, __ddiv_rn(__dmul_rn(NUDGE, sz), ln));
-                }
-            }
-            int face;
-            double t;
-            int kind = exit_search(T, ox, oy, oz, dx, dy, dz, entry, &face, &t);
-            bool done = false;
-            bool event = true;
-            if (kind == 2) {  // stuck ladder, search.py:199-235
-                if (contains(T, dx, dy, dz, STUCK_TOL)) {
-                    kind = 0;
-                    ++n_recov;
-                } else if (st == 0) {
-                    st = 1;
-                    ++n_recov;
-                    event = false;
-                } else if (st == 1) {
-                    int hop = -1;
-#pragma unroll 1
-                    for (int f = 0; f < 4; ++f) {  // rare path: reload, no local arrays
-                        const int nbp = __ldg(&a.rec[e].nb[f]);
-                        if (hop < 0 && nbp >= 0) {
-                            const int nb = nbp >> 2;
-                            const ElemRec rn = load_rec(a.rec, nb);
-                            Tet Tn;
-                            load_tet(a, rn, Tn);
-                            if (contains(Tn, ox, oy, oz, EPS_BARY)) hop = nb;
-                        }
-                    }
-                    event = false;
-                    if (hop >= 0) {
-                        e = hop;
-                        entry = -1;
-                        st = 2;
-                        ++n_recov;
-                    } else {
-                        a.outcome[idx] = OUT_STUCK_KILLED;
-                        a.alive[idx] = 0;
-                        ++n_killed;
-                        done = true;
-                    }
-                } else {
-                    a.outcome[idx] = OUT_STUCK_KILLED;
-                    a.alive[idx] = 0;
-                    ++n_killed;
-                    event = false;
-                    done = true;
-                }
-            }
-            if (event) {  // search.py:236-274
-                ++n_events;
-                st = 0;
-                if (DIGEST) {
-                    dig = (dig ^ (uint64_t)((int64_t)e * 8 + face + 1)) * DIGEST_PRIME;
-                    ++dcnt;
-                }
-                double qx, qy, qz;
-                if (kind == 0) {
-                    qx = dx;
-                    qy = dy;
-                    qz = dz;
-                } else {
-                    qx = __dadd_rn(ox, __dmul_rn(t, __dsub_rn(dx, ox)));
-                    qy = __dadd_rn(oy, __dmul_rn(t, __dsub_rn(dy, oy)));
-                    qz = __dadd_rn(oz, __dmul_rn(t, __dsub_rn(dz, oz)));
-                }
-                const double ax = __dsub_rn(qx, px), ay = __dsub_rn(qy, py),
-                             az = __dsub_rn(qz, pz);
-                const double seg = __dsqrt_rn(__dadd_rn(
-                    __dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)), __dmul_rn(az, az)));
-                if (a.score) {
-                    has_score = true;
-                    bin = (int64_t)e * a.ngroups + g;
-                    val = __dmul_rn(w, seg);
-                }
-                seg_acc = __dadd_rn(seg_acc, seg);
-                px = qx;
-                py = qy;
-                pz = qz;
-                if (kind == 0) {
-                    entry = -1;
-                    a.outcome[idx] = OUT_REACHED;
-                    a.alive[idx] = 1;
-                    ++n_reached;
-                    done = true;
-                } else {
-                    const int nbp = face == 0 ? r.nb[0]
-                                    : face == 1 ? r.nb[1]
-                                    : face == 2 ? r.nb[2] : r.nb[3];
-                    if (nbp < 0) {
-                        a.outcome[idx] = OUT_LEAKED;
-                        a.alive[idx] = 0;
-                        ++n_boundary;
-                        done = true;
-                    } else {
-                        e = nbp >> 2;
-                        entry = nbp & 3;
-                    }
-                }
-            }
-            ++iters;
-            if (!done && iters > a.max_sweeps) {  // sweep guard, search.py:513-516
-                err = 1;
-                a.alive[idx] = 1;
-                done = true;
-            }
-            if (done) {
-                a.pos[3 * idx] = px;
-                a.pos[3 * idx + 1] = py;
-                a.pos[3 * idx + 2] = pz;
-                a.element[idx] = e;
-                a.entry[idx] = (int8_t)entry;
-                a.stuck[idx] = (int8_t)st;
-                a.seg_total[idx] = seg_acc;
-                if (DIGEST) {
-                    a.digest[idx] = dig;
-                    a.dcount[idx] = dcnt;
-                }
-                max_iters = max(max_iters, iters);
-                idx = -1;
-            }
+        if (L.idx >= 0) {
+            if (walk_step<DIGEST>(a, L, C, has_score, bin, val)) finish<DIGEST>(a, L, C);
         }
+        score<WAGG>(a, has_score, bin, val);
+    }
+    flush_counters(a, C);
+}
 
-        // ---- tally: fp64 atomics, optionally aggregated over equal bins
-        if (WAGG) {
-            const unsigned m = __ballot_sync(FULL, has_score);
-            if (has_score) {
-                const unsigned peers = __match_any_sync(m, (unsigned long long)bin);
-                const int leader = __ffs(peers) - 1;
-                double sum = val;
-                if (peers != (1u << lane)) {
-                    sum = 0.0;
-                    unsigned rest = peers;
-                    while (rest) {
-                        const int src = __ffs(rest) - 1;
-                        rest &= rest - 1;
-                        sum = __dadd_rn(sum, __shfl_sync(peers, val, src));
-                    }
-                }
-                if (lane == leader) atomicAdd(a.tally + bin, sum);
+// ---------------------------------------------------------------------------
+// v2: staged walk.  A stage kernel compacts the flying particles into SoA
+// work arrays (coalesced); each warp then claims chunks of 32 work items and
+// prefetches the NEXT chunk into shared memory with cp.async while its lanes
+// keep walking, so refilling an idle lane is a shared-memory read instead of
+// a dependent DRAM gather on the step's critical path.
+
+struct WorkSoA {
+    double *px, *py, *pz, *dx, *dy, *dz, *w, *seg;
+    int *idx, *e, *g, *fl;  // fl = entry (low byte, signed) | stuck << 8
+};
+
+struct __align__(16) WarpStage {
+    double px[32], py[32], pz[32], dx[32], dy[32], dz[32], w[32], seg[32];
+    int idx[32], e[32], g[32], fl[32];
+};
+
+constexpr int STAGED_WARPS = WALK_THREADS / 32;
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+// claim the next chunk of 32 work items and start copying it into `st`;
+// returns the number of valid items (warp-uniform)
+__device__ __forceinline__ int claim_chunk(const WalkArgs& a, const WorkSoA& W, WarpStage& st,
+                                           int64_t nwork) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(a.queue, 32ull);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    const int64_t left = nwork - (int64_t)base;
+    const int n = left <= 0 ? 0 : (left >= 32 ? 32 : (int)left);
+    if (lane < n) {
+        const int64_t k = (int64_t)base + lane;
+        cp_async8(&st.px[lane], W.px + k);
+        cp_async8(&st.py[lane], W.py + k);
+        cp_async8(&st.pz[lane], W.pz + k);
+        cp_async8(&st.dx[lane], W.dx + k);
+        cp_async8(&st.dy[lane], W.dy + k);
+        cp_async8(&st.dz[lane], W.dz + k);
+        cp_async8(&st.w[lane], W.w + k);
+        cp_async8(&st.seg[lane], W.seg + k);
+        cp_async4(&st.idx[lane], W.idx + k);
+        cp_async4(&st.e[lane], W.e + k);
+        cp_async4(&st.g[lane], W.g + k);
+        cp_async4(&st.fl[lane], W.fl + k);
+    }
+    cp_async_commit();
+    return n;
+}
+
+template <bool DIGEST, bool WAGG, int MINB>
+__global__ void __launch_bounds__(WALK_THREADS, MINB)
+    walk_staged_kernel(const WalkArgs a, const WorkSoA W, const int64_t* __restrict__ nwork_p) {
+    constexpr unsigned FULL = 0xffffffffu;
+    __shared__ WarpStage stages[STAGED_WARPS][2];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    const int64_t nwork = *nwork_p;
+    Lane L;
+    L.idx = -1;
+    Counters C;
+    int cur = 0;
+    int head = 0;
+    int ncur = claim_chunk(a, W, stages[wid][0], nwork);
+    int nnext = ncur == 32 ? claim_chunk(a, W, stages[wid][1], nwork) : 0;
+    // only the first group must have landed; wait_group 1 would do, but the
+    // second claim may be empty -- a full wait costs one DRAM latency once
+    cp_async_wait_all();
+    __syncwarp();
+    while (true) {
+        unsigned idle = __ballot_sync(FULL, L.idx < 0);
+        while (idle) {
+            if (head == ncur) {  // current stage used up: switch to the prefetched one
+                if (nnext == 0) break;
+                cp_async_wait_all();
+                __syncwarp();
+                cur ^= 1;
+                head = 0;
+                ncur = nnext;
+                // the stage just emptied is free: prefetch the chunk after next
+                nnext = (ncur == 32) ? claim_chunk(a, W, stages[wid][cur ^ 1], nwork) : 0;
             }
-        } else if (has_score) {
-            atomicAdd(a.tally + bin, val);
+            const int take = min((int)__popc(idle), ncur - head);
+            if (L.idx < 0) {
+                const int rk = __popc(idle & lanemask_lt());
+                if (rk < take) {
+                    const WarpStage& s = stages[wid][cur];
+                    const int j = head + rk;
+                    L.idx = s.idx[j];
+                    L.px = s.px[j];
+                    L.py = s.py[j];
+                    L.pz = s.pz[j];
+                    L.dx = s.dx[j];
+                    L.dy = s.dy[j];
+                    L.dz = s.dz[j];
+                    L.w = s.w[j];
+                    L.seg = s.seg[j];
+                    L.e = s.e[j];
+                    L.g = s.g[j];
+                    const int fl = s.fl[j];
+                    L.entry = (int)(signed char)(fl & 0xff);
+                    L.st = (fl >> 8) & 0xff;
+                    begin(L);
+                }
+            }
+            head += take;
+            idle = __ballot_sync(FULL, L.idx < 0);
+        }
+        if (!__any_sync(FULL, L.idx >= 0)) break;  // no work left anywhere for this warp
+        bool has_score = false;
+        int64_t bin = 0;
+        double val = 0.0;
+        if (L.idx >= 0) {
+            if (walk_step<DIGEST>(a, L, C, has_score, bin, val)) finish<DIGEST>(a, L, C);
+        }
+        score<WAGG>(a, has_score, bin, val);
+    }
+    cp_async_wait_all();
+    flush_counters(a, C);
+}
+
+// Compact this move's flying particles into the work arrays (order of
+// indices within a warp preserved; warps in arbitrary order).  Non-flying
+// particles get an empty digest.
+template <bool DIGEST>
+__global__ void stage_kernel(const WalkArgs a, const WorkSoA W, int64_t* __restrict__ nwork) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    bool fly = false;
+    int64_t i = 0;
+    if (t < a.count) {
+        i = a.order ? (int64_t)a.order[t] : t;
+        fly = a.fly_in[i] != 0;
+        if (DIGEST && !fly) {
+            a.digest[i] = DIGEST_INIT;
+            a.dcount[i] = 0;
         }
     }
-
-    // ---- counters: warp reduce, one atomic per warp
-    n_events = __reduce_add_sync(FULL, n_events);
-    n_reached = __reduce_add_sync(FULL, n_reached);
-    n_boundary = __reduce_add_sync(FULL, n_boundary);
-    n_recov = __reduce_add_sync(FULL, n_recov);
-    n_killed = __reduce_add_sync(FULL, n_killed);
-    max_iters = __reduce_max_sync(FULL, max_iters);
-    err = __reduce_or_sync(FULL, err);
-    if (lane == 0) {
-        if (n_events) atomicAdd(a.counters + C_EVENTS, (unsigned long long)n_events);
-        if (n_reached) atomicAdd(a.counters + C_REACHED, (unsigned long long)n_reached);
-        if (n_boundary) atomicAdd(a.counters + C_BOUNDARY, (unsigned long long)n_boundary);
-        if (n_recov) atomicAdd(a.counters + C_RECOV, (unsigned long long)n_recov);
-        if (n_killed) atomicAdd(a.counters + C_KILLED, (unsigned long long)n_killed);
-        if (max_iters) atomicMax(a.counters + C_SWEEPS, (unsigned long long)max_iters);
-        if (err) atomicOr(a.counters + C_ERR, 1ull);
-    }
+    const unsigned m = __ballot_sync(0xffffffffu, fly);
+    if (!m) return;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd((unsigned long long*)nwork, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (!fly) return;
+    const int64_t k = (int64_t)base + __popc(m & lanemask_lt());
+    W.idx[k] = (int)i;
+    W.px[k] = a.pos[3 * i];
+    W.py[k] = a.pos[3 * i + 1];
+    W.pz[k] = a.pos[3 * i + 2];
+    W.dx[k] = a.dest[3 * i];
+    W.dy[k] = a.dest[3 * i + 1];
+    W.dz[k] = a.dest[3 * i + 2];
+    W.w[k] = a.score ? a.weight[i] : 0.0;
+    W.seg[k] = a.seg_total[i];
+    W.e[k] = a.element[i];
+    W.g[k] = a.score ? a.group[i] : 0;
+    W.fl[k] = ((int)(unsigned char)a.entry[i]) | ((int)(unsigned char)a.stuck[i] << 8);
 }
 
 // ---------------------------------------------------------------------------
@@ -707,7 +905,10 @@ struct bt_tally {
     int64_t max_sweeps = -1;
     bool opt_digest = false;
     bool opt_sort = false;
-    bool opt_wagg = true;
+    bool opt_wagg = false;
+    bool opt_staged = true;
+    WorkSoA work{};
+    void* work_mem = nullptr;
     int blocks_per_sm = 0;
     // timing
     float walk_ms = 0.f, call_ms = 0.f;
@@ -731,7 +932,7 @@ static bt_status free_all(bt_tally* h) {
                     h->weight, h->digest, h->dcount, h->order, h->sort_keys_in,
                     h->sort_keys_out, h->sort_vals_in, h->sort_tmp, h->tally, h->sum,
                     h->sum_sq, h->dcounters, h->dwsum, h->snap_pos, h->snap_element,
-                    h->snap_flags, h->snap_seg};
+                    h->snap_flags, h->snap_seg, h->work_mem};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->hcounters) cudaFreeHost(h->hcounters);
@@ -1033,13 +1234,37 @@ bt_status bt_set_option(bt_tally* h, int32_t key, int64_t value) {
             break;
         case BT_OPT_WARP_AGG: h->opt_wagg = value != 0; break;
         case BT_OPT_BLOCKS_PER_SM: h->blocks_per_sm = (int)value; break;
+        case BT_OPT_STAGED: h->opt_staged = value != 0; break;
         default: return set_err(BT_EINVAL, "unknown option %d", key);
     }
     return BT_OK;
 }
 
+static bt_status ensure_work(bt_tally* h) {
+    if (h->work_mem) return BT_OK;
+    const size_t n = (size_t)h->cap;
+    char* p = nullptr;
+    CK(cudaMalloc((void**)&p, n * (8 * sizeof(double) + 4 * sizeof(int)) + 256));
+    h->work_mem = p;
+    WorkSoA& W = h->work;
+    double* d = reinterpret_cast<double*>(p);
+    W.px = d; W.py = d + n; W.pz = d + 2 * n; W.dx = d + 3 * n; W.dy = d + 4 * n;
+    W.dz = d + 5 * n; W.w = d + 6 * n; W.seg = d + 7 * n;
+    int* q = reinterpret_cast<int*>(d + 8 * n);
+    W.idx = q; W.e = q + n; W.g = q + 2 * n; W.fl = q + 3 * n;
+    return BT_OK;
+}
+
+// Host work overlapped with the walk kernel (runs after the launch, before
+// the stream synchronisation).
+struct HostOverlap {
+    void (*fn)(void*) = nullptr;
+    void* ctx = nullptr;
+};
+
 static bt_status run_walk(bt_tally* h, const double* dest, const int8_t* fly, const double* w,
-                          int64_t count, bool score, bt_summary* summary) {
+                          int64_t count, bool score, bt_summary* summary,
+                          HostOverlap overlap = HostOverlap()) {
     WalkArgs a;
     a.rec = h->rec;
     a.vtx = h->vtx;
@@ -1086,19 +1311,44 @@ static bt_status run_walk(bt_tally* h, const double* dest, const int8_t* fly, co
          {walk_kernel<false, true, 1>, walk_kernel<false, true, 2>, walk_kernel<false, true, 3>}},
         {{walk_kernel<true, false, 1>, walk_kernel<true, false, 2>, walk_kernel<true, false, 3>},
          {walk_kernel<true, true, 1>, walk_kernel<true, true, 2>, walk_kernel<true, true, 3>}}};
-    KernT kern = table[dig ? 1 : 0][h->opt_wagg ? 1 : 0][minb - 1];
+    using StagedT = void (*)(const WalkArgs, const WorkSoA, const int64_t*);
+    static const StagedT staged_table[2][2][3] = {
+        {{walk_staged_kernel<false, false, 1>, walk_staged_kernel<false, false, 2>,
+          walk_staged_kernel<false, false, 3>},
+         {walk_staged_kernel<false, true, 1>, walk_staged_kernel<false, true, 2>,
+          walk_staged_kernel<false, true, 3>}},
+        {{walk_staged_kernel<true, false, 1>, walk_staged_kernel<true, false, 2>,
+          walk_staged_kernel<true, false, 3>},
+         {walk_staged_kernel<true, true, 1>, walk_staged_kernel<true, true, 2>,
+          walk_staged_kernel<true, true, 3>}}};
+    const bool staged = h->opt_staged;
+    const void* kptr = staged ? (const void*)staged_table[dig ? 1 : 0][h->opt_wagg ? 1 : 0][minb - 1]
+                              : (const void*)table[dig ? 1 : 0][h->opt_wagg ? 1 : 0][minb - 1];
     int bps = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, WALK_THREADS, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kptr, WALK_THREADS, 0));
     bps = std::max(1, bps);
     const int64_t want = (count + WALK_THREADS - 1) / WALK_THREADS;
     const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)bps * h->num_sms));
+    int64_t* nwork = reinterpret_cast<int64_t*>(h->dcounters + 14);
+    if (staged) {
+        TRY(ensure_work(h));
+        auto sk = dig ? stage_kernel<true> : stage_kernel<false>;
+        sk<<<grid_for(count, 256), 256, 0, h->stream>>>(a, h->work, nwork);
+        CK(cudaGetLastError());
+        h->kernels += 1;
+    }
     CK(cudaEventRecord(h->ev0, h->stream));
-    kern<<<blocks, WALK_THREADS, 0, h->stream>>>(a);
+    if (staged)
+        staged_table[dig ? 1 : 0][h->opt_wagg ? 1 : 0][minb - 1]<<<blocks, WALK_THREADS, 0,
+                                                                  h->stream>>>(a, h->work, nwork);
+    else
+        table[dig ? 1 : 0][h->opt_wagg ? 1 : 0][minb - 1]<<<blocks, WALK_THREADS, 0, h->stream>>>(a);
     CK(cudaGetLastError());
     CK(cudaEventRecord(h->ev1, h->stream));
     h->kernels += 1;
     CK(cudaMemcpyAsync(h->hcounters, h->dcounters, sizeof(unsigned long long) * 16,
                        cudaMemcpyDeviceToHost, h->stream));
+    if (overlap.fn) overlap.fn(overlap.ctx);
     CK(cudaStreamSynchronize(h->stream));
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
@@ -1202,20 +1452,12 @@ bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, cons
     const bool host = mem_kind == BT_MEM_HOST;
     // host-side checks and the recorded source weight (tally.py:262-269)
     bool need_w = h->source_weight == 0.0;
-    double hw = 0.0;
     if (host) {
         if (groups) {
             for (int64_t i = 0; i < count; ++i)
                 if (groups[i] < 0 || groups[i] >= h->ngroups)
                     return set_err(BT_EINDEX, "group %d out of range [0, %d)", groups[i],
                                    h->ngroups);
-        }
-        if (need_w) {
-            std::vector<double> sel;
-            sel.reserve((size_t)count);
-            for (int64_t i = 0; i < count; ++i)
-                if (flying[i] != 0) sel.push_back(weights[i]);
-            hw = pairwise_sum(sel.data(), (int64_t)sel.size());
         }
     }
     CK(cudaEventRecord(h->ev2, h->stream));
@@ -1258,8 +1500,28 @@ bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, cons
         return set_err(BT_EINVAL,
                        "a flying particle is not localized (element = -1); call "
                        "initialize_particle_location first");
-    if (need_w) h->source_weight = host ? hw : dw;
-    bt_status s = run_walk(h, d_dest, d_fly, d_w, count, true, summary);
+    // the recorded source weight (host inputs: numpy's pairwise order, computed
+    // on the host while the walk kernel runs)
+    struct WJob {
+        const double* w;
+        const int8_t* fly;
+        int64_t n;
+        double out;
+    } job{weights, flying, count, 0.0};
+    HostOverlap ov;
+    if (host && need_w) {
+        ov.ctx = &job;
+        ov.fn = [](void* c) {
+            WJob* j = static_cast<WJob*>(c);
+            std::vector<double> sel;
+            sel.reserve((size_t)j->n);
+            for (int64_t i = 0; i < j->n; ++i)
+                if (j->fly[i] != 0) sel.push_back(j->w[i]);
+            j->out = pairwise_sum(sel.data(), (int64_t)sel.size());
+        };
+    }
+    bt_status s = run_walk(h, d_dest, d_fly, d_w, count, true, summary, ov);
+    if (need_w) h->source_weight = host ? job.out : dw;
     CK(cudaEventRecord(h->ev3, h->stream));
     CK(cudaEventSynchronize(h->ev3));
     CK(cudaEventElapsedTime(&h->call_ms, h->ev2, h->ev3));

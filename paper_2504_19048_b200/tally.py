@@ -199,7 +199,7 @@ class MeshTally:
 
     def __init__(self, mesh, num_particles: int, num_groups: int = 1, threads: int = 1, *,
                  device: int = 0, localize: str = "grid", digest: bool = False,
-                 sort: bool = False, warp_aggregate: bool = True):
+                 sort: bool = False, warp_aggregate: bool = False, staged: bool = True):
         if isinstance(mesh, (str, Path)):
             mesh = read_tetmesh(mesh)
         if not all(hasattr(mesh, a) for a in ("vertices", "elements", "adj_elem", "adj_face",
@@ -235,6 +235,7 @@ class MeshTally:
         self.set_option(_lib.BT_OPT_DIGEST, int(digest))
         self.set_option(_lib.BT_OPT_SORT, int(sort))
         self.set_option(_lib.BT_OPT_WARP_AGG, int(warp_aggregate))
+        self.set_option(_lib.BT_OPT_STAGED, int(staged))
         self._grid = TallyGrid(self)
 
     # ------------------------------------------------------------------ props

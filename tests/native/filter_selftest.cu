@@ -1,0 +1,62 @@
+// Host self-test of the filtered exit search (csrc/geometry.cuh): walks
+// particles through a mesh on the CPU, and at EVERY step compares
+// exit_search_fast() against exit_search() (the reference's literal
+// arithmetic), following the literal result.  Built by
+// tests/test_filter_selftest.py with nvcc (host code, -ffp-contract=off).
+#include <cstdint>
+#include <cstring>
+
+#include "../../paper_2504_19048_b200/csrc/geometry.cuh"
+
+using namespace bt;
+
+extern "C" int bt_filter_selftest(const double* vertices, const int32_t* elements,
+                                  const int32_t* adj_elem, const int8_t* adj_face,
+                                  const int32_t* start_elem, const double* start_pos,
+                                  const double* dest, int64_t n, int64_t max_steps,
+                                  int64_t* stats /* steps, mismatches, fallbacks, stuck */) {
+    int64_t steps = 0, mism = 0, fb = 0, stuck = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        int e = start_elem[i];
+        if (e < 0) continue;
+        double ox = start_pos[3 * i], oy = start_pos[3 * i + 1], oz = start_pos[3 * i + 2];
+        const double dx = dest[3 * i], dy = dest[3 * i + 1], dz = dest[3 * i + 2];
+        int entry = -1;
+        for (int64_t k = 0; k < max_steps; ++k) {
+            Tet T;
+            for (int j = 0; j < 4; ++j) {
+                const int v = elements[4 * e + j];
+                T.x[j] = vertices[3 * v];
+                T.y[j] = vertices[3 * v + 1];
+                T.z[j] = vertices[3 * v + 2];
+            }
+            int f1 = 0, f2 = 0;
+            double t1 = 0, t2 = 0;
+            bool ex = false;
+            const int k1 = exit_search(T, ox, oy, oz, dx, dy, dz, entry, &f1, &t1);
+            const int k2 = exit_search_fast(T, ox, oy, oz, dx, dy, dz, entry, &f2, &t2, &ex);
+            ++steps;
+            if (ex) ++fb;
+            if (k1 != k2 || f1 != f2 || std::memcmp(&t1, &t2, sizeof t1) != 0) ++mism;
+            if (k1 != 1) {
+                if (k1 == 2) ++stuck;
+                break;
+            }
+            const double qx = rn_add(ox, rn_mul(t1, rn_sub(dx, ox)));
+            const double qy = rn_add(oy, rn_mul(t1, rn_sub(dy, oy)));
+            const double qz = rn_add(oz, rn_mul(t1, rn_sub(dz, oz)));
+            const int nb = adj_elem[4 * e + f1];
+            if (nb < 0) break;
+            entry = adj_face[4 * e + f1];
+            e = nb;
+            ox = qx;
+            oy = qy;
+            oz = qz;
+        }
+    }
+    stats[0] = steps;
+    stats[1] = mism;
+    stats[2] = fb;
+    stats[3] = stuck;
+    return 0;
+}
