@@ -133,7 +133,7 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // walk kernels: the fused sweep (search.py:169-275) run to completion per lane
 
 constexpr int WALK_THREADS = 256;
-constexpr int DEFAULT_MINB = 2;
+constexpr int DEFAULT_MINB = 1;
 
 // one particle's walk state, held in registers while it flies
 struct Lane {
