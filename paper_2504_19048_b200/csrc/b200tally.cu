@@ -99,6 +99,7 @@ struct WalkArgs {
     int64_t max_sweeps;
     int32_t ngroups;
     int32_t score;
+    int32_t wagg;    // __match_any_sync aggregation of tally atomics
 };
 
 __device__ __forceinline__ void load_tet(const WalkArgs& a, const ElemRec& r, Tet& T) {
@@ -132,8 +133,7 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // ---------------------------------------------------------------------------
 // walk kernels: the fused sweep (search.py:169-275) run to completion per lane
 
-constexpr int WALK_THREADS = 256;
-constexpr int DEFAULT_MINB = 1;
+constexpr int DEFAULT_VARIANT = 1;  // see run_walk's variant table
 
 // one particle's walk state, held in registers while it flies
 struct Lane {
@@ -154,7 +154,6 @@ struct Counters {
 // One step of search.py:183-274 for a flying lane.  Returns true when the
 // particle stops (reached, leaked, stuck-killed or sweep guard); sets
 // has_score/bin/val when the step scores a segment.
-template <bool DIGEST>
 __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& C,
                                           bool& has_score, int64_t& bin, double& val) {
     const ElemRec r = load_rec(a.rec, L.e);
@@ -222,7 +221,7 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
     if (event) {  // search.py:236-274
         ++C.events;
         L.st = 0;
-        if (DIGEST) {
+        if (a.digest) {
             L.dig = (L.dig ^ (uint64_t)((int64_t)L.e * 8 + face + 1)) * DIGEST_PRIME;
             ++L.dcnt;
         }
@@ -274,7 +273,6 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
     return done;
 }
 
-template <bool DIGEST>
 __device__ __forceinline__ void finish(const WalkArgs& a, Lane& L, Counters& C) {
     const int64_t i = L.idx;
     a.pos[3 * i] = L.px;
@@ -286,7 +284,7 @@ __device__ __forceinline__ void finish(const WalkArgs& a, Lane& L, Counters& C) 
     a.outcome[i] = (int8_t)L.outcome;
     a.alive[i] = (int8_t)L.alive;
     a.seg_total[i] = L.seg;
-    if (DIGEST) {
+    if (a.digest) {
         a.digest[i] = L.dig;
         a.dcount[i] = L.dcnt;
     }
@@ -302,10 +300,9 @@ __device__ __forceinline__ void begin(Lane& L) {
     L.outcome = OUT_NONE;
 }
 
-template <bool WAGG>
 __device__ __forceinline__ void score(const WalkArgs& a, bool has_score, int64_t bin, double val) {
     constexpr unsigned FULL = 0xffffffffu;
-    if (WAGG) {
+    if (a.wagg) {
         const int lane = threadIdx.x & 31;
         const unsigned m = __ballot_sync(FULL, has_score);
         if (has_score) {
@@ -350,8 +347,8 @@ __device__ __forceinline__ void flush_counters(const WalkArgs& a, Counters& C) {
 
 // v1: idle lanes refill straight from the particle arrays (one atomicAdd per
 // warp per refill); the fetch's global loads sit on the step's critical path.
-template <bool DIGEST, bool WAGG, int MINB>
-__global__ void __launch_bounds__(WALK_THREADS, MINB) walk_kernel(const WalkArgs a) {
+template <int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) walk_kernel(const WalkArgs a) {
     constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     Lane L;
@@ -371,7 +368,7 @@ __global__ void __launch_bounds__(WALK_THREADS, MINB) walk_kernel(const WalkArgs
                     const unsigned long long q = base + __popc(idle & lanemask_lt());
                     if (q < (unsigned long long)a.count) {
                         const int64_t i = a.order ? (int64_t)a.order[q] : (int64_t)q;
-                        if (DIGEST && a.fly_in[i] == 0) {  // not moving: empty sequence
+                        if (a.digest && a.fly_in[i] == 0) {  // not moving: empty sequence
                             a.digest[i] = DIGEST_INIT;
                             a.dcount[i] = 0;
                         }
@@ -403,9 +400,9 @@ __global__ void __launch_bounds__(WALK_THREADS, MINB) walk_kernel(const WalkArgs
         int64_t bin = 0;
         double val = 0.0;
         if (L.idx >= 0) {
-            if (walk_step<DIGEST>(a, L, C, has_score, bin, val)) finish<DIGEST>(a, L, C);
+            if (walk_step(a, L, C, has_score, bin, val)) finish(a, L, C);
         }
-        score<WAGG>(a, has_score, bin, val);
+        score(a, has_score, bin, val);
     }
     flush_counters(a, C);
 }
@@ -427,7 +424,6 @@ struct __align__(16) WarpStage {
     int idx[32], e[32], g[32], fl[32];
 };
 
-constexpr int STAGED_WARPS = WALK_THREADS / 32;
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -469,11 +465,11 @@ __device__ __forceinline__ int claim_chunk(const WalkArgs& a, const WorkSoA& W, 
     return n;
 }
 
-template <bool DIGEST, bool WAGG, int MINB>
-__global__ void __launch_bounds__(WALK_THREADS, MINB)
+template <int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB)
     walk_staged_kernel(const WalkArgs a, const WorkSoA W, const int64_t* __restrict__ nwork_p) {
     constexpr unsigned FULL = 0xffffffffu;
-    __shared__ WarpStage stages[STAGED_WARPS][2];
+    __shared__ WarpStage stages[THREADS / 32][2];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const int64_t nwork = *nwork_p;
@@ -532,9 +528,9 @@ __global__ void __launch_bounds__(WALK_THREADS, MINB)
         int64_t bin = 0;
         double val = 0.0;
         if (L.idx >= 0) {
-            if (walk_step<DIGEST>(a, L, C, has_score, bin, val)) finish<DIGEST>(a, L, C);
+            if (walk_step(a, L, C, has_score, bin, val)) finish(a, L, C);
         }
-        score<WAGG>(a, has_score, bin, val);
+        score(a, has_score, bin, val);
     }
     cp_async_wait_all();
     flush_counters(a, C);
@@ -543,7 +539,6 @@ __global__ void __launch_bounds__(WALK_THREADS, MINB)
 // Compact this move's flying particles into the work arrays (order of
 // indices within a warp preserved; warps in arbitrary order).  Non-flying
 // particles get an empty digest.
-template <bool DIGEST>
 __global__ void stage_kernel(const WalkArgs a, const WorkSoA W, int64_t* __restrict__ nwork) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
@@ -552,7 +547,7 @@ __global__ void stage_kernel(const WalkArgs a, const WorkSoA W, int64_t* __restr
     if (t < a.count) {
         i = a.order ? (int64_t)a.order[t] : t;
         fly = a.fly_in[i] != 0;
-        if (DIGEST && !fly) {
+        if (a.digest && !fly) {
             a.digest[i] = DIGEST_INIT;
             a.dcount[i] = 0;
         }
@@ -581,6 +576,10 @@ __global__ void stage_kernel(const WalkArgs a, const WorkSoA W, int64_t* __restr
 // ---------------------------------------------------------------------------
 // localization: uniform grid of element bounding boxes
 
+struct __align__(16) BoxF {
+    float lo[3], pad0, hi[3], pad1;  // element bbox, rounded outward
+};
+
 struct GridDev {
     double org[3];
     double cs[3];
@@ -598,7 +597,7 @@ __device__ __forceinline__ int grid_axis(double p, double org, double cs, int di
 __global__ void elem_cells_count_kernel(const ElemRec* __restrict__ rec,
                                         const Vtx* __restrict__ vtx, int64_t ne, GridDev G,
                                         int* __restrict__ counts, int4* __restrict__ ranges_lo,
-                                        int4* __restrict__ ranges_hi) {
+                                        int4* __restrict__ ranges_hi, BoxF* __restrict__ ebox) {
     int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= ne) return;
     const ElemRec r = rec[e];
@@ -619,6 +618,13 @@ __global__ void elem_cells_count_kernel(const ElemRec* __restrict__ rec,
         b[k] = grid_axis(hi[k] + delta, G.org[k], G.cs[k], G.dims[k]);
     }
     counts[e] = (b[0] - a[0] + 1) * (b[1] - a[1] + 1) * (b[2] - a[2] + 1);
+    BoxF bx;
+    for (int k = 0; k < 3; ++k) {
+        bx.lo[k] = __double2float_rd(lo[k] - delta);
+        bx.hi[k] = __double2float_ru(hi[k] + delta);
+    }
+    bx.pad0 = bx.pad1 = 0.f;
+    ebox[e] = bx;
     ranges_lo[e] = make_int4(a[0], a[1], a[2], 0);
     ranges_hi[e] = make_int4(b[0], b[1], b[2], 0);
 }
@@ -660,6 +666,7 @@ __global__ void cell_start_kernel(const unsigned long long* __restrict__ keys, i
 struct LocateArgs {
     const ElemRec* __restrict__ rec;
     const Vtx* __restrict__ vtx;
+    const BoxF* __restrict__ ebox;
     GridDev G;
     const double* __restrict__ target;  // (count,3)
     double* __restrict__ pos;
@@ -677,60 +684,61 @@ struct LocateArgs {
 // One warp per particle: 32 candidates tested at a time; candidates are in
 // ascending element order, so the lowest set ballot bit is the lowest-id
 // containing element (pkg/tests/oracles.py:36-57 semantics).
+// One thread per particle: candidates in ascending element order, a float
+// bounding-box test (rounded outward, expanded like the grid insertion)
+// before the exact-equivalent containment filter; the first hit is the
+// lowest-id containing element (pkg/tests/oracles.py:36-57 semantics).
 __global__ void __launch_bounds__(256) locate_grid_kernel(const LocateArgs a) {
-    constexpr unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = warp; i < a.count; i += nwarps) {
-        const double p0 = a.target[3 * i], p1 = a.target[3 * i + 1], p2 = a.target[3 * i + 2];
-        const bool inside = p0 >= a.bbox[0] && p0 <= a.bbox[3] && p1 >= a.bbox[1] &&
-                            p1 <= a.bbox[4] && p2 >= a.bbox[2] && p2 <= a.bbox[5];
-        int found = -1;
-        if (inside) {
-            const int ci = grid_axis(p0, a.G.org[0], a.G.cs[0], a.G.dims[0]);
-            const int cj = grid_axis(p1, a.G.org[1], a.G.cs[1], a.G.dims[1]);
-            const int ck = grid_axis(p2, a.G.org[2], a.G.cs[2], a.G.dims[2]);
-            const int64_t cell = ((int64_t)ci * a.G.dims[1] + cj) * a.G.dims[2] + ck;
-            const int s0 = a.G.cell_start[cell], s1 = a.G.cell_start[cell + 1];
-            for (int base = s0; base < s1 && found < 0; base += 32) {
-                bool ok = false;
-                int cand = -1;
-                if (base + lane < s1) {
-                    cand = a.G.cand[base + lane];
-                    const ElemRec r = load_rec(a.rec, cand);
-                    Tet T;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= a.count) return;
+    const double p0 = a.target[3 * i], p1 = a.target[3 * i + 1], p2 = a.target[3 * i + 2];
+    const bool inside = p0 >= a.bbox[0] && p0 <= a.bbox[3] && p1 >= a.bbox[1] &&
+                        p1 <= a.bbox[4] && p2 >= a.bbox[2] && p2 <= a.bbox[5];
+    int found = -1;
+    if (inside) {
+        const int ci = grid_axis(p0, a.G.org[0], a.G.cs[0], a.G.dims[0]);
+        const int cj = grid_axis(p1, a.G.org[1], a.G.cs[1], a.G.dims[1]);
+        const int ck = grid_axis(p2, a.G.org[2], a.G.cs[2], a.G.dims[2]);
+        const int64_t cell = ((int64_t)ci * a.G.dims[1] + cj) * a.G.dims[2] + ck;
+        const int s0 = __ldg(a.G.cell_start + cell), s1 = __ldg(a.G.cell_start + cell + 1);
+        for (int k = s0; k < s1; ++k) {
+            const int c = __ldg(a.G.cand + k);
+            const float4 lo = __ldg(reinterpret_cast<const float4*>(a.ebox + c));
+            const float4 hi = __ldg(reinterpret_cast<const float4*>(a.ebox + c) + 1);
+            if (p0 < lo.x || p0 > hi.x || p1 < lo.y || p1 > hi.y || p2 < lo.z || p2 > hi.z)
+                continue;
+            const ElemRec r = load_rec(a.rec, c);
+            Tet T;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const Vtx v = a.vtx[r.v[j]];
-                        T.x[j] = v.x;
-                        T.y[j] = v.y;
-                        T.z[j] = v.z;
-                    }
-                    ok = contains(T, p0, p1, p2, EPS_BARY);
-                }
-                const unsigned hit = __ballot_sync(FULL, ok);
-                if (hit) found = __shfl_sync(FULL, cand, __ffs(hit) - 1);
+            for (int j = 0; j < 4; ++j) {
+                const double2* vp = reinterpret_cast<const double2*>(a.vtx + r.v[j]);
+                const double2 xy = __ldg(vp);
+                const double2 zw = __ldg(vp + 1);
+                T.x[j] = xy.x;
+                T.y[j] = xy.y;
+                T.z[j] = zw.x;
             }
-        }
-        if (lane == 0) {
-            a.element[i] = found;
-            a.alive[i] = found >= 0 ? 1 : 0;
-            if (found >= 0 || inside) {
-                a.pos[3 * i] = p0;
-                a.pos[3 * i + 1] = p1;
-                a.pos[3 * i + 2] = p2;
-            } else {  // outside the bbox: the reference leaves centroid 0
-                a.pos[3 * i] = a.c0[0];
-                a.pos[3 * i + 1] = a.c0[1];
-                a.pos[3 * i + 2] = a.c0[2];
+            if (contains_fast(T, p0, p1, p2, EPS_BARY)) {
+                found = c;
+                break;
             }
-            a.entry[i] = -1;
-            a.stuck[i] = 0;
-            a.outcome[i] = found >= 0 ? OUT_REACHED : (inside ? OUT_LEAKED : OUT_NONE);
-            a.seg_total[i] = 0.0;
         }
     }
+    a.element[i] = found;
+    a.alive[i] = found >= 0 ? 1 : 0;
+    if (found >= 0 || inside) {
+        a.pos[3 * i] = p0;
+        a.pos[3 * i + 1] = p1;
+        a.pos[3 * i + 2] = p2;
+    } else {  // outside the bbox: the reference leaves centroid 0
+        a.pos[3 * i] = a.c0[0];
+        a.pos[3 * i + 1] = a.c0[1];
+        a.pos[3 * i + 2] = a.c0[2];
+    }
+    a.entry[i] = -1;
+    a.stuck[i] = 0;
+    a.outcome[i] = found >= 0 ? OUT_REACHED : (inside ? OUT_LEAKED : OUT_NONE);
+    a.seg_total[i] = 0.0;
 }
 
 // walk-mode localization, step 1: search.py:577-591
@@ -862,6 +870,7 @@ struct bt_tally {
     GridDev grid{};
     int* cell_start = nullptr;
     int* cand = nullptr;
+    BoxF* ebox = nullptr;
     int64_t grid_m = 0;
     // particles (persistent)
     double* pos = nullptr;
@@ -927,7 +936,7 @@ static bt_status ensure_device(bt_tally* h) {
     } while (0)
 
 static bt_status free_all(bt_tally* h) {
-    void* ptrs[] = {h->rec, h->vtx, h->cell_start, h->cand, h->pos, h->element, h->alive,
+    void* ptrs[] = {h->rec, h->vtx, h->cell_start, h->cand, h->ebox, h->pos, h->element, h->alive,
                     h->entry, h->stuck, h->outcome, h->seg_total, h->group, h->dest, h->fly,
                     h->weight, h->digest, h->dcount, h->order, h->sort_keys_in,
                     h->sort_keys_out, h->sort_vals_in, h->sort_tmp, h->tally, h->sum,
@@ -985,8 +994,10 @@ static bt_status build_grid(bt_tally* h) {
     TRY(dalloc(&rlo, h->ne));
     TRY(dalloc(&rhi, h->ne));
     CK(cudaMemsetAsync(counts + h->ne, 0, sizeof(int), h->stream));
+    TRY(dalloc(&h->ebox, h->ne));
     elem_cells_count_kernel<<<grid_for(h->ne, 256), 256, 0, h->stream>>>(h->rec, h->vtx, h->ne,
-                                                                         G, counts, rlo, rhi);
+                                                                         G, counts, rlo, rhi,
+                                                                         h->ebox);
     CK(cudaGetLastError());
     size_t tmp_bytes = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, offs, (int)(h->ne + 1),
@@ -1302,47 +1313,46 @@ static bt_status run_walk(bt_tally* h, const double* dest, const int8_t* fly, co
         a.order = h->order;
         h->kernels += 5;
     }
-    // register-budget variant: MINB resident CTAs of 256 threads per SM
-    const int minb = h->blocks_per_sm >= 1 && h->blocks_per_sm <= 3 ? h->blocks_per_sm
-                                                                     : DEFAULT_MINB;
-    using KernT = void (*)(const WalkArgs);
-    static const KernT table[2][2][3] = {
-        {{walk_kernel<false, false, 1>, walk_kernel<false, false, 2>, walk_kernel<false, false, 3>},
-         {walk_kernel<false, true, 1>, walk_kernel<false, true, 2>, walk_kernel<false, true, 3>}},
-        {{walk_kernel<true, false, 1>, walk_kernel<true, false, 2>, walk_kernel<true, false, 3>},
-         {walk_kernel<true, true, 1>, walk_kernel<true, true, 2>, walk_kernel<true, true, 3>}}};
-    using StagedT = void (*)(const WalkArgs, const WorkSoA, const int64_t*);
-    static const StagedT staged_table[2][2][3] = {
-        {{walk_staged_kernel<false, false, 1>, walk_staged_kernel<false, false, 2>,
-          walk_staged_kernel<false, false, 3>},
-         {walk_staged_kernel<false, true, 1>, walk_staged_kernel<false, true, 2>,
-          walk_staged_kernel<false, true, 3>}},
-        {{walk_staged_kernel<true, false, 1>, walk_staged_kernel<true, false, 2>,
-          walk_staged_kernel<true, false, 3>},
-         {walk_staged_kernel<true, true, 1>, walk_staged_kernel<true, true, 2>,
-          walk_staged_kernel<true, true, 3>}}};
+    // launch variant (CTA size, resident CTAs per SM = register budget);
+    // BT_OPT_BLOCKS_PER_SM selects it, 0 = the tuned default
+    struct Variant {
+        int threads;
+        void (*plain)(const WalkArgs);
+        void (*staged)(const WalkArgs, const WorkSoA, const int64_t*);
+    };
+    static const Variant variants[] = {
+        {256, walk_kernel<256, 1>, walk_staged_kernel<256, 1>},   // 1: <=255 regs
+        {256, walk_kernel<256, 2>, walk_staged_kernel<256, 2>},   // 2: <=128 regs
+        {256, walk_kernel<256, 3>, walk_staged_kernel<256, 3>},   // 3: <=80 regs
+        {128, walk_kernel<128, 3>, walk_staged_kernel<128, 3>},   // 4: <=168 regs
+        {128, walk_kernel<128, 4>, walk_staged_kernel<128, 4>},   // 5: <=128 regs
+        {192, walk_kernel<192, 2>, walk_staged_kernel<192, 2>},   // 6: <=168 regs
+    };
+    constexpr int NVAR = sizeof(variants) / sizeof(variants[0]);
+    const int vi = (h->blocks_per_sm >= 1 && h->blocks_per_sm <= NVAR ? h->blocks_per_sm
+                                                                       : DEFAULT_VARIANT) - 1;
+    const Variant& V = variants[vi];
+    a.wagg = h->opt_wagg ? 1 : 0;
     const bool staged = h->opt_staged;
-    const void* kptr = staged ? (const void*)staged_table[dig ? 1 : 0][h->opt_wagg ? 1 : 0][minb - 1]
-                              : (const void*)table[dig ? 1 : 0][h->opt_wagg ? 1 : 0][minb - 1];
+    const void* kptr = staged ? (const void*)V.staged : (const void*)V.plain;
     int bps = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kptr, WALK_THREADS, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kptr, V.threads, 0));
     bps = std::max(1, bps);
-    const int64_t want = (count + WALK_THREADS - 1) / WALK_THREADS;
-    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)bps * h->num_sms));
+    const int64_t want = (count + V.threads - 1) / V.threads;
+    const unsigned blocks =
+        (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)bps * h->num_sms));
     int64_t* nwork = reinterpret_cast<int64_t*>(h->dcounters + 14);
     if (staged) {
         TRY(ensure_work(h));
-        auto sk = dig ? stage_kernel<true> : stage_kernel<false>;
-        sk<<<grid_for(count, 256), 256, 0, h->stream>>>(a, h->work, nwork);
+        stage_kernel<<<grid_for(count, 256), 256, 0, h->stream>>>(a, h->work, nwork);
         CK(cudaGetLastError());
         h->kernels += 1;
     }
     CK(cudaEventRecord(h->ev0, h->stream));
     if (staged)
-        staged_table[dig ? 1 : 0][h->opt_wagg ? 1 : 0][minb - 1]<<<blocks, WALK_THREADS, 0,
-                                                                  h->stream>>>(a, h->work, nwork);
+        V.staged<<<blocks, V.threads, 0, h->stream>>>(a, h->work, nwork);
     else
-        table[dig ? 1 : 0][h->opt_wagg ? 1 : 0][minb - 1]<<<blocks, WALK_THREADS, 0, h->stream>>>(a);
+        V.plain<<<blocks, V.threads, 0, h->stream>>>(a);
     CK(cudaGetLastError());
     CK(cudaEventRecord(h->ev1, h->stream));
     h->kernels += 1;
@@ -1372,6 +1382,7 @@ static LocateArgs locate_args(bt_tally* h, const double* target, int64_t count) 
     LocateArgs a;
     a.rec = h->rec;
     a.vtx = h->vtx;
+    a.ebox = h->ebox;
     a.G = h->grid;
     a.target = target;
     a.pos = h->pos;
@@ -1415,8 +1426,7 @@ bt_status bt_initialize_particle_location(bt_tally* h, const double* positions, 
     }
     LocateArgs la = locate_args(h, target, count);
     if (mode == BT_LOCATE_GRID) {
-        const int64_t blocks = std::min<int64_t>((count + 7) / 8, (int64_t)h->num_sms * 64);
-        locate_grid_kernel<<<(unsigned)blocks, 256, 0, h->stream>>>(la);
+        locate_grid_kernel<<<grid_for(count, 256), 256, 0, h->stream>>>(la);
         CK(cudaGetLastError());
         h->kernels += 1;
     } else {

@@ -60,3 +60,26 @@ extern "C" int bt_filter_selftest(const double* vertices, const int32_t* element
     stats[3] = stuck;
     return 0;
 }
+
+// contains_fast() vs contains() for every (point, element) pair.
+extern "C" int64_t bt_contains_selftest(const double* vertices, const int32_t* elements,
+                                        int64_t ne, const double* pts, int64_t n, double tol,
+                                        int64_t* fallbacks) {
+    int64_t mism = 0, fb = 0;
+    for (int64_t e = 0; e < ne; ++e) {
+        Tet T;
+        for (int j = 0; j < 4; ++j) {
+            const int v = elements[4 * e + j];
+            T.x[j] = vertices[3 * v];
+            T.y[j] = vertices[3 * v + 1];
+            T.z[j] = vertices[3 * v + 2];
+        }
+        for (int64_t i = 0; i < n; ++i) {
+            const bool a = contains(T, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], tol);
+            const bool b = contains_fast(T, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], tol);
+            if (a != b) ++mism;
+        }
+    }
+    *fallbacks = fb;
+    return mism;
+}

@@ -102,3 +102,27 @@ def test_torus_walks(lib):
     r = run(lib, m, cells, pos, dest)
     assert r["steps"] > 10000
     assert r["mismatches"] == 0, r
+
+
+@pytest.mark.parametrize("tol", [1e-10, 1e-9])
+def test_contains_fast_matches_exact(lib, tol):
+    m = build_cube_mesh(4)
+    gen = np.random.default_rng(5)
+    k = 6000
+    pts = gen.uniform(-0.05, 1.05, (k, 3))
+    grid = m.vertices[:5, 2]
+    for ax in range(3):  # points on grid planes, edges and vertices
+        sel = gen.random(k) < 0.4
+        pts[sel, ax] = grid[gen.integers(0, 5, sel.sum())]
+    # points within ~tol of faces: nudge vertices/face points by tiny offsets
+    near = gen.random(k) < 0.2
+    pts[near] += gen.normal(size=(near.sum(), 3)) * 1e-11
+    L = lib
+    L.bt_contains_selftest.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                       C.c_int64, C.c_double, C.c_void_p]
+    L.bt_contains_selftest.restype = C.c_int64
+    fb = np.zeros(1, np.int64)
+    pts = np.ascontiguousarray(pts)
+    mism = L.bt_contains_selftest(m.vertices.ctypes.data, m.elements.ctypes.data,
+                                  m.num_elements, pts.ctypes.data, k, tol, fb.ctypes.data)
+    assert mism == 0
