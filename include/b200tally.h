@@ -100,7 +100,10 @@ bt_status bt_destroy(bt_tally *h);
  * (tally.py:239-245 -> search.py:557-601).  size = number of doubles
  * (3 * count); size % 3 != 0 or count > capacity -> BT_EINVAL.  Resets the
  * batch's recorded source weight.  `summary` (nullable) receives the trial
- * walk's counters in BT_LOCATE_WALK mode, zeros in grid mode.
+ * walk's counters in BT_LOCATE_WALK mode, zeros in grid mode.  With HOST
+ * positions in grid mode the call returns once the positions have been
+ * copied; the localization kernel completes asynchronously, ordered before
+ * every later call on the handle (so the next move's input copies overlap it).
  */
 bt_status bt_initialize_particle_location(bt_tally *h, const double *positions, int64_t size,
                                           int32_t mem_kind, int32_t mode, bt_summary *summary);
@@ -146,6 +149,13 @@ bt_status bt_set_option(bt_tally *h, int32_t key, int64_t value);
 /* Device time of the last call's walk kernel(s), CUDA events on the
  * handle's stream, and the number of kernels the library launched. */
 bt_status bt_last_timing(bt_tally *h, float *walk_ms, float *call_ms, int64_t *kernels);
+
+/* Device pointers of the persistent particle state (position (N,3) f64,
+ * element i32, alive i8) so a device-side driver (e.g. a transport step in
+ * torch) can build the next move's destinations without a host round trip.
+ * Valid until bt_destroy; write access only between calls. */
+bt_status bt_particle_device_ptrs(bt_tally *h, double **position, int32_t **element,
+                                  int8_t **alive);
 
 /* Snapshot / restore of the per-particle state (device-to-device); used by
  * the benchmark to replay one move over an identical start state. */

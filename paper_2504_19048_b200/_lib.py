@@ -27,7 +27,8 @@ EXPORTS = (
     "bt_move_to_next_location", "bt_finalize_batch", "bt_read_tally",
     "bt_tally_device_ptr", "bt_get_source_weight", "bt_set_source_weight",
     "bt_batches_completed", "bt_read_particles", "bt_read_digest", "bt_set_option",
-    "bt_last_timing", "bt_save_state", "bt_restore_state", "bt_info",
+    "bt_last_timing", "bt_particle_device_ptrs", "bt_save_state", "bt_restore_state",
+    "bt_info",
     "bt_last_error", "bt_version",
 )
 
@@ -57,6 +58,7 @@ _SIGS = {
     "bt_read_digest": [_P, _I64, _P, _P],
     "bt_set_option": [_P, _I32, _I64],
     "bt_last_timing": [_P, C.POINTER(C.c_float), C.POINTER(C.c_float), C.POINTER(_I64)],
+    "bt_particle_device_ptrs": [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P)],
     "bt_save_state": [_P],
     "bt_restore_state": [_P],
     "bt_info": [_P, C.POINTER(_I32), C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I32)],

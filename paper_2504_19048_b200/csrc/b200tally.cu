@@ -133,7 +133,7 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // ---------------------------------------------------------------------------
 // walk kernels: the fused sweep (search.py:169-275) run to completion per lane
 
-constexpr int DEFAULT_VARIANT = 1;  // see run_walk's variant table
+constexpr int DEFAULT_VARIANT = 6;  // see run_walk's variant table
 
 // one particle's walk state, held in registers while it flies
 struct Lane {
@@ -857,8 +857,11 @@ __global__ void iota_keys_kernel(const int32_t* __restrict__ element, int64_t co
 struct bt_tally {
     int dev = 0;
     int num_sms = 148;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;   // kernels
+    cudaStream_t cstream = nullptr;  // host-to-device copies (overlap with kernels)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+    cudaEvent_t evc0 = nullptr, evc1 = nullptr, ev_loc = nullptr;
+    double* init_stage = nullptr;    // (N,3) localization targets (host inputs)
     int64_t nv = 0, ne = 0, cap = 0;
     int32_t ngroups = 1;
     double bbox[6];
@@ -921,6 +924,7 @@ struct bt_tally {
     int blocks_per_sm = 0;
     // timing
     float walk_ms = 0.f, call_ms = 0.f;
+    bool call_pending = false;  // ev2..ev3 of an asynchronous call not yet read
     int64_t kernels = 0;
 };
 
@@ -941,7 +945,7 @@ static bt_status free_all(bt_tally* h) {
                     h->weight, h->digest, h->dcount, h->order, h->sort_keys_in,
                     h->sort_keys_out, h->sort_vals_in, h->sort_tmp, h->tally, h->sum,
                     h->sum_sq, h->dcounters, h->dwsum, h->snap_pos, h->snap_element,
-                    h->snap_flags, h->snap_seg, h->work_mem};
+                    h->snap_flags, h->snap_seg, h->work_mem, h->init_stage};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->hcounters) cudaFreeHost(h->hcounters);
@@ -949,7 +953,11 @@ static bt_status free_all(bt_tally* h) {
     if (h->ev1) cudaEventDestroy(h->ev1);
     if (h->ev2) cudaEventDestroy(h->ev2);
     if (h->ev3) cudaEventDestroy(h->ev3);
+    if (h->evc0) cudaEventDestroy(h->evc0);
+    if (h->evc1) cudaEventDestroy(h->evc1);
+    if (h->ev_loc) cudaEventDestroy(h->ev_loc);
     if (h->stream) cudaStreamDestroy(h->stream);
+    if (h->cstream) cudaStreamDestroy(h->cstream);
     return BT_OK;
 }
 
@@ -1142,6 +1150,11 @@ bt_status bt_create(const double* vertices, int64_t num_vertices, const int32_t*
     CKF(cudaEventCreate(&h->ev1));
     CKF(cudaEventCreate(&h->ev2));
     CKF(cudaEventCreate(&h->ev3));
+    CKF(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
+    CKF(cudaEventCreateWithFlags(&h->evc0, cudaEventDisableTiming));
+    CKF(cudaEventCreateWithFlags(&h->evc1, cudaEventDisableTiming));
+    CKF(cudaEventCreateWithFlags(&h->ev_loc, cudaEventDisableTiming));
+    CKF(cudaEventRecord(h->ev_loc, h->stream));
 
     // ---- mesh records (host packing, one upload)
     {
@@ -1210,6 +1223,7 @@ bt_status bt_destroy(bt_tally* h) {
     if (!h) return BT_OK;
     cudaSetDevice(h->dev);
     cudaStreamSynchronize(h->stream);
+    cudaStreamSynchronize(h->cstream);
     free_all(h);
     delete h;
     return BT_OK;
@@ -1419,7 +1433,29 @@ bt_status bt_initialize_particle_location(bt_tally* h, const double* positions, 
     if (!positions) return set_err(BT_EINVAL, "positions is NULL");
     CK(cudaEventRecord(h->ev2, h->stream));
     const double* target = positions;
-    if (mem_kind == BT_MEM_HOST) {
+    const bool host = mem_kind == BT_MEM_HOST;
+    if (host && mode == BT_LOCATE_GRID) {
+        // Copy on the copy stream into a dedicated staging buffer, then
+        // return as soon as the caller's buffer has been read: the
+        // localization kernel runs on while the next call's copies proceed
+        // (every later kernel or readout is ordered after it on `stream`).
+        if (!h->init_stage) TRY(dalloc(&h->init_stage, 3 * h->cap));
+        CK(cudaStreamWaitEvent(h->cstream, h->ev_loc, 0));  // previous localization done
+        CK(cudaMemcpyAsync(h->init_stage, positions, sizeof(double) * 3 * count,
+                           cudaMemcpyHostToDevice, h->cstream));
+        CK(cudaEventRecord(h->evc0, h->cstream));
+        CK(cudaStreamWaitEvent(h->stream, h->evc0, 0));
+        LocateArgs la = locate_args(h, h->init_stage, count);
+        locate_grid_kernel<<<grid_for(count, 256), 256, 0, h->stream>>>(la);
+        CK(cudaGetLastError());
+        h->kernels += 1;
+        CK(cudaEventRecord(h->ev_loc, h->stream));
+        CK(cudaEventRecord(h->ev3, h->stream));
+        CK(cudaEventSynchronize(h->evc0));
+        h->call_pending = true;
+        return BT_OK;
+    }
+    if (host) {
         CK(cudaMemcpyAsync(h->dest, positions, sizeof(double) * 3 * count,
                            cudaMemcpyHostToDevice, h->stream));
         target = h->dest;
@@ -1438,9 +1474,11 @@ bt_status bt_initialize_particle_location(bt_tally* h, const double* positions, 
         CK(cudaGetLastError());
         h->kernels += 1;
     }
+    CK(cudaEventRecord(h->ev_loc, h->stream));
     CK(cudaEventRecord(h->ev3, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     CK(cudaEventElapsedTime(&h->call_ms, h->ev2, h->ev3));
+    h->call_pending = false;
     return BT_OK;
 }
 
@@ -1474,21 +1512,26 @@ bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, cons
     const double* d_dest = destinations;
     const int8_t* d_fly = flying;
     const double* d_w = weights;
-    if (host) {
+    if (host) {  // on the copy stream: overlaps a still-running localization
         CK(cudaMemcpyAsync(h->dest, destinations, sizeof(double) * 3 * count,
-                           cudaMemcpyHostToDevice, h->stream));
-        CK(cudaMemcpyAsync(h->fly, flying, count, cudaMemcpyHostToDevice, h->stream));
+                           cudaMemcpyHostToDevice, h->cstream));
+        CK(cudaMemcpyAsync(h->fly, flying, count, cudaMemcpyHostToDevice, h->cstream));
         CK(cudaMemcpyAsync(h->weight, weights, sizeof(double) * count, cudaMemcpyHostToDevice,
-                           h->stream));
+                           h->cstream));
+        if (groups)
+            CK(cudaMemcpyAsync(h->group, groups, sizeof(int32_t) * count,
+                               cudaMemcpyHostToDevice, h->cstream));
+        CK(cudaEventRecord(h->evc1, h->cstream));
+        CK(cudaStreamWaitEvent(h->stream, h->evc1, 0));
         d_dest = h->dest;
         d_fly = h->fly;
         d_w = h->weight;
     }
     const int32_t* d_groups_in = nullptr;
-    if (groups) {
-        CK(cudaMemcpyAsync(h->group, groups, sizeof(int32_t) * count,
-                           host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, h->stream));
-        if (!host) d_groups_in = h->group;
+    if (groups && !host) {
+        CK(cudaMemcpyAsync(h->group, groups, sizeof(int32_t) * count, cudaMemcpyDeviceToDevice,
+                           h->stream));
+        d_groups_in = h->group;
     }
     // device-side checks: unlocalized flying particles (+ groups, weight sum)
     CK(cudaMemsetAsync(h->dcounters + 15, 0, sizeof(unsigned long long), h->stream));
@@ -1535,6 +1578,7 @@ bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, cons
     CK(cudaEventRecord(h->ev3, h->stream));
     CK(cudaEventSynchronize(h->ev3));
     CK(cudaEventElapsedTime(&h->call_ms, h->ev2, h->ev3));
+    h->call_pending = false;
     return s;
 }
 
@@ -1637,9 +1681,24 @@ bt_status bt_read_digest(bt_tally* h, int64_t count, uint64_t* digest, int64_t* 
 
 bt_status bt_last_timing(bt_tally* h, float* walk_ms, float* call_ms, int64_t* kernels) {
     if (!h) return set_err(BT_EINVAL, "NULL handle");
+    if (h->call_pending) {
+        TRY(ensure_device(h));
+        CK(cudaEventSynchronize(h->ev3));
+        CK(cudaEventElapsedTime(&h->call_ms, h->ev2, h->ev3));
+        h->call_pending = false;
+    }
     if (walk_ms) *walk_ms = h->walk_ms;
     if (call_ms) *call_ms = h->call_ms;
     if (kernels) *kernels = h->kernels;
+    return BT_OK;
+}
+
+bt_status bt_particle_device_ptrs(bt_tally* h, double** position, int32_t** element,
+                                  int8_t** alive) {
+    if (!h) return set_err(BT_EINVAL, "NULL handle");
+    if (position) *position = h->pos;
+    if (element) *element = h->element;
+    if (alive) *alive = h->alive;
     return BT_OK;
 }
 

@@ -60,8 +60,8 @@ class _CudaArray:
     """__cuda_array_interface__ wrapper of a raw device pointer (zero-copy
     torch view of the library-owned tally)."""
 
-    def __init__(self, ptr: int, n: int):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8",
+    def __init__(self, ptr: int, n: int, typestr: str = "<f8"):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
                                          "data": (ptr, False), "version": 3,
                                          "strides": None}
 

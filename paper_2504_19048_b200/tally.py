@@ -84,6 +84,13 @@ def _is_device(x) -> bool:
     return hasattr(x, "data_ptr") and getattr(x, "is_cuda", False)
 
 
+def _producer_sync(t) -> None:
+    """The library runs on its own stream: wait for the producer stream of a
+    CUDA tensor argument (torch's current stream on its device) first."""
+    import torch
+    torch.cuda.current_stream(t.device).synchronize()
+
+
 class TallyGrid:
     """Read-through view of the device tally (tally.py:21-44 field names)."""
 
@@ -274,6 +281,7 @@ class MeshTally:
         s = _lib.Summary()
         if _is_device(positions):
             self._check_tensor(positions, 8)
+            _producer_sync(positions)
             size = positions.numel()
             _lib.check(self._L.bt_initialize_particle_location(
                 self._h, positions.data_ptr(), size, _lib.BT_MEM_DEVICE, m, C.byref(s)))
@@ -312,6 +320,7 @@ class MeshTally:
                 gp = groups.data_ptr()
             if count == 0:
                 return None
+            _producer_sync(flying)
             _lib.check(self._L.bt_move_to_next_location(
                 self._h, destinations.data_ptr(), flying.data_ptr(), weights.data_ptr(), gp,
                 count, _lib.BT_MEM_DEVICE, C.byref(s)))
@@ -404,6 +413,20 @@ class MeshTally:
         k = C.c_int64()
         _lib.check(self._L.bt_last_timing(self._h, C.byref(w), C.byref(c), C.byref(k)))
         return float(w.value), float(c.value), int(k.value)
+
+    def particle_tensors(self):
+        """Zero-copy torch views (position (N,3) f64, element i32, alive i8) of
+        the device particle state, for device-side drivers."""
+        import torch
+        from .distributed import _CudaArray
+        p, e, a = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        _lib.check(self._L.bt_particle_device_ptrs(self._h, C.byref(p), C.byref(e), C.byref(a)))
+        dev = torch.device("cuda", self.device)
+        n = self.capacity
+        pos = torch.as_tensor(_CudaArray(p.value, 3 * n, "<f8"), device=dev).view(n, 3)
+        el = torch.as_tensor(_CudaArray(e.value, n, "<i4"), device=dev)
+        al = torch.as_tensor(_CudaArray(a.value, n, "|i1"), device=dev)
+        return pos, el, al
 
     def save_state(self) -> None:
         _lib.check(self._L.bt_save_state(self._h))
