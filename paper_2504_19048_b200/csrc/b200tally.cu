@@ -137,6 +137,8 @@ constexpr int DEFAULT_VARIANT = 6;  // see run_walk's variant table
 
 // one particle's walk state, held in registers while it flies
 struct Lane {
+    ElemRec nr;   // prefetched record of the element entered next
+    bool have_nr;
     double px, py, pz, dx, dy, dz, w, seg;
     int64_t idx;  // -1: lane idle
     int e, g, entry, st, iters;
@@ -156,7 +158,8 @@ struct Counters {
 // has_score/bin/val when the step scores a segment.
 __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& C,
                                           bool& has_score, int64_t& bin, double& val) {
-    const ElemRec r = load_rec(a.rec, L.e);
+    const ElemRec r = L.have_nr ? L.nr : load_rec(a.rec, L.e);
+    L.have_nr = false;
     Tet T;
     load_tet(a, r, T);
     double ox = L.px, oy = L.py, oz = L.pz;
@@ -173,8 +176,20 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
     }
     int face;
     double t;
-    bool exact_used;
-    int kind = exit_search_fast(T, ox, oy, oz, L.dx, L.dy, L.dz, L.entry, &face, &t, &exact_used);
+    bool exact_used, need_t;
+    int kind = exit_search_fast(T, ox, oy, oz, L.dx, L.dy, L.dz, L.entry, &face, &t, &exact_used,
+                                true, &need_t);
+    if (kind == 1) {
+        // issue the next element's record load now: it lands while the exact
+        // t division and the commit below run
+        const int nbp = face == 0 ? r.nb[0] : face == 1 ? r.nb[1] : face == 2 ? r.nb[2] : r.nb[3];
+        if (nbp >= 0) {
+            L.nr = load_rec(a.rec, nbp >> 2);
+            L.have_nr = true;
+        }
+        if (need_t)
+            t = exact_t(T, face, ox, oy, oz, rn_sub(L.dx, ox), rn_sub(L.dy, oy), rn_sub(L.dz, oz));
+    }
     bool done = false;
     bool event = true;
     if (kind == 2) {  // stuck ladder, search.py:199-235
@@ -293,6 +308,7 @@ __device__ __forceinline__ void finish(const WalkArgs& a, Lane& L, Counters& C) 
 }
 
 __device__ __forceinline__ void begin(Lane& L) {
+    L.have_nr = false;
     L.iters = 0;
     L.dig = DIGEST_INIT;
     L.dcnt = 0;
