@@ -67,7 +67,8 @@ enum {
     BT_OPT_SORT = 2,         /* 1: hand particles to warps in element order */
     BT_OPT_WARP_AGG = 3,     /* 1: __match_any_sync aggregation of tally atomics */
     BT_OPT_BLOCKS_PER_SM = 4, /* walk register budget: 1..3 resident 256-thread CTAs/SM */
-    BT_OPT_STAGED = 5         /* 1: compact flying particles + cp.async-prefetched refill */
+    BT_OPT_STAGED = 5,        /* 1: compact flying particles + cp.async-prefetched refill */
+    BT_OPT_MOVE_CHUNKS = 6    /* host inputs: copy/walk pipeline depth (0 = auto, <= 16) */
 };
 
 /* Mirrors meshtally.search.TraceSummary (search.py:150-157). */
@@ -165,6 +166,17 @@ bt_status bt_restore_state(bt_tally *h);
 /* Device ordinal and sizes. */
 bt_status bt_info(bt_tally *h, int32_t *device, int64_t *num_elements, int64_t *capacity,
                   int32_t *num_groups);
+
+/*
+ * Face adjacency of a tet mesh on `device` (build_adjacency, mesh.py:188-235):
+ * elements (E,4) i32 host in; adj_elem (E,4) i32 and adj_face (E,4) i8 host
+ * out, -1 on the boundary.  Face f of an element is opposite local vertex f.
+ * BT_EINVAL (MalformedMeshError) for a face shared by 3+ elements, an element
+ * listing a face twice, a duplicated element, or an out-of-range vertex id.
+ * Two stable device radix sorts of the face keys (c, then (a,b)).
+ */
+bt_status bt_build_adjacency(const int32_t *elements, int64_t num_elements, int64_t num_vertices,
+                             int32_t device, int32_t *adj_elem, int8_t *adj_face);
 
 const char *bt_last_error(void);
 const char *bt_version(void);

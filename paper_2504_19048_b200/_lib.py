@@ -19,7 +19,7 @@ BT_MEM_HOST, BT_MEM_DEVICE = 0, 1
 BT_LOCATE_GRID, BT_LOCATE_WALK = 0, 1
 BT_TALLY_BATCH, BT_TALLY_SUM, BT_TALLY_SUM_SQ = 0, 1, 2
 (BT_OPT_MAX_SWEEPS, BT_OPT_DIGEST, BT_OPT_SORT, BT_OPT_WARP_AGG,
- BT_OPT_BLOCKS_PER_SM, BT_OPT_STAGED) = range(6)
+ BT_OPT_BLOCKS_PER_SM, BT_OPT_STAGED, BT_OPT_MOVE_CHUNKS) = range(7)
 
 # every symbol declared in include/b200tally.h (checked by tests/test_abi.py)
 EXPORTS = (
@@ -28,7 +28,7 @@ EXPORTS = (
     "bt_tally_device_ptr", "bt_get_source_weight", "bt_set_source_weight",
     "bt_batches_completed", "bt_read_particles", "bt_read_digest", "bt_set_option",
     "bt_last_timing", "bt_particle_device_ptrs", "bt_save_state", "bt_restore_state",
-    "bt_info",
+    "bt_info", "bt_build_adjacency",
     "bt_last_error", "bt_version",
 )
 
@@ -62,6 +62,7 @@ _SIGS = {
     "bt_save_state": [_P],
     "bt_restore_state": [_P],
     "bt_info": [_P, C.POINTER(_I32), C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I32)],
+    "bt_build_adjacency": [_P, _I64, _I64, _I32, _P, _P],
     "bt_last_error": [],
     "bt_version": [],
 }

@@ -73,7 +73,11 @@ struct __align__(32) Vtx {
 };
 static_assert(sizeof(Vtx) == 32, "one 32-byte sector per vertex");
 
-enum { C_EVENTS = 0, C_REACHED, C_BOUNDARY, C_RECOV, C_KILLED, C_SWEEPS, C_ERR, C_NCOUNTERS };
+enum { C_EVENTS = 0, C_REACHED, C_BOUNDARY, C_RECOV, C_KILLED, C_SWEEPS, C_ERR, C_UNLOC, C_NCOUNTERS };
+// dcounters layout (unsigned long long): [1..8] counters, [15] flags,
+// [16 + c] queue of chunk c, [32 + c] work count of chunk c, c < MAX_CHUNKS
+constexpr int MAX_CHUNKS = 16;
+constexpr int NDCOUNTERS = 48;
 
 struct WalkArgs {
     const ElemRec* __restrict__ rec;
@@ -133,7 +137,7 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // ---------------------------------------------------------------------------
 // walk kernels: the fused sweep (search.py:169-275) run to completion per lane
 
-constexpr int DEFAULT_VARIANT = 6;  // see run_walk's variant table
+constexpr int DEFAULT_VARIANT = 1;  // see run_walk's variant table
 
 // one particle's walk state, held in registers while it flies
 struct Lane {
@@ -388,7 +392,9 @@ __global__ void __launch_bounds__(THREADS, MINB) walk_kernel(const WalkArgs a) {
                             a.digest[i] = DIGEST_INIT;
                             a.dcount[i] = 0;
                         }
-                        if (a.fly_in[i] != 0) {
+                        const bool unloc = a.fly_in[i] != 0 && a.element[i] < 0;
+                        if (unloc) atomicAdd(a.counters + C_UNLOC, 1ull);
+                        if (a.fly_in[i] != 0 && !unloc) {
                             L.idx = i;
                             L.e = a.element[i];
                             L.px = a.pos[3 * i];
@@ -486,7 +492,6 @@ __global__ void __launch_bounds__(THREADS, MINB)
     walk_staged_kernel(const WalkArgs a, const WorkSoA W, const int64_t* __restrict__ nwork_p) {
     constexpr unsigned FULL = 0xffffffffu;
     __shared__ WarpStage stages[THREADS / 32][2];
-    const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const int64_t nwork = *nwork_p;
     Lane L;
@@ -555,18 +560,33 @@ __global__ void __launch_bounds__(THREADS, MINB)
 // Compact this move's flying particles into the work arrays (order of
 // indices within a warp preserved; warps in arbitrary order).  Non-flying
 // particles get an empty digest.
-__global__ void stage_kernel(const WalkArgs a, const WorkSoA W, int64_t* __restrict__ nwork) {
+// Particles [lo, lo + a.count) of this move; work items go to W (already
+// offset by the caller).  A flying particle with element < 0 is not staged
+// and counted (the move then reports it); wsum (nullable) accumulates the
+// flying particles' weights (device-resident inputs).
+__global__ void stage_kernel(const WalkArgs a, const WorkSoA W, int64_t* __restrict__ nwork,
+                             int64_t lo, double* __restrict__ wsum) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     bool fly = false;
     int64_t i = 0;
+    double wv = 0.0;
     if (t < a.count) {
-        i = a.order ? (int64_t)a.order[t] : t;
+        i = a.order ? (int64_t)a.order[t] : lo + t;
         fly = a.fly_in[i] != 0;
         if (a.digest && !fly) {
             a.digest[i] = DIGEST_INIT;
             a.dcount[i] = 0;
         }
+        if (fly && wsum) wv = a.weight[i];
+        if (fly && a.element[i] < 0) {
+            atomicAdd(a.counters + C_UNLOC, 1ull);
+            fly = false;
+        }
+    }
+    if (wsum) {
+        for (int o = 16; o > 0; o >>= 1) wv += __shfl_xor_sync(0xffffffffu, wv, o);
+        if (lane == 0 && wv != 0.0) atomicAdd(wsum, wv);
     }
     const unsigned m = __ballot_sync(0xffffffffu, fly);
     if (!m) return;
@@ -868,6 +888,98 @@ __global__ void iota_keys_kernel(const int32_t* __restrict__ element, int64_t co
 }
 
 // ---------------------------------------------------------------------------
+// mesh ingest: face adjacency by two stable radix sorts (
+// the reference builds it on the host with a lexsort, mesh.py:188-235)
+
+__device__ __forceinline__ void face_triple(const int* __restrict__ el, int64_t row, int& a,
+                                            int& b, int& c) {
+    const int64_t e = row >> 2;
+    const int f = (int)(row & 3);
+    // face f = the three local vertices other than f (FACE_VERTICES, mesh.py:24-26)
+    const int4 v = *reinterpret_cast<const int4*>(el + 4 * e);
+    int x = f == 0 ? v.y : v.x;
+    int y = f <= 1 ? v.z : v.y;
+    int z = f == 3 ? v.z : v.w;
+    // sort (x, y, z)
+    int t;
+    if (x > y) { t = x; x = y; y = t; }
+    if (y > z) { t = y; y = z; z = t; }
+    if (x > y) { t = x; x = y; y = t; }
+    a = x; b = y; c = z;
+}
+
+__global__ void adj_keys_c_kernel(const int* __restrict__ el, int64_t nrows,
+                                  unsigned* __restrict__ kc, int* __restrict__ rows) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= nrows) return;
+    int a, b, c;
+    face_triple(el, r, a, b, c);
+    kc[r] = (unsigned)c;
+    rows[r] = (int)r;
+}
+
+__global__ void adj_keys_ab_kernel(const int* __restrict__ el, int64_t nrows,
+                                   const int* __restrict__ rows,
+                                   unsigned long long* __restrict__ kab) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= nrows) return;
+    int a, b, c;
+    face_triple(el, rows[k], a, b, c);
+    kab[k] = ((unsigned long long)(unsigned)a << 32) | (unsigned)b;
+}
+
+// flags: 1 = face shared by 3+ elements (first sorted index in err[0]),
+//        2 = element lists one face twice (element in err[1])
+__global__ void adj_match_kernel(const int* __restrict__ el, int64_t nrows,
+                                 const int* __restrict__ rows, int* __restrict__ adj_e,
+                                 signed char* __restrict__ adj_f, unsigned* __restrict__ flags,
+                                 long long* __restrict__ err) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k + 1 >= nrows) return;
+    int a0, b0, c0, a1, b1, c1;
+    face_triple(el, rows[k], a0, b0, c0);
+    face_triple(el, rows[k + 1], a1, b1, c1);
+    if (a0 != a1 || b0 != b1 || c0 != c1) return;
+    if (k + 2 < nrows) {
+        int a2, b2, c2;
+        face_triple(el, rows[k + 2], a2, b2, c2);
+        if (a2 == a0 && b2 == b0 && c2 == c0) {
+            atomicOr(flags, 1u);
+            atomicMin(err, (long long)k);
+            return;
+        }
+    }
+    if (k > 0) {
+        int am, bm, cm;
+        face_triple(el, rows[k - 1], am, bm, cm);
+        if (am == a0 && bm == b0 && cm == c0) return;  // part of a 3-run, reported above
+    }
+    const int r0 = rows[k], r1 = rows[k + 1];
+    const int e0 = r0 >> 2, f0 = r0 & 3, e1 = r1 >> 2, f1 = r1 & 3;
+    if (e0 == e1) {
+        atomicOr(flags, 2u);
+        atomicMin(err + 1, (long long)e0);
+        return;
+    }
+    adj_e[4 * (int64_t)e0 + f0] = e1;
+    adj_f[4 * (int64_t)e0 + f0] = (signed char)f1;
+    adj_e[4 * (int64_t)e1 + f1] = e0;
+    adj_f[4 * (int64_t)e1 + f1] = (signed char)f0;
+}
+
+// duplicated element: all four faces shared with one and the same element
+__global__ void adj_dup_kernel(const int* __restrict__ adj_e, int64_t ne,
+                               unsigned* __restrict__ flags, long long* __restrict__ err) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= ne) return;
+    const int4 v = *reinterpret_cast<const int4*>(adj_e + 4 * e);
+    if (v.x >= 0 && v.x == v.y && v.x == v.z && v.x == v.w) {
+        atomicOr(flags, 4u);
+        atomicMin(err + 2, (long long)e);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // handle
 
 struct bt_tally {
@@ -877,6 +989,7 @@ struct bt_tally {
     cudaStream_t cstream = nullptr;  // host-to-device copies (overlap with kernels)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
     cudaEvent_t evc0 = nullptr, evc1 = nullptr, ev_loc = nullptr;
+    cudaEvent_t evchunk[MAX_CHUNKS] = {};
     double* init_stage = nullptr;    // (N,3) localization targets (host inputs)
     int64_t nv = 0, ne = 0, cap = 0;
     int32_t ngroups = 1;
@@ -923,6 +1036,7 @@ struct bt_tally {
     unsigned long long* dcounters = nullptr;  // queue + counters + flags
     double* dwsum = nullptr;
     unsigned long long* hcounters = nullptr;  // pinned
+    int move_chunks = 0;                      // host-input pipeline depth (0 = auto)
     // snapshot
     double* snap_pos = nullptr;
     int32_t* snap_element = nullptr;
@@ -941,6 +1055,7 @@ struct bt_tally {
     // timing
     float walk_ms = 0.f, call_ms = 0.f;
     bool call_pending = false;  // ev2..ev3 of an asynchronous call not yet read
+    bool walk_first = false;    // ev0 not yet recorded for this move
     int64_t kernels = 0;
 };
 
@@ -972,6 +1087,8 @@ static bt_status free_all(bt_tally* h) {
     if (h->evc0) cudaEventDestroy(h->evc0);
     if (h->evc1) cudaEventDestroy(h->evc1);
     if (h->ev_loc) cudaEventDestroy(h->ev_loc);
+    for (cudaEvent_t e : h->evchunk)
+        if (e) cudaEventDestroy(e);
     if (h->stream) cudaStreamDestroy(h->stream);
     if (h->cstream) cudaStreamDestroy(h->cstream);
     return BT_OK;
@@ -997,7 +1114,10 @@ static bt_status build_grid(bt_tally* h) {
     }
     double maxext = std::max(ext[0], std::max(ext[1], ext[2]));
     for (int k = 0; k < 3; ++k) vol *= std::max(ext[k], 1e-6 * maxext);
-    double target = std::max(1.0, (double)h->ne / 6.0);
+    // cells per element (experiments: B200TALLY_GRID_DENSITY)
+    double density = 1.0 / 6.0;
+    if (const char* env = getenv("B200TALLY_GRID_DENSITY")) density = std::max(1e-3, atof(env));
+    double target = std::max(1.0, (double)h->ne * density);
     target = std::min(target, (double)(1 << 26));
     double cell = std::cbrt(vol / target);
     GridDev G{};
@@ -1092,14 +1212,6 @@ static double pairwise_sum(const double* a, int64_t n) {
     }
 }
 
-static bool is_device_ptr(const void* p) {
-    cudaPointerAttributes at;
-    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-    }
-    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
-}
 
 // ---------------------------------------------------------------------------
 // C ABI
@@ -1170,6 +1282,7 @@ bt_status bt_create(const double* vertices, int64_t num_vertices, const int32_t*
     CKF(cudaEventCreateWithFlags(&h->evc0, cudaEventDisableTiming));
     CKF(cudaEventCreateWithFlags(&h->evc1, cudaEventDisableTiming));
     CKF(cudaEventCreateWithFlags(&h->ev_loc, cudaEventDisableTiming));
+    for (cudaEvent_t& e : h->evchunk) CKF(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CKF(cudaEventRecord(h->ev_loc, h->stream));
 
     // ---- mesh records (host packing, one upload)
@@ -1213,9 +1326,9 @@ bt_status bt_create(const double* vertices, int64_t num_vertices, const int32_t*
     TRYF(dalloc(&h->tally, nbins));
     TRYF(dalloc(&h->sum, nbins));
     TRYF(dalloc(&h->sum_sq, nbins));
-    TRYF(dalloc(&h->dcounters, 16));
+    TRYF(dalloc(&h->dcounters, NDCOUNTERS));
     TRYF(dalloc(&h->dwsum, 1));
-    CKF(cudaMallocHost((void**)&h->hcounters, 16 * sizeof(unsigned long long)));
+    CKF(cudaMallocHost((void**)&h->hcounters, NDCOUNTERS * sizeof(unsigned long long)));
     CKF(cudaMemset(h->pos, 0, sizeof(double) * 3 * n));
     CKF(cudaMemset(h->element, 0xff, sizeof(int32_t) * n));  // -1: unlocalized
     CKF(cudaMemset(h->alive, 0, n));
@@ -1276,6 +1389,7 @@ bt_status bt_set_option(bt_tally* h, int32_t key, int64_t value) {
         case BT_OPT_WARP_AGG: h->opt_wagg = value != 0; break;
         case BT_OPT_BLOCKS_PER_SM: h->blocks_per_sm = (int)value; break;
         case BT_OPT_STAGED: h->opt_staged = value != 0; break;
+        case BT_OPT_MOVE_CHUNKS: h->move_chunks = (int)value; break;
         default: return set_err(BT_EINVAL, "unknown option %d", key);
     }
     return BT_OK;
@@ -1303,9 +1417,23 @@ struct HostOverlap {
     void* ctx = nullptr;
 };
 
-static bt_status run_walk(bt_tally* h, const double* dest, const int8_t* fly, const double* w,
-                          int64_t count, bool score, bt_summary* summary,
-                          HostOverlap overlap = HostOverlap()) {
+static const struct Variant {
+    int threads;
+    void (*plain)(const WalkArgs);
+    void (*staged)(const WalkArgs, const WorkSoA, const int64_t*);
+} kVariants[] = {
+    // launch variant (CTA size, resident CTAs per SM = register budget);
+    // BT_OPT_BLOCKS_PER_SM selects it, 0 = the tuned default
+    {256, walk_kernel<256, 1>, walk_staged_kernel<256, 1>},  // 1: <=255 regs
+    {256, walk_kernel<256, 2>, walk_staged_kernel<256, 2>},  // 2: <=128 regs
+    {256, walk_kernel<256, 3>, walk_staged_kernel<256, 3>},  // 3: <=80 regs
+    {128, walk_kernel<128, 3>, walk_staged_kernel<128, 3>},  // 4: <=168 regs
+    {128, walk_kernel<128, 4>, walk_staged_kernel<128, 4>},  // 5: <=128 regs
+    {192, walk_kernel<192, 2>, walk_staged_kernel<192, 2>},  // 6: <=168 regs
+};
+
+static WalkArgs walk_args(bt_tally* h, const double* dest, const int8_t* fly, const double* w,
+                          bool score) {
     WalkArgs a;
     a.rec = h->rec;
     a.vtx = h->vtx;
@@ -1325,14 +1453,32 @@ static bt_status run_walk(bt_tally* h, const double* dest, const int8_t* fly, co
     a.digest = dig ? h->digest : nullptr;
     a.dcount = dig ? h->dcount : nullptr;
     a.order = nullptr;
-    a.queue = h->dcounters;
+    a.queue = h->dcounters + 16;
     a.counters = h->dcounters + 1;
-    a.count = count;
+    a.count = 0;
     a.max_sweeps = h->max_sweeps >= 0 ? h->max_sweeps : 2 * h->ne + 1000;
     a.ngroups = h->ngroups;
     a.score = score ? 1 : 0;
-    CK(cudaMemsetAsync(h->dcounters, 0, sizeof(unsigned long long) * 16, h->stream));
-    if (h->opt_sort && score) {
+    a.wagg = h->opt_wagg ? 1 : 0;
+    return a;
+}
+
+// zero the move's counters; the first walk launch records ev0
+static bt_status walk_begin(bt_tally* h) {
+    CK(cudaMemsetAsync(h->dcounters, 0, sizeof(unsigned long long) * NDCOUNTERS, h->stream));
+    h->walk_first = true;
+    return BT_OK;
+}
+
+// enqueue stage + walk of particles [lo, hi) as chunk `chunk` (staged path),
+// or the whole range with the v1 kernel / element-sorted hand-out
+static bt_status walk_enqueue(bt_tally* h, WalkArgs a, int64_t lo, int64_t hi, int chunk,
+                              double* wsum) {
+    const int64_t count = hi - lo;
+    a.count = count;
+    a.queue = h->dcounters + 16 + chunk;
+    const bool staged = h->opt_staged;
+    if (h->opt_sort && a.score) {  // whole move only (lo == 0)
         iota_keys_kernel<<<grid_for(count, 256), 256, 0, h->stream>>>(
             h->element, count, h->sort_keys_in, h->sort_vals_in);
         CK(cudaGetLastError());
@@ -1343,27 +1489,10 @@ static bt_status run_walk(bt_tally* h, const double* dest, const int8_t* fly, co
         a.order = h->order;
         h->kernels += 5;
     }
-    // launch variant (CTA size, resident CTAs per SM = register budget);
-    // BT_OPT_BLOCKS_PER_SM selects it, 0 = the tuned default
-    struct Variant {
-        int threads;
-        void (*plain)(const WalkArgs);
-        void (*staged)(const WalkArgs, const WorkSoA, const int64_t*);
-    };
-    static const Variant variants[] = {
-        {256, walk_kernel<256, 1>, walk_staged_kernel<256, 1>},   // 1: <=255 regs
-        {256, walk_kernel<256, 2>, walk_staged_kernel<256, 2>},   // 2: <=128 regs
-        {256, walk_kernel<256, 3>, walk_staged_kernel<256, 3>},   // 3: <=80 regs
-        {128, walk_kernel<128, 3>, walk_staged_kernel<128, 3>},   // 4: <=168 regs
-        {128, walk_kernel<128, 4>, walk_staged_kernel<128, 4>},   // 5: <=128 regs
-        {192, walk_kernel<192, 2>, walk_staged_kernel<192, 2>},   // 6: <=168 regs
-    };
-    constexpr int NVAR = sizeof(variants) / sizeof(variants[0]);
+    constexpr int NVAR = sizeof(kVariants) / sizeof(kVariants[0]);
     const int vi = (h->blocks_per_sm >= 1 && h->blocks_per_sm <= NVAR ? h->blocks_per_sm
                                                                        : DEFAULT_VARIANT) - 1;
-    const Variant& V = variants[vi];
-    a.wagg = h->opt_wagg ? 1 : 0;
-    const bool staged = h->opt_staged;
+    const Variant& V = kVariants[vi];
     const void* kptr = staged ? (const void*)V.staged : (const void*)V.plain;
     int bps = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kptr, V.threads, 0));
@@ -1371,22 +1500,35 @@ static bt_status run_walk(bt_tally* h, const double* dest, const int8_t* fly, co
     const int64_t want = (count + V.threads - 1) / V.threads;
     const unsigned blocks =
         (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)bps * h->num_sms));
-    int64_t* nwork = reinterpret_cast<int64_t*>(h->dcounters + 14);
+    int64_t* nwork = reinterpret_cast<int64_t*>(h->dcounters + 32 + chunk);
+    WorkSoA W = h->work;
     if (staged) {
         TRY(ensure_work(h));
-        stage_kernel<<<grid_for(count, 256), 256, 0, h->stream>>>(a, h->work, nwork);
+        W = h->work;
+        W.px += lo; W.py += lo; W.pz += lo; W.dx += lo; W.dy += lo; W.dz += lo;
+        W.w += lo; W.seg += lo; W.idx += lo; W.e += lo; W.g += lo; W.fl += lo;
+        stage_kernel<<<grid_for(count, 256), 256, 0, h->stream>>>(a, W, nwork, lo, wsum);
         CK(cudaGetLastError());
         h->kernels += 1;
     }
-    CK(cudaEventRecord(h->ev0, h->stream));
+    if (h->walk_first) {
+        CK(cudaEventRecord(h->ev0, h->stream));
+        h->walk_first = false;
+    }
     if (staged)
-        V.staged<<<blocks, V.threads, 0, h->stream>>>(a, h->work, nwork);
+        V.staged<<<blocks, V.threads, 0, h->stream>>>(a, W, nwork);
     else
         V.plain<<<blocks, V.threads, 0, h->stream>>>(a);
     CK(cudaGetLastError());
-    CK(cudaEventRecord(h->ev1, h->stream));
     h->kernels += 1;
-    CK(cudaMemcpyAsync(h->hcounters, h->dcounters, sizeof(unsigned long long) * 16,
+    return BT_OK;
+}
+
+// read the counters (running `overlap` on the host meanwhile) and fill the summary
+static bt_status walk_end(bt_tally* h, int64_t max_sweeps, bt_summary* summary,
+                          HostOverlap overlap = HostOverlap()) {
+    CK(cudaEventRecord(h->ev1, h->stream));
+    CK(cudaMemcpyAsync(h->hcounters, h->dcounters, sizeof(unsigned long long) * NDCOUNTERS,
                        cudaMemcpyDeviceToHost, h->stream));
     if (overlap.fn) overlap.fn(overlap.ctx);
     CK(cudaStreamSynchronize(h->stream));
@@ -1404,8 +1546,22 @@ static bt_status run_walk(bt_tally* h, const double* dest, const int8_t* fly, co
     }
     if (c[C_ERR])
         return set_err(BT_ERUNTIME, "trace did not terminate within %lld sweeps",
-                       (long long)a.max_sweeps);
+                       (long long)max_sweeps);
+    if (c[C_UNLOC])
+        return set_err(BT_EINVAL,
+                       "%llu flying particle(s) not localized (element = -1) were not moved; "
+                       "call initialize_particle_location first",
+                       (unsigned long long)c[C_UNLOC]);
     return BT_OK;
+}
+
+static bt_status run_walk(bt_tally* h, const double* dest, const int8_t* fly, const double* w,
+                          int64_t count, bool score, bt_summary* summary,
+                          HostOverlap overlap = HostOverlap()) {
+    WalkArgs a = walk_args(h, dest, fly, w, score);
+    TRY(walk_begin(h));
+    TRY(walk_enqueue(h, a, 0, count, 0, nullptr));
+    return walk_end(h, a.max_sweeps, summary, overlap);
 }
 
 static LocateArgs locate_args(bt_tally* h, const double* target, int64_t count) {
@@ -1525,52 +1681,8 @@ bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, cons
         }
     }
     CK(cudaEventRecord(h->ev2, h->stream));
-    const double* d_dest = destinations;
-    const int8_t* d_fly = flying;
-    const double* d_w = weights;
-    if (host) {  // on the copy stream: overlaps a still-running localization
-        CK(cudaMemcpyAsync(h->dest, destinations, sizeof(double) * 3 * count,
-                           cudaMemcpyHostToDevice, h->cstream));
-        CK(cudaMemcpyAsync(h->fly, flying, count, cudaMemcpyHostToDevice, h->cstream));
-        CK(cudaMemcpyAsync(h->weight, weights, sizeof(double) * count, cudaMemcpyHostToDevice,
-                           h->cstream));
-        if (groups)
-            CK(cudaMemcpyAsync(h->group, groups, sizeof(int32_t) * count,
-                               cudaMemcpyHostToDevice, h->cstream));
-        CK(cudaEventRecord(h->evc1, h->cstream));
-        CK(cudaStreamWaitEvent(h->stream, h->evc1, 0));
-        d_dest = h->dest;
-        d_fly = h->fly;
-        d_w = h->weight;
-    }
-    const int32_t* d_groups_in = nullptr;
-    if (groups && !host) {
-        CK(cudaMemcpyAsync(h->group, groups, sizeof(int32_t) * count, cudaMemcpyDeviceToDevice,
-                           h->stream));
-        d_groups_in = h->group;
-    }
-    // device-side checks: unlocalized flying particles (+ groups, weight sum)
-    CK(cudaMemsetAsync(h->dcounters + 15, 0, sizeof(unsigned long long), h->stream));
-    const bool dev_w = !host && need_w;
-    if (dev_w) CK(cudaMemsetAsync(h->dwsum, 0, sizeof(double), h->stream));
-    prepare_kernel<<<grid_for(count, 256), 256, 0, h->stream>>>(
-        d_fly, h->element, d_groups_in, h->ngroups, d_w, count, h->dcounters + 15,
-        dev_w ? h->dwsum : nullptr);
-    CK(cudaGetLastError());
-    h->kernels += 1;
-    unsigned long long flags = 0;
-    double dw = 0.0;
-    CK(cudaMemcpyAsync(&flags, h->dcounters + 15, sizeof flags, cudaMemcpyDeviceToHost,
-                       h->stream));
-    if (dev_w) CK(cudaMemcpyAsync(&dw, h->dwsum, sizeof dw, cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
-    if (flags & 2ull) return set_err(BT_EINDEX, "group out of range [0, %d)", h->ngroups);
-    if (flags & 1ull)
-        return set_err(BT_EINVAL,
-                       "a flying particle is not localized (element = -1); call "
-                       "initialize_particle_location first");
     // the recorded source weight (host inputs: numpy's pairwise order, computed
-    // on the host while the walk kernel runs)
+    // on the host while the walk kernels run; device inputs: summed in stage)
     struct WJob {
         const double* w;
         const int8_t* fly;
@@ -1589,8 +1701,60 @@ bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, cons
             j->out = pairwise_sum(sel.data(), (int64_t)sel.size());
         };
     }
-    bt_status s = run_walk(h, d_dest, d_fly, d_w, count, true, summary, ov);
-    if (need_w) h->source_weight = host ? job.out : dw;
+    bt_status s;
+    if (host) {
+        // pipeline: chunk c's input copies (copy stream) overlap chunk c-1's walk
+        WalkArgs a = walk_args(h, h->dest, h->fly, h->weight, true);
+        int nch = 1;
+        if (h->opt_staged && !h->opt_sort) {
+            nch = h->move_chunks > 0 ? h->move_chunks : (count >= (4 << 20) ? 4 : 1);
+            nch = (int)std::min<int64_t>(std::min(nch, MAX_CHUNKS), count);
+        }
+        TRY(walk_begin(h));
+        for (int c = 0; c < nch; ++c) {
+            const int64_t lo = count * c / nch, hi = count * (c + 1) / nch;
+            const int64_t n = hi - lo;
+            CK(cudaMemcpyAsync(h->dest + 3 * lo, destinations + 3 * lo, sizeof(double) * 3 * n,
+                               cudaMemcpyHostToDevice, h->cstream));
+            CK(cudaMemcpyAsync(h->fly + lo, flying + lo, n, cudaMemcpyHostToDevice, h->cstream));
+            CK(cudaMemcpyAsync(h->weight + lo, weights + lo, sizeof(double) * n,
+                               cudaMemcpyHostToDevice, h->cstream));
+            if (groups)
+                CK(cudaMemcpyAsync(h->group + lo, groups + lo, sizeof(int32_t) * n,
+                                   cudaMemcpyHostToDevice, h->cstream));
+            CK(cudaEventRecord(h->evchunk[c], h->cstream));
+            CK(cudaStreamWaitEvent(h->stream, h->evchunk[c], 0));
+            TRY(walk_enqueue(h, a, lo, hi, c, nullptr));
+        }
+        s = walk_end(h, a.max_sweeps, summary, ov);
+        if (need_w) h->source_weight = job.out;
+    } else {
+        if (groups) {  // device groups: range check before any work
+            CK(cudaMemcpyAsync(h->group, groups, sizeof(int32_t) * count,
+                               cudaMemcpyDeviceToDevice, h->stream));
+            CK(cudaMemsetAsync(h->dcounters + 15, 0, sizeof(unsigned long long), h->stream));
+            prepare_kernel<<<grid_for(count, 256), 256, 0, h->stream>>>(
+                flying, h->element, h->group, h->ngroups, weights, count, h->dcounters + 15,
+                nullptr);
+            CK(cudaGetLastError());
+            h->kernels += 1;
+            unsigned long long flags = 0;
+            CK(cudaMemcpyAsync(&flags, h->dcounters + 15, sizeof flags, cudaMemcpyDeviceToHost,
+                               h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+            if (flags & 2ull) return set_err(BT_EINDEX, "group out of range [0, %d)", h->ngroups);
+        }
+        WalkArgs a = walk_args(h, destinations, flying, weights, true);
+        if (need_w) CK(cudaMemsetAsync(h->dwsum, 0, sizeof(double), h->stream));
+        TRY(walk_begin(h));
+        TRY(walk_enqueue(h, a, 0, count, 0, need_w ? h->dwsum : nullptr));
+        s = walk_end(h, a.max_sweeps, summary);
+        if (need_w) {
+            double dw = 0.0;
+            CK(cudaMemcpy(&dw, h->dwsum, sizeof dw, cudaMemcpyDeviceToHost));
+            h->source_weight = dw;
+        }
+    }
     CK(cudaEventRecord(h->ev3, h->stream));
     CK(cudaEventSynchronize(h->ev3));
     CK(cudaEventElapsedTime(&h->call_ms, h->ev2, h->ev3));
@@ -1756,6 +1920,106 @@ bt_status bt_restore_state(bt_tally* h) {
     CK(cudaMemcpyAsync(h->seg_total, h->snap_seg, sizeof(double) * n, d2d, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     return BT_OK;
+}
+
+bt_status bt_build_adjacency(const int32_t* elements, int64_t num_elements, int64_t num_vertices,
+                             int32_t device, int32_t* adj_elem, int8_t* adj_face) {
+    if (num_elements < 0 || num_vertices < 0) return set_err(BT_EINVAL, "negative sizes");
+    if (num_elements >= (1ll << 29)) return set_err(BT_EINVAL, "mesh too large (>= 2^29 tets)");
+    if (num_elements == 0) return BT_OK;
+    if (!elements || !adj_elem || !adj_face) return set_err(BT_EINVAL, "NULL array");
+    for (int64_t i = 0; i < 4 * num_elements; ++i)
+        if (elements[i] < 0 || elements[i] >= num_vertices)
+            return set_err(BT_EINVAL, "element vertex id out of range");
+    CK(cudaSetDevice(device));
+    const int64_t ne = num_elements, nrows = 4 * ne;
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    int *d_el = nullptr, *rows = nullptr, *rows2 = nullptr, *ae = nullptr;
+    unsigned *kc = nullptr, *kc2 = nullptr, *flags = nullptr;
+    unsigned long long *kab = nullptr, *kab2 = nullptr;
+    signed char* af = nullptr;
+    long long* err = nullptr;
+    void* tmp = nullptr;
+    bt_status rc = BT_OK;
+    auto cleanup = [&]() {
+        void* ps[] = {d_el, rows, rows2, ae, kc, kc2, flags, kab, kab2, af, err, tmp};
+        for (void* p : ps)
+            if (p) cudaFree(p);
+        cudaStreamDestroy(st);
+    };
+#define CKA(call)                                                                       \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess) {                                                        \
+            rc = set_err(e_ == cudaErrorMemoryAllocation ? BT_ENOMEM : BT_ECUDA,        \
+                         "%s failed: %s", #call, cudaGetErrorString(e_));               \
+            cleanup();                                                                  \
+            return rc;                                                                  \
+        }                                                                               \
+    } while (0)
+    CKA(cudaMalloc(&d_el, sizeof(int) * nrows));
+    CKA(cudaMalloc(&rows, sizeof(int) * nrows));
+    CKA(cudaMalloc(&rows2, sizeof(int) * nrows));
+    CKA(cudaMalloc(&kc, sizeof(unsigned) * nrows));
+    CKA(cudaMalloc(&kc2, sizeof(unsigned) * nrows));
+    CKA(cudaMalloc(&kab, sizeof(unsigned long long) * nrows));
+    CKA(cudaMalloc(&kab2, sizeof(unsigned long long) * nrows));
+    CKA(cudaMalloc(&ae, sizeof(int) * nrows));
+    CKA(cudaMalloc(&af, nrows));
+    CKA(cudaMalloc(&flags, sizeof(unsigned)));
+    CKA(cudaMalloc(&err, 3 * sizeof(long long)));
+    CKA(cudaMemcpyAsync(d_el, elements, sizeof(int) * nrows, cudaMemcpyHostToDevice, st));
+    CKA(cudaMemsetAsync(ae, 0xff, sizeof(int) * nrows, st));
+    CKA(cudaMemsetAsync(af, 0xff, nrows, st));
+    CKA(cudaMemsetAsync(flags, 0, sizeof(unsigned), st));
+    CKA(cudaMemsetAsync(err, 0x7f, 3 * sizeof(long long), st));
+    int vbits = 1;
+    while ((1ll << vbits) < num_vertices + 1) ++vbits;
+    adj_keys_c_kernel<<<grid_for(nrows, 256), 256, 0, st>>>(d_el, nrows, kc, rows);
+    CKA(cudaGetLastError());
+    size_t b1 = 0, b2 = 0;
+    CKA(cub::DeviceRadixSort::SortPairs(nullptr, b1, kc, kc2, rows, rows2, (int)nrows, 0, vbits, st));
+    CKA(cub::DeviceRadixSort::SortPairs(nullptr, b2, kab, kab2, rows2, rows, (int)nrows, 0,
+                                        32 + vbits, st));
+    CKA(cudaMalloc(&tmp, std::max(b1, b2)));
+    CKA(cub::DeviceRadixSort::SortPairs(tmp, b1, kc, kc2, rows, rows2, (int)nrows, 0, vbits, st));
+    adj_keys_ab_kernel<<<grid_for(nrows, 256), 256, 0, st>>>(d_el, nrows, rows2, kab);
+    CKA(cudaGetLastError());
+    CKA(cub::DeviceRadixSort::SortPairs(tmp, b2, kab, kab2, rows2, rows, (int)nrows, 0, 32 + vbits,
+                                        st));
+    adj_match_kernel<<<grid_for(nrows, 256), 256, 0, st>>>(d_el, nrows, rows, ae, af, flags, err);
+    CKA(cudaGetLastError());
+    adj_dup_kernel<<<grid_for(ne, 256), 256, 0, st>>>(ae, ne, flags, err);
+    CKA(cudaGetLastError());
+    unsigned hflags = 0;
+    long long herr[3];
+    CKA(cudaMemcpyAsync(&hflags, flags, sizeof hflags, cudaMemcpyDeviceToHost, st));
+    CKA(cudaMemcpyAsync(herr, err, sizeof herr, cudaMemcpyDeviceToHost, st));
+    CKA(cudaMemcpyAsync(adj_elem, ae, sizeof(int) * nrows, cudaMemcpyDeviceToHost, st));
+    CKA(cudaMemcpyAsync(adj_face, af, nrows, cudaMemcpyDeviceToHost, st));
+    CKA(cudaStreamSynchronize(st));
+    if (hflags & 1u) {
+        int row = 0;
+        CKA(cudaMemcpy(&row, rows + herr[0], sizeof row, cudaMemcpyDeviceToHost));
+        const int64_t e = row >> 2, f = row & 3;
+        int v[3], j = 0;
+        for (int q = 0; q < 4; ++q)
+            if (q != f) v[j++] = elements[4 * e + q];
+        std::sort(v, v + 3);
+        rc = set_err(BT_EINVAL,
+                     "face with vertices (%d, %d, %d) is shared by more than two elements "
+                     "(duplicate or non-manifold mesh)", v[0], v[1], v[2]);
+    } else if (hflags & 2u) {
+        rc = set_err(BT_EINVAL, "element %lld lists the same face twice (repeated vertex id)",
+                     herr[1]);
+    } else if (hflags & 4u) {
+        rc = set_err(BT_EINVAL, "element %lld duplicates element %d", herr[2],
+                     adj_elem[4 * herr[2]]);
+    }
+    cleanup();
+#undef CKA
+    return rc;
 }
 
 bt_status bt_info(bt_tally* h, int32_t* device, int64_t* num_elements, int64_t* capacity,

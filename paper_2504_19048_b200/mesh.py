@@ -89,7 +89,9 @@ class TetMesh:
         return np.stack([self.adj_elem, self.adj_face.astype(np.int32)], axis=2)
 
     @classmethod
-    def from_arrays(cls, vertices, elements) -> "TetMesh":
+    def from_arrays(cls, vertices, elements, device: int | None = None) -> "TetMesh":
+        """Orientation fix, degeneracy check, adjacency (on `device` when
+        given: bt_build_adjacency, else host numpy)."""
         vertices = np.ascontiguousarray(vertices, dtype=np.float64)
         elements = np.array(elements, dtype=np.int32, copy=True, order="C")
         if vertices.ndim != 2 or vertices.shape[1] != 3:
@@ -115,7 +117,7 @@ class TetMesh:
             raise MalformedMeshError(
                 f"element {bad} is degenerate (volume {vol6[bad] / 6.0:g})")
 
-        adj_elem, adj_face = build_adjacency(elements, nv)
+        adj_elem, adj_face = build_adjacency(elements, nv, device=device)
         centroids = vertices[elements].mean(axis=1)
         if vertices.size:
             bbox = np.stack([vertices.min(axis=0), vertices.max(axis=0)])
@@ -136,7 +138,7 @@ def signed_volumes6(vertices: np.ndarray, elements: np.ndarray) -> np.ndarray:
     return np.einsum("ij,ij->i", np.cross(a, b), c)
 
 
-def build_cube_mesh(n: int, edge_length: float = 1.0) -> TetMesh:
+def build_cube_mesh(n: int, edge_length: float = 1.0, device: int | None = None) -> TetMesh:
     """[0, edge_length]^3 split into n^3 hex cells of 6 Kuhn tets each."""
     if not isinstance(n, (int, np.integer)) or isinstance(n, bool) or n < 1:
         raise ValueError(f"subdivisions must be a positive integer, got {n!r}")
@@ -159,13 +161,15 @@ def build_cube_mesh(n: int, edge_length: float = 1.0) -> TetMesh:
     offs = np.array([((b >> 2) & 1) * nv * nv + ((b >> 1) & 1) * nv + (b & 1)
                      for b in range(8)], dtype=np.int64)
     elements = base[:, None, None] + offs[KUHN_TETS][None, :, :]   # (cells, 6, 4)
-    return TetMesh.from_arrays(vertices, elements.reshape(-1, 4))
+    return TetMesh.from_arrays(vertices, elements.reshape(-1, 4), device=device)
 
 
 def build_torus_shell_mesh(nr: int, ntheta: int, nphi: int, R: float = 300.0,
-                           a_in: float = 100.0, a_out: float = 120.0) -> TetMesh:
+                           a_in: float = 100.0, a_out: float = 120.0,
+                           device: int | None = None) -> TetMesh:
     """Toroidal-shell mesh; see torus_shell_arrays."""
-    return TetMesh.from_arrays(*torus_shell_arrays(nr, ntheta, nphi, R, a_in, a_out))
+    return TetMesh.from_arrays(*torus_shell_arrays(nr, ntheta, nphi, R, a_in, a_out),
+                               device=device)
 
 
 def torus_shell_arrays(nr: int, ntheta: int, nphi: int, R: float = 300.0,
@@ -207,17 +211,28 @@ def _face_keys(elements: np.ndarray, nv: int):
     return tri.reshape(-1, 3)
 
 
-def build_adjacency(elements, vertex_count: int):
+def build_adjacency(elements, vertex_count: int, device: int | None = None):
     """(adj_elem, adj_face), both (E, 4), -1 on the boundary.
 
     Raises MalformedMeshError for a face shared by 3+ elements, an element
-    listing one face twice, or a duplicated element.
+    listing one face twice, or a duplicated element.  With `device`, the
+    sort runs on that GPU (bt_build_adjacency); the result is identical
+    (adjacency of a conforming mesh is unique).
     """
     elements = np.ascontiguousarray(elements, dtype=np.int32)
     ne = elements.shape[0]
     adj_elem = np.full((ne, 4), -1, dtype=np.int32)
     adj_face = np.full((ne, 4), -1, dtype=np.int8)
     if ne == 0:
+        return adj_elem, adj_face
+    if device is not None:
+        from . import _lib
+        L = _lib.load()
+        st = L.bt_build_adjacency(elements.ctypes.data, ne, int(vertex_count), int(device),
+                                  adj_elem.ctypes.data, adj_face.ctypes.data)
+        if st == _lib.BT_EINVAL:
+            raise MalformedMeshError(L.bt_last_error().decode())
+        _lib.check(st)
         return adj_elem, adj_face
     if int(elements.min()) < 0 or int(elements.max()) >= vertex_count:
         raise MalformedMeshError("element vertex id out of range")

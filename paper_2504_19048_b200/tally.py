@@ -21,8 +21,9 @@ Documented deviations from the reference:
   reference's slab/thread mismatch bug, cannot occur).
 * ``groups`` values outside ``[0, num_groups)`` raise ``IndexError`` instead
   of silently scoring into another element's bin (tally.py:262-266).
-* A flying particle with ``element == -1`` raises ``ValueError`` before any
-  work (the reference's fused path reads element -1 with numba wraparound).
+* A flying particle with ``element == -1`` is not moved and the call raises
+  ``ValueError`` after moving the others (the reference's fused path reads
+  element -1 with numba wraparound; its callback path raises up front).
 * Localization defaults to the grid search (``localize="grid"``): it returns
   the lowest-id element containing the point (pkg/tests/oracles.py:36-57),
   which equals the reference's centroid-0 walk + tie-break on every generic
@@ -206,7 +207,8 @@ class MeshTally:
 
     def __init__(self, mesh, num_particles: int, num_groups: int = 1, threads: int = 1, *,
                  device: int = 0, localize: str = "grid", digest: bool = False,
-                 sort: bool = False, warp_aggregate: bool = False, staged: bool = True):
+                 sort: bool = False, warp_aggregate: bool = False, staged: bool = True,
+                 move_chunks: int = 0):
         if isinstance(mesh, (str, Path)):
             mesh = read_tetmesh(mesh)
         if not all(hasattr(mesh, a) for a in ("vertices", "elements", "adj_elem", "adj_face",
@@ -243,6 +245,7 @@ class MeshTally:
         self.set_option(_lib.BT_OPT_SORT, int(sort))
         self.set_option(_lib.BT_OPT_WARP_AGG, int(warp_aggregate))
         self.set_option(_lib.BT_OPT_STAGED, int(staged))
+        self.set_option(_lib.BT_OPT_MOVE_CHUNKS, int(move_chunks))
         self._grid = TallyGrid(self)
 
     # ------------------------------------------------------------------ props

@@ -88,7 +88,8 @@ def test_walk_matches_reference_grid_localize(name):
 
 @pytest.mark.parametrize("opts", [dict(sort=True), dict(warp_aggregate=True),
                                   dict(staged=False), dict(staged=False, sort=True,
-                                                           warp_aggregate=True)])
+                                                           warp_aggregate=True),
+                                  dict(move_chunks=3), dict(move_chunks=16, warp_aggregate=True)])
 def test_walk_options_keep_parity(opts):
     _check_case(load_walk_case("c1_point_s2"), "grid", **opts)
     _check_case(load_walk_case("n6_uniform_g3"), "grid", **opts)
@@ -201,10 +202,13 @@ def test_error_behaviour():
         mt.flux()
     with pytest.raises(RuntimeError):
         mt.finalize_batch()
-    # unlocalized flying particle
+    # unlocalized flying particle: not moved, reported after the move
     mt2 = MeshTally(m, 4)
+    mt2.initialize_particle_location(np.array([[0.31, 0.32, 0.33], [2.0, 0, 0]]))
     with pytest.raises(ValueError):
-        mt2.move_to_next_location(pos, np.ones(4), np.ones(4))
+        mt2.move_to_next_location([[0.4, 0.4, 0.4], [0.5, 0.5, 0.5]], [1, 1], [1.0, 1.0])
+    st = mt2.read_particles(2)
+    assert st.element[1] == -1 and np.array_equal(st.position[0], [0.4, 0.4, 0.4])
     # sweep guard
     mt.set_option(0, 1)
     mt.initialize_particle_location(np.array([[0.05, 0.05, 0.05]]))
@@ -214,3 +218,26 @@ def test_error_behaviour():
         MeshTally(object(), 4)
     with pytest.raises(ValueError):
         MeshTally(m, 0)
+
+
+def test_gpu_adjacency_matches_host():
+    from paper_2504_19048_b200 import mesh as M
+    gen = np.random.default_rng(9)
+    for n in (1, 2, 5, 13):
+        h = M.build_cube_mesh(n)
+        g = M.build_cube_mesh(n, device=0)
+        assert np.array_equal(h.adj_elem, g.adj_elem) and np.array_equal(h.adj_face, g.adj_face)
+    v, e = M.torus_shell_arrays(3, 16, 24)
+    perm = gen.permutation(e.shape[0])
+    for els in (e, e[perm]):
+        a = M.TetMesh.from_arrays(v, els)
+        b = M.TetMesh.from_arrays(v, els, device=0)
+        assert np.array_equal(a.adj_elem, b.adj_elem) and np.array_equal(a.adj_face, b.adj_face)
+    bad = [np.array([[0, 1, 2, 3], [0, 1, 2, 4], [0, 1, 2, 5]]),   # 3 tets on one face
+           np.array([[0, 1, 2, 3], [0, 1, 2, 3]]),                 # duplicated element
+           np.array([[0, 1, 1, 3]])]                               # repeated vertex id
+    for els in bad:
+        with pytest.raises(M.MalformedMeshError):
+            M.build_adjacency(els, 6, device=0)
+        with pytest.raises(M.MalformedMeshError):
+            M.build_adjacency(els, 6)
