@@ -357,5 +357,78 @@ def main():
     ])
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--transport" not in sys.argv:
     main()
+
+
+# ----------------------------------------------------------------------------
+# transport: philox KATs and small reference runs
+
+def transport_fixtures():
+    from meshtally import rng as mtr
+    from meshtally import transport as mtt2
+    out = {}
+    # raw philox4x64-10 words (rng.py:38-49) and (0,1] uniforms (rng.py:52-64)
+    ctrs = [(0, 0, 0, 0), (1, 2, 3, 4), (2**63 - 1, 5, 7, 0), (123456789, 42, 3, 0)]
+    keys = [(0, 0), (42, 2**62 + 5), (2**62, 99), (7, 7)]  # raw_block rejects words >= 2^63
+    raw = np.array([mtr.raw_block(c, k) for c in ctrs for k in keys], dtype=np.uint64)
+    out["philox_ctr"] = np.array([c for c in ctrs for _ in keys], dtype=np.uint64)
+    out["philox_key"] = np.array([k for _ in ctrs for k in keys], dtype=np.uint64)
+    out["philox_out"] = raw
+    gen = np.random.default_rng(3)
+    q = gen.integers(0, 2**31, (500, 4))
+    out["uni_key"] = q.astype(np.int64)
+    out["uni_out"] = np.array([mtr._uniform_block_arr(int(a), int(b), int(c), int(d))
+                               for a, b, c, d in q])
+    cases = {
+        "t1g": mtt2.RunConfig(mesh_n=4, num_particles=3000, num_batches=3,
+                              cross_sections=mtt2.CrossSections.one_group(10.0, 8.0),
+                              seed=42),
+        "t2g": mtt2.RunConfig(mesh_n=5, num_particles=2000, num_batches=2,
+                              cross_sections=mtt2.CrossSections(
+                                  np.array([5.0, 8.0]), np.array([[2.0, 2.5], [0.5, 6.0]])),
+                              seed=7, source_box=((0.1, 0.2, 0.3), (0.6, 0.5, 0.9))),
+        "tdir": mtt2.RunConfig(mesh_n=3, num_particles=1500, num_batches=2,
+                               cross_sections=mtt2.CrossSections.one_group(3.0, 2.0),
+                               seed=11, source_direction=(1.0, 0.5, 0.25)),
+    }
+    for name, cfg in cases.items():
+        mesh = mt.build_cube_mesh(cfg.mesh_n, cfg.edge_length)
+        eng = mtt2.build_engine(cfg, mesh)
+        res = mtt2.run(cfg, engine=eng)
+        n = cfg.num_particles
+        pre = f"{name}_"
+        xs = cfg.cross_sections
+        out[pre + "cfg"] = np.array([cfg.mesh_n, cfg.num_particles, cfg.num_batches, cfg.seed],
+                                    dtype=np.int64)
+        out[pre + "sigma_t"] = xs.sigma_t
+        out[pre + "sigma_s"] = xs.sigma_s
+        out[pre + "box"] = np.array(cfg.source_box, dtype=np.float64)
+        out[pre + "dir"] = (np.array(cfg.source_direction) if cfg.source_direction is not None
+                            else np.zeros(0))
+        for key in ("source_weight", "leaked_weight", "absorbed_weight", "stuck_weight",
+                    "collisions", "events", "sweeps", "track_length_total"):
+            out[pre + key] = np.array(getattr(res, key))
+        out[pre + "flux_track_mean"] = res.flux_track.mean
+        out[pre + "flux_track_rel"] = res.flux_track.rel_error
+        out[pre + "flux_col_mean"] = res.flux_collision.mean
+        out[pre + "flux_col_rel"] = res.flux_collision.rel_error
+        b, ws = eng.batch, eng.workspace
+        out[pre + "final_position"] = np.array(b.position[:n])
+        out[pre + "final_direction"] = np.array(b.direction[:n])
+        out[pre + "final_element"] = np.array(b.element[:n])
+        out[pre + "final_group"] = np.array(b.group[:n])
+        out[pre + "final_alive"] = np.array(b.alive[:n])
+        out[pre + "final_outcome"] = np.array(ws.outcome[:n])
+        out[pre + "final_rng_block"] = np.array(ws.rng_block[:n])
+        out[pre + "final_seg_total"] = np.array(ws.seg_total[:n])
+        print(f"  transport {name}: collisions {res.collisions} events {res.events} "
+              f"leaked {res.leaked_weight} absorbed {res.absorbed_weight} stuck {res.stuck_weight}")
+    path = OUT / "transport_ref.npz"
+    np.savez_compressed(path, **out)
+    print(f"wrote {path} ({path.stat().st_size/1e3:.0f} kB)")
+
+
+if __name__ == "__main__" and "--transport" in sys.argv:
+    OUT.mkdir(parents=True, exist_ok=True)
+    transport_fixtures()

@@ -65,6 +65,12 @@ def lib():
         L.om_locate_exhaustive.argtypes = [_P, _P, C.c_int64, _P, C.c_int64, _P, C.c_int]
         L.om_finalize.argtypes = [_P, C.c_int64, C.c_int64, C.c_double, _P, _P]
         L.om_max_threads.restype = C.c_int
+        L.om_philox.argtypes = [_P, _P, _P]
+        L.om_uniform_block.argtypes = [C.c_uint64] * 4 + [_P]
+        L.om_transport_run.restype = C.c_int
+        L.om_transport_run.argtypes = (
+            [_P, _P, _P, _P, C.c_int64, _P, C.c_int64, _P, _P, _P, C.c_int64, C.c_int64,
+             C.c_uint64, _P, C.c_int, _P] + [_P] * 7 + [C.POINTER(_Particles), _P, _P, _P])
         _lib = L
     return _lib
 
@@ -261,3 +267,89 @@ class OracleTally:
 
 if os.environ.get("ORACLE_BUILD_ON_IMPORT"):
     build()
+
+
+# ----------------------------------------------------------------------------
+# transport: restatement of transport.run, serial
+
+def philox(ctr, key):
+    c = np.ascontiguousarray(ctr, dtype=np.uint64)
+    k = np.ascontiguousarray(key, dtype=np.uint64)
+    out = np.zeros(4, np.uint64)
+    lib().om_philox(_ptr(c), _ptr(k), _ptr(out))
+    return out
+
+
+def uniform_block(seed, batch, particle, block):
+    u = np.zeros(4)
+    lib().om_uniform_block(C.c_uint64(seed), C.c_uint64(batch), C.c_uint64(particle),
+                           C.c_uint64(block), _ptr(u))
+    return u
+
+
+def xs_kernel_data(sigma_t, sigma_s):
+    """XSData (transport.py:83-99): scatter probability and group CDF."""
+    st = np.ascontiguousarray(np.atleast_1d(sigma_t), dtype=np.float64)
+    ss = np.ascontiguousarray(np.atleast_2d(sigma_s), dtype=np.float64)
+    g = st.shape[0]
+    rows = ss.sum(axis=1)
+    prob = rows / st
+    cdf = np.zeros((g, g))
+    for i in range(g):
+        if rows[i] > 0.0:
+            cdf[i] = np.cumsum(ss[i]) / rows[i]
+        cdf[i, g - 1] = 1.0
+    return st, np.ascontiguousarray(prob), np.ascontiguousarray(cdf)
+
+
+def transport_run(mesh, sigma_t, sigma_s, num_particles, num_batches, seed, box,
+                  direction=None):
+    """Returns dict with totals, flux moments and final particle state."""
+    L = lib()
+    st, prob, cdf = xs_kernel_data(sigma_t, sigma_s)
+    ng = st.shape[0]
+    n = int(num_particles)
+    nb = mesh.num_elements * ng
+    t = OracleTally(mesh, n, ng, threads=1)
+    direction_arr = np.zeros((n, 3))
+    rngb = np.zeros(n, np.uint64)
+    grp = np.zeros(n, np.int32)
+    tp, ts, tsq = np.zeros(nb), np.zeros(nb), np.zeros(nb)
+    cp, cs, csq = np.zeros(nb), np.zeros(nb), np.zeros(nb)
+    totals = np.zeros(8)
+    box = np.ascontiguousarray(np.asarray(box, dtype=np.float64).reshape(6))
+    fd = np.zeros(3) if direction is None else np.ascontiguousarray(direction, dtype=np.float64)
+    v, e, ae, af = t._mesh_arrays
+    P = t._particles()
+    rc = L.om_transport_run(
+        _ptr(v), _ptr(e), _ptr(ae), _ptr(af), C.c_int64(mesh.num_elements), _ptr(t._c0),
+        C.c_int64(ng), _ptr(st), _ptr(prob), _ptr(cdf), C.c_int64(n), C.c_int64(num_batches),
+        C.c_uint64(seed), _ptr(box), C.c_int(0 if direction is None else 1), _ptr(fd),
+        _ptr(tp), _ptr(ts), _ptr(tsq), _ptr(cp), _ptr(cs), _ptr(csq), _ptr(totals),
+        C.byref(P), _ptr(direction_arr), _ptr(grp), _ptr(rngb))
+    if rc != 0:
+        raise RuntimeError("oracle transport did not terminate")
+    keys = ("source_weight", "leaked_weight", "absorbed_weight", "stuck_weight",
+            "collisions", "events", "sweeps", "track_length_total")
+    out = dict(zip(keys, totals.tolist()))
+    out.update(track_sum=ts, track_sum_sq=tsq, col_sum=cs, col_sum_sq=csq,
+               position=t.position.copy(), direction=direction_arr, element=t.element.copy(),
+               group=grp, alive=t.alive.copy(), outcome=t.outcome.copy(), rng_block=rngb,
+               seg_total=t.seg_total.copy())
+    return out
+
+
+def flux_from_moments(s, sq, n, volumes, ng):
+    shape = (volumes.shape[0], ng)
+    s = s.reshape(shape)
+    sq = sq.reshape(shape)
+    bm = s / n
+    mean = bm / volumes[:, None]
+    rel = np.zeros(shape)
+    if n >= 2:
+        var = (sq - s * s / n) / (n - 1)
+        np.clip(var, 0.0, None, out=var)
+        se = np.sqrt(var / n)
+        nz = bm > 0.0
+        rel[nz] = se[nz] / bm[nz]
+    return mean, rel

@@ -478,3 +478,204 @@ int om_max_threads(void) {
     return 1;
 #endif
 }
+
+/* ======================================================================== */
+/* Transport driver: philox4x64-10 (rng.py:16-64) and the
+ * event loop of transport.run (transport.py:445-549) with _source (154-181),
+ * _trial_setup (184-201), _rearm (204-210), _flight (213-226) and _collide
+ * (229-275).  Serial (threads = 1) to reproduce the reference's summation
+ * order exactly.  log/cos/sin come from the C library, as numba's do. */
+
+static const uint64_t PH_M0 = 0xD2E7470EE14C6C93ULL, PH_M1 = 0xCA5A826395121157ULL;
+static const uint64_t PH_W0 = 0x9E3779B97F4A7C15ULL, PH_W1 = 0xBB67AE8584CAA73BULL;
+static const uint64_t PH_KEY1 = 0xD1B54A32D192ED03ULL;
+
+void om_philox(const uint64_t *ctr, const uint64_t *key, uint64_t *out) {
+    uint64_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3], k0 = key[0], k1 = key[1];
+    for (int r = 0; r < 10; ++r) {
+        __uint128_t p0 = (__uint128_t)PH_M0 * c0, p1 = (__uint128_t)PH_M1 * c2;
+        uint64_t hi0 = (uint64_t)(p0 >> 64), lo0 = (uint64_t)p0;
+        uint64_t hi1 = (uint64_t)(p1 >> 64), lo1 = (uint64_t)p1;
+        uint64_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+        k0 += PH_W0;
+        k1 += PH_W1;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+void om_uniform_block(uint64_t seed, uint64_t batch, uint64_t particle, uint64_t block,
+                      double *u) {
+    uint64_t ctr[4] = {block, particle, batch, 0}, key[2] = {seed, PH_KEY1}, w[4];
+    om_philox(ctr, key, w);
+    for (int j = 0; j < 4; ++j) u[j] = ((double)(w[j] >> 11) + 1.0) * (1.0 / 9007199254740992.0);
+}
+
+typedef struct {
+    int64_t ng;
+    const double *sigma_t;      /* (G) */
+    const double *scatter_prob; /* (G)  = rowsum(sigma_s)/sigma_t  (XSData) */
+    const double *group_cdf;    /* (G,G) */
+} om_xs;
+
+/* totals: source_w, leaked_w, absorbed_w, stuck_w, collisions, events, sweeps, track_total */
+int om_transport_run(const double *vertices, const int32_t *elements, const int32_t *adj_elem,
+                     const int8_t *adj_face, int64_t ne, const double *centroid0,
+                     int64_t ng, const double *sigma_t, const double *scatter_prob,
+                     const double *group_cdf, int64_t n, int64_t num_batches, uint64_t seed,
+                     const double *box, int fixed_dir, const double *fd, double *track_partials,
+                     double *track_sum, double *track_sum_sq, double *col_partials,
+                     double *col_sum, double *col_sum_sq, double *totals, om_particles *P,
+                     double *direction, int32_t *group_out, uint64_t *rng_block) {
+    om_mesh m = {vertices, elements, adj_elem, adj_face, ne};
+    (void)m;
+    double *dest = (double *)P->destination; /* the caller gives a writable buffer */
+    double *weight = (double *)P->weight;
+    int32_t *group = (int32_t *)P->group;
+    int64_t nb = ne * ng;
+    double source_w = 0, leaked_w = 0, absorbed_w = 0, stuck_w = 0, track_total = 0;
+    int64_t collisions = 0, events = 0, sweeps = 0;
+    int64_t *active = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    int64_t summ[6];
+    double sink = 0.0;
+    for (int64_t b = 0; b < num_batches; ++b) {
+        /* _source */
+        for (int64_t i = 0; i < n; ++i) {
+            double u[4];
+            om_uniform_block(seed, (uint64_t)b, (uint64_t)i, 0, u);
+            dest[3 * i] = box[0] + (box[3] - box[0]) * u[0];
+            dest[3 * i + 1] = box[1] + (box[4] - box[1]) * u[1];
+            dest[3 * i + 2] = box[2] + (box[5] - box[2]) * u[2];
+            if (fixed_dir) {
+                direction[3 * i] = fd[0];
+                direction[3 * i + 1] = fd[1];
+                direction[3 * i + 2] = fd[2];
+            } else {
+                double v[4];
+                om_uniform_block(seed, (uint64_t)b, (uint64_t)i, 1, v);
+                double mu = 2.0 * v[0] - 1.0;
+                double phi = (2.0 * 3.141592653589793) * v[1];
+                double t = 1.0 - mu * mu;
+                double s = sqrt(t > 0.0 ? t : 0.0);
+                direction[3 * i] = s * cos(phi);
+                direction[3 * i + 1] = s * sin(phi);
+                direction[3 * i + 2] = mu;
+            }
+            weight[i] = 1.0;
+            group[i] = 0;
+            P->alive[i] = 1;
+            P->flying[i] = 0;
+            rng_block[i] = 2;
+            P->outcome[i] = OUT_NONE;
+        }
+        /* _trial_setup + unscored walk + tie-break (_localize_adjacency) */
+        for (int64_t i = 0; i < n; ++i) {
+            P->position[3 * i] = centroid0[0];
+            P->position[3 * i + 1] = centroid0[1];
+            P->position[3 * i + 2] = centroid0[2];
+            P->element[i] = 0;
+            P->flying[i] = P->alive[i];
+            P->entry_face[i] = -1;
+            P->stuck[i] = 0;
+            P->seg_total[i] = 0.0;
+        }
+        om_particles Q = *P;
+        Q.digest = NULL;
+        Q.count = NULL;
+        if (om_trace(vertices, elements, adj_elem, adj_face, ne, &Q, n, &sink, 1, 1, 0, 1,
+                     2 * ne + 1000, summ) != 0)
+            return -1;
+        tie_break_faces(&m, P, n);
+        /* _rearm */
+        for (int64_t i = 0; i < n; ++i) {
+            P->flying[i] = P->alive[i];
+            P->entry_face[i] = -1;
+            P->outcome[i] = OUT_NONE;
+            P->seg_total[i] = 0.0;
+        }
+        /* batch source weight: weight[:n][alive].sum() (all weights are 1.0) */
+        double bsw = 0.0;
+        for (int64_t i = 0; i < n; ++i)
+            if (P->alive[i]) bsw += weight[i];
+        source_w += bsw;
+        for (;;) {
+            int64_t mcount = 0;
+            for (int64_t i = 0; i < n; ++i)
+                if (P->flying[i]) active[mcount++] = i;
+            if (mcount == 0) break;
+            /* _flight */
+            for (int64_t k = 0; k < mcount; ++k) {
+                int64_t i = active[k];
+                double u[4];
+                om_uniform_block(seed, (uint64_t)b, (uint64_t)i, rng_block[i], u);
+                rng_block[i] += 1;
+                double lc = -log(u[0]) / sigma_t[group[i]];
+                dest[3 * i] = P->position[3 * i] + lc * direction[3 * i];
+                dest[3 * i + 1] = P->position[3 * i + 1] + lc * direction[3 * i + 1];
+                dest[3 * i + 2] = P->position[3 * i + 2] + lc * direction[3 * i + 2];
+                P->outcome[i] = OUT_NONE;
+            }
+            if (om_trace(vertices, elements, adj_elem, adj_face, ne, &Q, n, track_partials, 1,
+                         (int32_t)ng, 1, 1, 2 * ne + 1000, summ) != 0)
+                return -1;
+            events += summ[1];
+            sweeps += summ[0];
+            /* _collide */
+            for (int64_t k = 0; k < mcount; ++k) {
+                int64_t i = active[k];
+                int8_t oc = P->outcome[i];
+                if (oc == OUT_REACHED) {
+                    int32_t g = group[i];
+                    double w = weight[i];
+                    int64_t e = P->element[i];
+                    col_partials[e * ng + g] += w / sigma_t[g];
+                    collisions += 1;
+                    double u[4];
+                    om_uniform_block(seed, (uint64_t)b, (uint64_t)i, rng_block[i], u);
+                    rng_block[i] += 1;
+                    if (u[0] <= scatter_prob[g]) {
+                        int32_t gp = 0;
+                        for (int64_t j = 0; j < ng; ++j) {
+                            gp = (int32_t)j;
+                            if (u[1] <= group_cdf[g * ng + j]) break;
+                        }
+                        double mu = 2.0 * u[2] - 1.0;
+                        double phi = (2.0 * 3.141592653589793) * u[3];
+                        double t = 1.0 - mu * mu;
+                        double s = sqrt(t > 0.0 ? t : 0.0);
+                        direction[3 * i] = s * cos(phi);
+                        direction[3 * i + 1] = s * sin(phi);
+                        direction[3 * i + 2] = mu;
+                        group[i] = gp;
+                        P->flying[i] = 1;
+                    } else {
+                        P->alive[i] = 0;
+                        P->flying[i] = 0;
+                        P->outcome[i] = 5; /* OUTCOME_ABSORBED */
+                        absorbed_w += w;
+                    }
+                } else if (oc == OUT_LEAKED) {
+                    leaked_w += weight[i];
+                } else if (oc == OUT_STUCK_KILLED) {
+                    stuck_w += weight[i];
+                }
+            }
+        }
+        double ts = 0.0;
+        for (int64_t i = 0; i < n; ++i) ts += P->seg_total[i];
+        track_total += ts;
+        om_finalize(track_partials, 1, nb, bsw, track_sum, track_sum_sq);
+        om_finalize(col_partials, 1, nb, bsw, col_sum, col_sum_sq);
+    }
+    for (int64_t i = 0; i < n; ++i) group_out[i] = group[i];
+    free(active);
+    totals[0] = source_w;
+    totals[1] = leaked_w;
+    totals[2] = absorbed_w;
+    totals[3] = stuck_w;
+    totals[4] = (double)collisions;
+    totals[5] = (double)events;
+    totals[6] = (double)sweeps;
+    totals[7] = track_total;
+    return 0;
+}
