@@ -55,9 +55,12 @@ enum {
 
 /* tally arrays for bt_read_tally / bt_tally_device_ptr */
 enum {
-    BT_TALLY_BATCH = 0, /* unfinalized per-bin totals (tally.py:101-104) */
-    BT_TALLY_SUM = 1,   /* running sum of normalised batch tallies */
-    BT_TALLY_SUM_SQ = 2 /* running sum of squares */
+    BT_TALLY_BATCH = 0,     /* unfinalized per-bin totals (tally.py:101-104) */
+    BT_TALLY_SUM = 1,       /* running sum of normalised batch tallies */
+    BT_TALLY_SUM_SQ = 2,    /* running sum of squares */
+    BT_TALLY_COL_BATCH = 3, /* collision estimator (bt_transport_run) */
+    BT_TALLY_COL_SUM = 4,
+    BT_TALLY_COL_SUM_SQ = 5
 };
 
 /* options for bt_set_option */
@@ -177,6 +180,44 @@ bt_status bt_info(bt_tally *h, int32_t *device, int64_t *num_elements, int64_t *
  */
 bt_status bt_build_adjacency(const int32_t *elements, int64_t num_elements, int64_t num_vertices,
                              int32_t device, int32_t *adj_elem, int8_t *adj_face);
+
+/* Totals of bt_transport_run, mirroring transport.RunResult (transport.py:422-442). */
+typedef struct {
+    double source_weight;
+    double leaked_weight;
+    double absorbed_weight;
+    double stuck_weight;
+    double track_length_total;
+    int64_t collisions;
+    int64_t events;
+    int64_t sweeps;
+    float ms_localization;
+    float ms_transport;
+} bt_transport_totals;
+
+/*
+ * Fixed-source analog multigroup transport on the device (transport.run,
+ * transport.py:445-549): per batch, source sampling in
+ * `box` (2,3) with isotropic (fixed_direction NULL) or fixed directions,
+ * localization, then every particle's whole history in one persistent kernel
+ * (flight -> walk with track-length scoring -> collision estimator +
+ * scatter/absorb), finalized into the handle's track and collision tallies.
+ * Random draws are philox4x64-10 keyed (seed, batch, particle, block)
+ * exactly as rng.py:58-64.  Cross sections: sigma_t (G), scatter probability
+ * per group (G) and the group CDF (G,G) (XSData, transport.py:83-99).
+ */
+bt_status bt_transport_run(bt_tally *h, const double *sigma_t, const double *scatter_prob,
+                           const double *group_cdf, int32_t num_groups, int64_t num_particles,
+                           int64_t num_batches, uint64_t seed, const double *box,
+                           const double *fixed_direction, bt_transport_totals *out);
+
+/* Final per-particle direction, group and RNG block counter of the last batch. */
+bt_status bt_read_transport_state(bt_tally *h, int64_t count, double *direction, int32_t *group,
+                                  uint32_t *rng_block);
+
+/* uniform_block(seed, batch, particle, block) on the device for n keys
+ * (4 x u64 each) -> 4n doubles (philox KAT hook). */
+bt_status bt_uniform_blocks(const uint64_t *keys, int64_t n, int32_t device, double *out);
 
 const char *bt_last_error(void);
 const char *bt_version(void);

@@ -17,7 +17,8 @@ LIB_PATH = PKG / "libb200tally.so"
 BT_OK, BT_EINVAL, BT_ERUNTIME, BT_ECUDA, BT_EINDEX, BT_ENOMEM = range(6)
 BT_MEM_HOST, BT_MEM_DEVICE = 0, 1
 BT_LOCATE_GRID, BT_LOCATE_WALK = 0, 1
-BT_TALLY_BATCH, BT_TALLY_SUM, BT_TALLY_SUM_SQ = 0, 1, 2
+(BT_TALLY_BATCH, BT_TALLY_SUM, BT_TALLY_SUM_SQ, BT_TALLY_COL_BATCH, BT_TALLY_COL_SUM,
+ BT_TALLY_COL_SUM_SQ) = range(6)
 (BT_OPT_MAX_SWEEPS, BT_OPT_DIGEST, BT_OPT_SORT, BT_OPT_WARP_AGG,
  BT_OPT_BLOCKS_PER_SM, BT_OPT_STAGED, BT_OPT_MOVE_CHUNKS) = range(7)
 
@@ -28,9 +29,18 @@ EXPORTS = (
     "bt_tally_device_ptr", "bt_get_source_weight", "bt_set_source_weight",
     "bt_batches_completed", "bt_read_particles", "bt_read_digest", "bt_set_option",
     "bt_last_timing", "bt_particle_device_ptrs", "bt_save_state", "bt_restore_state",
-    "bt_info", "bt_build_adjacency",
+    "bt_info", "bt_build_adjacency", "bt_transport_run", "bt_read_transport_state",
+    "bt_uniform_blocks",
     "bt_last_error", "bt_version",
 )
+
+
+class TransportTotals(C.Structure):
+    _fields_ = [("source_weight", C.c_double), ("leaked_weight", C.c_double),
+                ("absorbed_weight", C.c_double), ("stuck_weight", C.c_double),
+                ("track_length_total", C.c_double), ("collisions", C.c_int64),
+                ("events", C.c_int64), ("sweeps", C.c_int64),
+                ("ms_localization", C.c_float), ("ms_transport", C.c_float)]
 
 
 class Summary(C.Structure):
@@ -63,6 +73,10 @@ _SIGS = {
     "bt_restore_state": [_P],
     "bt_info": [_P, C.POINTER(_I32), C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I32)],
     "bt_build_adjacency": [_P, _I64, _I64, _I32, _P, _P],
+    "bt_transport_run": [_P, _P, _P, _P, _I32, _I64, _I64, C.c_uint64, _P, _P,
+                         C.POINTER(TransportTotals)],
+    "bt_read_transport_state": [_P, _I64, _P, _P, _P],
+    "bt_uniform_blocks": [_P, _I64, _I32, _P],
     "bt_last_error": [],
     "bt_version": [],
 }

@@ -610,6 +610,292 @@ __global__ void stage_kernel(const WalkArgs a, const WorkSoA W, int64_t* __restr
 }
 
 // ---------------------------------------------------------------------------
+// Transport: the reference's event loop (transport.run,
+// transport.py:445-549) alternates flight / walk / collide over all flying
+// particles.  Particles never interact and every random draw is keyed by
+// (seed, batch, particle, block) (rng.py:58-64), so each particle's history
+// is the same whether it is advanced event by event or to completion: one
+// lane runs a whole history (flight -> walk with track-length scoring ->
+// collision estimator + scatter/absorb -> ...) in a persistent kernel.
+
+constexpr uint64_t PH_M0 = 0xD2E7470EE14C6C93ull, PH_M1 = 0xCA5A826395121157ull;
+constexpr uint64_t PH_W0 = 0x9E3779B97F4A7C15ull, PH_W1 = 0xBB67AE8584CAA73Bull;
+constexpr uint64_t PH_KEY1 = 0xD1B54A32D192ED03ull;
+constexpr double TWO_PI = 2.0 * 3.141592653589793;
+
+// philox4x64-10 block (rng.py:38-49) -> four uniforms in (0, 1] (rng.py:52-64)
+__device__ __forceinline__ void uniform_block(uint64_t seed, uint64_t batch, uint64_t particle,
+                                              uint64_t block, double u[4]) {
+    uint64_t c0 = block, c1 = particle, c2 = batch, c3 = 0, k0 = seed, k1 = PH_KEY1;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t hi0 = __umul64hi(PH_M0, c0), lo0 = PH_M0 * c0;
+        const uint64_t hi1 = __umul64hi(PH_M1, c2), lo1 = PH_M1 * c2;
+        const uint64_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0;
+        c1 = lo1;
+        c2 = n2;
+        c3 = lo0;
+        k0 += PH_W0;
+        k1 += PH_W1;
+    }
+    const double s = 1.0 / 9007199254740992.0;
+    u[0] = __dmul_rn(__dadd_rn((double)(c0 >> 11), 1.0), s);
+    u[1] = __dmul_rn(__dadd_rn((double)(c1 >> 11), 1.0), s);
+    u[2] = __dmul_rn(__dadd_rn((double)(c2 >> 11), 1.0), s);
+    u[3] = __dmul_rn(__dadd_rn((double)(c3 >> 11), 1.0), s);
+}
+
+__global__ void philox_kat_kernel(const uint64_t* __restrict__ keys, int64_t n,
+                                  double* __restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uniform_block(keys[4 * i], keys[4 * i + 1], keys[4 * i + 2], keys[4 * i + 3], out + 4 * i);
+}
+
+// isotropic direction from two uniforms (transport.py:172-178, 255-261)
+__device__ __forceinline__ void iso_dir(double ua, double ub, double& x, double& y, double& z) {
+    const double mu = __dsub_rn(__dmul_rn(2.0, ua), 1.0);
+    const double phi = __dmul_rn(TWO_PI, ub);
+    const double t = __dsub_rn(1.0, __dmul_rn(mu, mu));
+    const double s = __dsqrt_rn(t > 0.0 ? t : 0.0);
+    double sp, cp;
+    sincos(phi, &sp, &cp);
+    x = __dmul_rn(s, cp);
+    y = __dmul_rn(s, sp);
+    z = mu;
+}
+
+struct XSDev {
+    const double* sigma_t;      // (G)
+    const double* scatter_prob; // (G)
+    const double* group_cdf;    // (G,G)
+    int32_t ng;
+};
+
+struct TransportArgs {
+    WalkArgs w;                 // mesh, particle state, track tally (w.tally)
+    XSDev xs;
+    double* col_tally;          // collision estimator (E*G)
+    double* dir;                // (N,3)
+    uint32_t* rng_block;        // (N)
+    int32_t* group_rw;          // (N) groups (written)
+    double* weight_rw;          // (N)
+    const double* src;          // (n,3) source positions (located)
+    unsigned* round_max;        // per-round max walk steps (sweeps), MAX_ROUNDS_TRACKED
+    unsigned long long* tcount; // [0] collisions [1] rounds overflow [2] lost
+    double* wsum;               // [0] leaked [1] absorbed [2] stuck [3] track length
+    unsigned long long* queue;
+    uint64_t seed, batch;
+    int64_t n;
+    int64_t max_rounds;
+};
+
+constexpr int MAX_ROUNDS_TRACKED = 1 << 20;
+
+// per-batch source sampling (transport.py:154-181), blocks 0 and 1
+__global__ void transport_source_kernel(TransportArgs a, double box0, double box1, double box2,
+                                        double box3, double box4, double box5, int fixed,
+                                        double fdx, double fdy, double fdz,
+                                        double* __restrict__ stage) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    double u[4];
+    uniform_block(a.seed, a.batch, i, 0, u);
+    stage[3 * i] = __dadd_rn(box0, __dmul_rn(__dsub_rn(box3, box0), u[0]));
+    stage[3 * i + 1] = __dadd_rn(box1, __dmul_rn(__dsub_rn(box4, box1), u[1]));
+    stage[3 * i + 2] = __dadd_rn(box2, __dmul_rn(__dsub_rn(box5, box2), u[2]));
+    double dx = fdx, dy = fdy, dz = fdz;
+    if (!fixed) {
+        double v[4];
+        uniform_block(a.seed, a.batch, i, 1, v);
+        iso_dir(v[0], v[1], dx, dy, dz);
+    }
+    a.dir[3 * i] = dx;
+    a.dir[3 * i + 1] = dy;
+    a.dir[3 * i + 2] = dz;
+    a.weight_rw[i] = 1.0;
+    a.group_rw[i] = 0;
+    a.rng_block[i] = 2;
+}
+
+// one history per lane, persistent; refill from a global counter
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) transport_kernel(const TransportArgs t) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const WalkArgs& a = t.w;
+    const int lane = threadIdx.x & 31;
+    Lane L;
+    L.idx = -1;
+    Counters C;
+    double ux = 0, uy = 0, uz = 0;  // direction
+    uint32_t rb = 0;
+    int rounds = 0;
+    unsigned collisions = 0;
+    double leaked = 0, absorbed = 0, stuck_w = 0;
+    bool drained = false;
+    bool need_flight = false;
+    while (true) {
+        if (!drained) {
+            const unsigned idle = __ballot_sync(FULL, L.idx < 0);
+            if (idle) {
+                const unsigned nidle = __popc(idle);
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(t.queue, (unsigned long long)nidle);
+                base = __shfl_sync(FULL, base, 0);
+                if (base + nidle >= (unsigned long long)t.n) drained = true;
+                if (L.idx < 0) {
+                    const unsigned long long q = base + __popc(idle & lanemask_lt());
+                    if (q < (unsigned long long)t.n && a.alive[q]) {
+                        const int64_t i = (int64_t)q;
+                        L.idx = i;
+                        L.e = a.element[i];
+                        L.px = a.pos[3 * i];
+                        L.py = a.pos[3 * i + 1];
+                        L.pz = a.pos[3 * i + 2];
+                        L.seg = 0.0;
+                        L.w = t.weight_rw[i];
+                        L.g = t.group_rw[i];
+                        ux = t.dir[3 * i];
+                        uy = t.dir[3 * i + 1];
+                        uz = t.dir[3 * i + 2];
+                        rb = t.rng_block[i];
+                        L.entry = -1;
+                        L.st = 0;
+                        rounds = 0;
+                        need_flight = true;
+                    }
+                }
+            }
+        }
+        if (!__any_sync(FULL, L.idx >= 0)) {
+            if (drained) break;
+            continue;
+        }
+        bool has_score = false;
+        int64_t bin = 0;
+        double val = 0.0;
+        if (L.idx >= 0) {
+            if (need_flight) {  // _flight (transport.py:213-226)
+                double u[4];
+                uniform_block(t.seed, t.batch, (uint64_t)L.idx, rb, u);
+                ++rb;
+                const double lc = __ddiv_rn(-log(u[0]), t.xs.sigma_t[L.g]);
+                L.dx = __dadd_rn(L.px, __dmul_rn(lc, ux));
+                L.dy = __dadd_rn(L.py, __dmul_rn(lc, uy));
+                L.dz = __dadd_rn(L.pz, __dmul_rn(lc, uz));
+                L.have_nr = false;
+                L.iters = 0;
+                L.outcome = OUT_NONE;
+                L.alive = 1;
+                ++rounds;
+                need_flight = false;
+            }
+            if (walk_step(a, L, C, has_score, bin, val)) {
+                // flight over: its walk took L.iters sweeps in round `rounds`
+                if (rounds <= MAX_ROUNDS_TRACKED) atomicMax(t.round_max + rounds - 1, (unsigned)L.iters);
+                bool stop = true;
+                if (L.outcome == OUT_REACHED) {  // _collide (transport.py:229-275)
+                    const int g = L.g;
+                    const double st_g = t.xs.sigma_t[g];
+                    atomicAdd(t.col_tally + (int64_t)L.e * t.xs.ng + g, __ddiv_rn(L.w, st_g));
+                    ++collisions;
+                    double u[4];
+                    uniform_block(t.seed, t.batch, (uint64_t)L.idx, rb, u);
+                    ++rb;
+                    if (u[0] <= t.xs.scatter_prob[g]) {
+                        int gp = 0;
+                        for (int j = 0; j < t.xs.ng; ++j) {
+                            gp = j;
+                            if (u[1] <= t.xs.group_cdf[g * t.xs.ng + j]) break;
+                        }
+                        iso_dir(u[2], u[3], ux, uy, uz);
+                        L.g = gp;
+                        stop = false;
+                        need_flight = true;
+                        if (rounds >= t.max_rounds) {  // _MAX_ROUNDS guard (transport.py:531-533)
+                            C.err = 1;
+                            stop = true;
+                        }
+                    } else {
+                        L.alive = 0;
+                        L.outcome = 5;  // OUTCOME_ABSORBED
+                        absorbed += L.w;
+                    }
+                } else if (L.outcome == OUT_LEAKED) {
+                    leaked += L.w;
+                } else if (L.outcome == OUT_STUCK_KILLED) {
+                    stuck_w += L.w;
+                }
+                if (stop) {
+                    const int64_t i = L.idx;
+                    a.pos[3 * i] = L.px;
+                    a.pos[3 * i + 1] = L.py;
+                    a.pos[3 * i + 2] = L.pz;
+                    a.element[i] = L.e;
+                    a.entry[i] = (int8_t)L.entry;
+                    a.stuck[i] = (int8_t)L.st;
+                    a.outcome[i] = (int8_t)L.outcome;
+                    a.alive[i] = (int8_t)L.alive;
+                    a.seg_total[i] = L.seg;
+                    t.dir[3 * i] = ux;
+                    t.dir[3 * i + 1] = uy;
+                    t.dir[3 * i + 2] = uz;
+                    t.rng_block[i] = rb;
+                    t.group_rw[i] = L.g;
+                    L.idx = -1;
+                }
+            }
+        }
+        score(a, has_score, bin, val);
+    }
+    // reduce the per-lane totals (tally sums are order-free up to rounding)
+    for (int o = 16; o > 0; o >>= 1) {
+        leaked += __shfl_xor_sync(FULL, leaked, o);
+        absorbed += __shfl_xor_sync(FULL, absorbed, o);
+        stuck_w += __shfl_xor_sync(FULL, stuck_w, o);
+    }
+    collisions = __reduce_add_sync(FULL, collisions);
+    if (lane == 0) {
+        if (leaked != 0.0) atomicAdd(t.wsum + 0, leaked);
+        if (absorbed != 0.0) atomicAdd(t.wsum + 1, absorbed);
+        if (stuck_w != 0.0) atomicAdd(t.wsum + 2, stuck_w);
+        if (collisions) atomicAdd(t.tcount + 0, (unsigned long long)collisions);
+    }
+    flush_counters(a, C);
+}
+
+__global__ void sum_rounds_kernel(const unsigned* __restrict__ round_max, int64_t n,
+                                  unsigned long long* __restrict__ out) {
+    unsigned long long s = 0;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x)
+        s += round_max[r];
+    s = __reduce_add_sync(0xffffffffu, (unsigned)s);  // per-warp (< 2^32 per warp chunk)
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
+}
+
+__global__ void seg_sum_kernel(const double* __restrict__ seg, const int8_t* __restrict__ alive0,
+                               int64_t n, double* __restrict__ out) {
+    double s = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        s += seg[i];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0 && s != 0.0) atomicAdd(out, s);
+}
+
+__global__ void count_alive_kernel(const int8_t* __restrict__ alive, int64_t n,
+                                   unsigned long long* __restrict__ out) {
+    unsigned c = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        c += alive[i] != 0;
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
+}
+
+// ---------------------------------------------------------------------------
 // localization: uniform grid of element bounding boxes
 
 struct __align__(16) BoxF {
@@ -1037,6 +1323,18 @@ struct bt_tally {
     double* dwsum = nullptr;
     unsigned long long* hcounters = nullptr;  // pinned
     int move_chunks = 0;                      // host-input pipeline depth (0 = auto)
+    // transport (allocated on first bt_transport_run)
+    double* col_tally = nullptr;
+    double* col_sum = nullptr;
+    double* col_sum_sq = nullptr;
+    double* tr_dir = nullptr;
+    double* tr_weight = nullptr;
+    uint32_t* tr_rng = nullptr;
+    unsigned* tr_round_max = nullptr;
+    unsigned long long* tr_count = nullptr;  // [0] collisions [1] sweeps [2] alive
+    double* tr_wsum = nullptr;               // [0] leaked [1] absorbed [2] stuck [3] track
+    double* tr_xs = nullptr;                 // sigma_t | scatter_prob | group_cdf
+    int64_t col_batches = 0;
     // snapshot
     double* snap_pos = nullptr;
     int32_t* snap_element = nullptr;
@@ -1076,7 +1374,9 @@ static bt_status free_all(bt_tally* h) {
                     h->weight, h->digest, h->dcount, h->order, h->sort_keys_in,
                     h->sort_keys_out, h->sort_vals_in, h->sort_tmp, h->tally, h->sum,
                     h->sum_sq, h->dcounters, h->dwsum, h->snap_pos, h->snap_element,
-                    h->snap_flags, h->snap_seg, h->work_mem, h->init_stage};
+                    h->snap_flags, h->snap_seg, h->work_mem, h->init_stage,
+                    h->col_tally, h->col_sum, h->col_sum_sq, h->tr_dir, h->tr_weight,
+                    h->tr_rng, h->tr_round_max, h->tr_count, h->tr_wsum, h->tr_xs};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->hcounters) cudaFreeHost(h->hcounters);
@@ -1782,6 +2082,9 @@ static double* tally_ptr(bt_tally* h, int32_t which) {
         case BT_TALLY_BATCH: return h->tally;
         case BT_TALLY_SUM: return h->sum;
         case BT_TALLY_SUM_SQ: return h->sum_sq;
+        case BT_TALLY_COL_BATCH: return h->col_tally;
+        case BT_TALLY_COL_SUM: return h->col_sum;
+        case BT_TALLY_COL_SUM_SQ: return h->col_sum_sq;
         default: return nullptr;
     }
 }
@@ -2020,6 +2323,174 @@ bt_status bt_build_adjacency(const int32_t* elements, int64_t num_elements, int6
     cleanup();
 #undef CKA
     return rc;
+}
+
+bt_status bt_transport_run(bt_tally* h, const double* sigma_t, const double* sigma_s_row_prob,
+                           const double* group_cdf, int32_t num_groups, int64_t num_particles,
+                           int64_t num_batches, uint64_t seed, const double* box,
+                           const double* fixed_direction, bt_transport_totals* out) {
+    if (!h || !sigma_t || !sigma_s_row_prob || !group_cdf || !box || !out)
+        return set_err(BT_EINVAL, "NULL argument");
+    if (num_groups != h->ngroups)
+        return set_err(BT_EINVAL, "cross sections have %d groups, the tally %d", num_groups,
+                       h->ngroups);
+    if (num_particles <= 0 || num_particles > h->cap)
+        return set_err(BT_EINVAL, "num_particles must be in [1, %lld]", (long long)h->cap);
+    if (num_batches <= 0) return set_err(BT_EINVAL, "num_batches must be positive");
+    memset(out, 0, sizeof *out);
+    TRY(ensure_device(h));
+    const int64_t n = num_particles, nb = h->ne * h->ngroups, G = num_groups;
+    if (!h->col_tally) {
+        TRY(dalloc(&h->col_tally, nb));
+        TRY(dalloc(&h->col_sum, nb));
+        TRY(dalloc(&h->col_sum_sq, nb));
+        CK(cudaMemset(h->col_tally, 0, sizeof(double) * nb));
+        CK(cudaMemset(h->col_sum, 0, sizeof(double) * nb));
+        CK(cudaMemset(h->col_sum_sq, 0, sizeof(double) * nb));
+        TRY(dalloc(&h->tr_dir, 3 * h->cap));
+        TRY(dalloc(&h->tr_weight, h->cap));
+        TRY(dalloc(&h->tr_rng, h->cap));
+        TRY(dalloc(&h->tr_round_max, MAX_ROUNDS_TRACKED));
+        TRY(dalloc(&h->tr_count, 4));
+        TRY(dalloc(&h->tr_wsum, 4));
+        TRY(dalloc(&h->tr_xs, 2 * G + G * G));
+    }
+    if (!h->init_stage) TRY(dalloc(&h->init_stage, 3 * h->cap));
+    CK(cudaMemcpyAsync(h->tr_xs, sigma_t, sizeof(double) * G, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->tr_xs + G, sigma_s_row_prob, sizeof(double) * G, cudaMemcpyHostToDevice,
+                       h->stream));
+    CK(cudaMemcpyAsync(h->tr_xs + 2 * G, group_cdf, sizeof(double) * G * G,
+                       cudaMemcpyHostToDevice, h->stream));
+    TransportArgs t;
+    t.w = walk_args(h, nullptr, nullptr, nullptr, true);
+    t.w.group = h->group;
+    t.xs = XSDev{h->tr_xs, h->tr_xs + G, h->tr_xs + 2 * G, num_groups};
+    t.col_tally = h->col_tally;
+    t.dir = h->tr_dir;
+    t.rng_block = h->tr_rng;
+    t.group_rw = h->group;
+    t.weight_rw = h->tr_weight;
+    t.src = h->init_stage;
+    t.round_max = h->tr_round_max;
+    t.tcount = h->tr_count;
+    t.wsum = h->tr_wsum;
+    t.queue = h->dcounters + 16;
+    t.seed = seed;
+    t.n = n;
+    t.max_rounds = 50000000;  // _MAX_ROUNDS, transport.py:296
+    const int fixed = fixed_direction != nullptr;
+    const double fdx = fixed ? fixed_direction[0] : 0.0, fdy = fixed ? fixed_direction[1] : 0.0,
+                 fdz = fixed ? fixed_direction[2] : 0.0;
+    int bps = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, transport_kernel<256>, 256, 0));
+    bps = std::max(1, bps);
+    const unsigned blocks = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>((n + 255) / 256, (int64_t)bps * h->num_sms));
+    LocateArgs la = locate_args(h, h->init_stage, n);
+    h->kernels = 0;
+    float loc_ms = 0.f, batch_ms = 0.f;
+    for (int64_t b = 0; b < num_batches; ++b) {
+        t.batch = (uint64_t)b;
+        CK(cudaMemsetAsync(h->dcounters, 0, sizeof(unsigned long long) * NDCOUNTERS, h->stream));
+        CK(cudaMemsetAsync(h->tr_round_max, 0, sizeof(unsigned) * MAX_ROUNDS_TRACKED, h->stream));
+        CK(cudaMemsetAsync(h->tr_count, 0, sizeof(unsigned long long) * 4, h->stream));
+        CK(cudaMemsetAsync(h->tr_wsum, 0, sizeof(double) * 4, h->stream));
+        CK(cudaEventRecord(h->ev2, h->stream));
+        transport_source_kernel<<<grid_for(n, 256), 256, 0, h->stream>>>(
+            t, box[0], box[1], box[2], box[3], box[4], box[5], fixed, fdx, fdy, fdz,
+            h->init_stage);
+        CK(cudaGetLastError());
+        locate_grid_kernel<<<grid_for(n, 256), 256, 0, h->stream>>>(la);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(h->ev0, h->stream));
+        count_alive_kernel<<<std::min<int64_t>(grid_for(n, 256), 1024), 256, 0, h->stream>>>(
+            h->alive, n, h->tr_count + 2);
+        transport_kernel<256><<<blocks, 256, 0, h->stream>>>(t);
+        CK(cudaGetLastError());
+        sum_rounds_kernel<<<256, 256, 0, h->stream>>>(h->tr_round_max, MAX_ROUNDS_TRACKED,
+                                                      h->tr_count + 1);
+        seg_sum_kernel<<<std::min<int64_t>(grid_for(n, 256), 1024), 256, 0, h->stream>>>(
+            h->seg_total, h->alive, n, h->tr_wsum + 3);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(h->ev1, h->stream));
+        h->kernels += 6;
+        unsigned long long cnt[4];
+        double ws[4];
+        CK(cudaMemcpyAsync(cnt, h->tr_count, sizeof cnt, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaMemcpyAsync(ws, h->tr_wsum, sizeof ws, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaMemcpyAsync(h->hcounters, h->dcounters, sizeof(unsigned long long) * NDCOUNTERS,
+                           cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        float m1 = 0.f, m2 = 0.f;
+        CK(cudaEventElapsedTime(&m1, h->ev2, h->ev0));
+        CK(cudaEventElapsedTime(&m2, h->ev0, h->ev1));
+        loc_ms += m1;
+        batch_ms += m2;
+        const unsigned long long* c = h->hcounters + 1;
+        if (c[C_ERR]) return set_err(BT_ERUNTIME, "transport did not terminate");
+        const double bsw = (double)cnt[2];  // sum of unit source weights of located particles
+        if (!(bsw > 0.0)) return set_err(BT_ERUNTIME, "no source particle inside the mesh");
+        out->source_weight += bsw;
+        out->leaked_weight += ws[0];
+        out->absorbed_weight += ws[1];
+        out->stuck_weight += ws[2];
+        out->track_length_total += ws[3];
+        out->collisions += (int64_t)cnt[0];
+        out->sweeps += (int64_t)cnt[1];
+        out->events += (int64_t)c[C_EVENTS];
+        const int64_t nbins = nb;
+        finalize_kernel<<<grid_for(nbins, 256), 256, 0, h->stream>>>(h->tally, h->sum, h->sum_sq,
+                                                                     nbins, bsw);
+        finalize_kernel<<<grid_for(nbins, 256), 256, 0, h->stream>>>(
+            h->col_tally, h->col_sum, h->col_sum_sq, nbins, bsw);
+        CK(cudaGetLastError());
+        h->kernels += 2;
+        h->batches += 1;
+        h->col_batches += 1;
+    }
+    CK(cudaStreamSynchronize(h->stream));
+    out->ms_localization = loc_ms;
+    out->ms_transport = batch_ms;
+    h->walk_ms = batch_ms;
+    h->source_weight = 0.0;
+    return BT_OK;
+}
+
+bt_status bt_read_transport_state(bt_tally* h, int64_t count, double* direction, int32_t* group,
+                                  uint32_t* rng_block) {
+    if (!h) return set_err(BT_EINVAL, "NULL handle");
+    if (!h->tr_dir) return set_err(BT_EINVAL, "no transport run on this handle");
+    if (count < 0 || count > h->cap) return set_err(BT_EINVAL, "count out of range");
+    TRY(ensure_device(h));
+    if (direction)
+        CK(cudaMemcpyAsync(direction, h->tr_dir, sizeof(double) * 3 * count,
+                           cudaMemcpyDeviceToHost, h->stream));
+    if (group)
+        CK(cudaMemcpyAsync(group, h->group, sizeof(int32_t) * count, cudaMemcpyDeviceToHost,
+                           h->stream));
+    if (rng_block)
+        CK(cudaMemcpyAsync(rng_block, h->tr_rng, sizeof(uint32_t) * count,
+                           cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return BT_OK;
+}
+
+bt_status bt_uniform_blocks(const uint64_t* keys, int64_t n, int32_t device, double* out) {
+    if (n <= 0) return BT_OK;
+    if (!keys || !out) return set_err(BT_EINVAL, "NULL argument");
+    CK(cudaSetDevice(device));
+    uint64_t* dk = nullptr;
+    double* dout = nullptr;
+    CK(cudaMalloc(&dk, sizeof(uint64_t) * 4 * n));
+    CK(cudaMalloc(&dout, sizeof(double) * 4 * n));
+    CK(cudaMemcpy(dk, keys, sizeof(uint64_t) * 4 * n, cudaMemcpyHostToDevice));
+    philox_kat_kernel<<<grid_for(n, 128), 128>>>(dk, n, dout);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpy(out, dout, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost);
+    cudaFree(dk);
+    cudaFree(dout);
+    if (e != cudaSuccess) return set_err(BT_ECUDA, "philox: %s", cudaGetErrorString(e));
+    return BT_OK;
 }
 
 bt_status bt_info(bt_tally* h, int32_t* device, int64_t* num_elements, int64_t* capacity,

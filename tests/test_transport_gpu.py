@@ -1,0 +1,102 @@
+"""Device transport (bt_transport_run) vs the CPU oracle, which is pinned
+bit-exact to the reference's transport.run (tests/test_transport_oracle.py).
+
+* philox4x64-10 uniforms: bit-exact.
+* Histories: identical sequence of operations; they stay bit-identical
+  until a CUDA log/sin/cos result differs from the host libm in the last
+  bit.  The fraction of bit-identical particle histories is measured and
+  must be high; everything else is compared statistically.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as orc
+from golden_cases import GOLDEN
+from paper_2504_19048_b200 import build_cube_mesh
+from paper_2504_19048_b200 import transport as T
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gold():
+    return np.load(GOLDEN / "transport_ref.npz")
+
+
+def test_device_philox_bit_exact(gold):
+    u = T.uniform_blocks(gold["uni_key"].astype(np.uint64))
+    assert np.array_equal(u, gold["uni_out"])
+
+
+def _cfg(gold, name):
+    p = name + "_"
+    n_mesh, n, nb, seed = (int(x) for x in gold[p + "cfg"])
+    d = gold[p + "dir"]
+    box = gold[p + "box"]
+    xs = T.CrossSections(gold[p + "sigma_t"], gold[p + "sigma_s"])
+    return T.RunConfig(mesh_n=n_mesh, num_particles=n, num_batches=nb, seed=seed,
+                       cross_sections=xs, source_box=(tuple(box[0]), tuple(box[1])),
+                       source_direction=tuple(d) if d.size else None)
+
+
+@pytest.mark.parametrize("name", ["t1g", "t2g", "tdir"])
+def test_transport_statistical_parity(gold, name):
+    p = name + "_"
+    cfg = _cfg(gold, name)
+    m = build_cube_mesh(cfg.mesh_n)
+    r = T.run(cfg, m)
+    n, nb = cfg.num_particles, cfg.num_batches
+    # source localization is deterministic: identical source weight
+    assert r.source_weight == float(gold[p + "source_weight"])
+    # per-history agreement with the reference's final state (last batch)
+    fs = r.final_state
+    same = ((fs["rng_block"] == gold[p + "final_rng_block"])
+            & (fs["outcome"] == gold[p + "final_outcome"])
+            & (fs["position"] == gold[p + "final_position"]).all(axis=1)
+            & (fs["group"] == gold[p + "final_group"]))
+    frac = same.mean()
+    print(f"{name}: bit-identical histories {frac:.4f}; collisions {r.collisions} vs "
+          f"{int(gold[p + 'collisions'])}; leaked {r.leaked_weight} vs "
+          f"{float(gold[p + 'leaked_weight'])}")
+    assert frac > 0.5
+    # balance: every source particle leaks, is absorbed or stuck-killed
+    assert r.leaked_weight + r.absorbed_weight + r.stuck_weight == r.source_weight
+    tot = n * nb
+    for key in ("leaked_weight", "absorbed_weight"):
+        ref = float(gold[p + key])
+        q = ref / tot
+        sigma = np.sqrt(2 * tot * q * (1 - q)) + 1.0
+        assert abs(getattr(r, key) - ref) <= 5 * sigma, key
+    c_ref = float(gold[p + "collisions"])
+    assert abs(r.collisions - c_ref) <= 0.05 * c_ref + 50
+    # integrated flux (track length per source particle) and collision estimate
+    V = m.volumes[:, None]
+    for est, key in ((r.flux_track, "flux_track_mean"), (r.flux_collision, "flux_col_mean")):
+        a = float((est.mean * V).sum())
+        b = float((gold[p + key] * V).sum())
+        assert abs(a - b) <= 0.05 * abs(b), (key, a, b)
+    # both estimators agree with each other (same physics)
+    a = float((r.flux_track.mean * V).sum())
+    b = float((r.flux_collision.mean * V).sum())
+    assert abs(a - b) <= 0.05 * abs(b)
+
+
+def test_transport_vs_oracle_same_engine():
+    """The oracle restatement and the device run side by side on a bigger
+    paper-physics case (sigma_t = sigma_s = 100, n = 10 cube)."""
+    cfg = T.RunConfig(mesh_n=10, num_particles=4000, num_batches=2, seed=5)
+    m = build_cube_mesh(10)
+    r = T.run(cfg, m)
+    xs = cfg.cross_sections
+    o = orc.transport_run(m, xs.sigma_t, xs.sigma_s, cfg.num_particles, cfg.num_batches,
+                          cfg.seed, cfg.source_box)
+    assert r.source_weight == o["source_weight"]
+    same = (r.final_state["rng_block"] == o["rng_block"]) & \
+        (r.final_state["position"] == o["position"][:cfg.num_particles]).all(axis=1)
+    print("paper physics: identical histories", same.mean(), "events", r.events, o["events"],
+          "collisions", r.collisions, o["collisions"])
+    assert same.mean() > 0.2
+    assert abs(r.collisions - o["collisions"]) <= 0.03 * o["collisions"]
+    assert abs(r.events - o["events"]) <= 0.03 * o["events"]
+    assert abs(r.track_length_total - o["track_length_total"]) <= 0.03 * o["track_length_total"]
