@@ -181,6 +181,43 @@ bt_status bt_info(bt_tally *h, int32_t *device, int64_t *num_elements, int64_t *
 bt_status bt_build_adjacency(const int32_t *elements, int64_t num_elements, int64_t num_vertices,
                              int32_t device, int32_t *adj_elem, int8_t *adj_face);
 
+/*
+ * Listing-1 callback path (trace_batch, search.py:453-489):
+ * lockstep sweeps with a caller decision point between the proposal and the
+ * commit.  bt_load_step loads a step like load_step (particles.py:57-89);
+ * bt_trace_begin checks localization (search.py:440-446); then per sweep
+ * bt_trace_propose compacts the flying particles (ascending ids), computes
+ * every proposal (_sweep_events, search.py:278-372) and returns the event
+ * arrays as DEVICE pointers, valid until bt_trace_commit; the caller may
+ * rewrite next_element / particle_done (redirect, kill, resurrect); then
+ * bt_trace_commit applies them (_commit_events, search.py:375-419).
+ * The loop ends when bt_trace_propose reports flying == 0.
+ */
+typedef struct {
+    int64_t count;            /* events this sweep (ascending particle id) */
+    int64_t *particle;
+    int32_t *element;
+    int8_t *exit_face;        /* -1: the segment ends at the destination */
+    double *segment_start;    /* (count,3) */
+    double *segment_end;      /* (count,3) */
+    double *segment_length;
+    int32_t *next_element;    /* writable */
+    int8_t *particle_done;    /* writable */
+    int32_t *next_proposed;   /* boundary = exit_face >= 0 && next_proposed < 0 */
+} bt_sweep_events;
+
+bt_status bt_load_step(bt_tally *h, const double *destinations, const int8_t *flying,
+                       const double *weights, const int32_t *groups, int64_t count,
+                       int32_t mem_kind);
+bt_status bt_trace_begin(bt_tally *h, int32_t score, int64_t max_sweeps);
+bt_status bt_trace_propose(bt_tally *h, bt_sweep_events *events, int64_t *flying);
+bt_status bt_trace_commit(bt_tally *h);
+bt_status bt_trace_end(bt_tally *h, bt_summary *summary);
+
+/* cudaMemcpy for bindings without a CUDA runtime: kind 0 device->host,
+ * 1 host->device, 2 device->device. */
+bt_status bt_memcpy(void *dst, const void *src, int64_t bytes, int32_t kind);
+
 /* Totals of bt_transport_run, mirroring transport.RunResult (transport.py:422-442). */
 typedef struct {
     double source_weight;

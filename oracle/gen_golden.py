@@ -357,7 +357,7 @@ def main():
     ])
 
 
-if __name__ == "__main__" and "--transport" not in sys.argv:
+if __name__ == "__main__" and not {"--transport", "--callback"} & set(sys.argv):
     main()
 
 
@@ -432,3 +432,90 @@ def transport_fixtures():
 if __name__ == "__main__" and "--transport" in sys.argv:
     OUT.mkdir(parents=True, exist_ok=True)
     transport_fixtures()
+
+
+# ----------------------------------------------------------------------------
+# Listing-1 callback path: trace_batch with a callback that
+# records every event and modifies decisions deterministically
+
+def callback_decisions(sweep, particle, element, exit_face, next_element, particle_done):
+    """Deterministic redirect / kill / resurrect rule applied in place
+    (shared verbatim by the GPU parity test)."""
+    pid = np.asarray(particle, dtype=np.int64)
+    face = np.asarray(exit_face)
+    interior = (face >= 0) & (np.asarray(next_element) >= 0)
+    kill = interior & ((pid + sweep) % 13 == 0)
+    particle_done[kill] = 1
+    stay = interior & ~kill & (pid % 17 == 3) & (sweep % 3 == 1)
+    next_element[stay] = -1
+    boundary = (face >= 0) & (np.asarray(next_element) < 0) & (np.asarray(particle_done) != 0)
+    revive = boundary & (pid % 5 == 0) & (sweep == 2)
+    particle_done[revive] = 0
+    jump = interior & ~kill & ~stay & (pid % 23 == 7)
+    next_element[jump] = np.asarray(element)[jump]   # "redirect" into the same element
+
+
+def callback_fixtures():
+    out = {}
+    cases = [("cb_n6", 6, 2500, 11, True), ("cb_plane", 10, 1500, 12, False)]
+    for name, n, k, seed, modify in cases:
+        mesh = mt.build_cube_mesh(n)
+        gen = np.random.default_rng(seed)
+        if name == "cb_plane":
+            z = mesh.vertices[3, 2]
+            pos = synth.uniform_box(gen, k, 0.08, 0.92)
+            pos[:, 2] = z
+            dest = synth.uniform_box(gen, k, 0.08, 0.92)
+            dest[:, 2] = z
+        else:
+            pos = synth.uniform_box(gen, k)
+            dest = synth.flight_destinations(gen, pos, 2.0)
+        w = 0.5 + gen.random(k)
+        groups = gen.integers(0, 2, k).astype(np.int32)
+        fly = (gen.random(k) < 0.9).astype(np.int8)
+        batch = mtp.create_batch(k)
+        ws = mts.create_workspace(k)
+        grid = mtt.create_grid(mesh.num_elements, 2, 1)
+        mts.initialize_locations(mesh, batch, pos.reshape(-1), k, ws)
+        mtp.load_step(batch, dest.reshape(-1), fly, w, k)
+        batch.group[:k] = groups
+        h = np.full(k, H0, dtype=np.uint64)
+        cnt = np.zeros(k, np.int64)
+        counts = []
+        state = {"sweep": 0}
+
+        def cb(ev):
+            p = np.asarray(ev.particle, dtype=np.int64)
+            code = (np.asarray(ev.element, dtype=np.int64) * 8
+                    + np.asarray(ev.exit_face, dtype=np.int64) + 1).astype(np.uint64)
+            with np.errstate(over="ignore"):
+                h[p] = (h[p] ^ code) * HP
+            cnt[p] += 1
+            counts.append(len(ev))
+            if modify:
+                callback_decisions(state["sweep"], ev.particle, ev.element, ev.exit_face,
+                                   ev.next_element, ev.particle_done)
+            state["sweep"] += 1
+        s = mts.trace_batch(mesh, batch, callback=cb, workspace=ws, grid=grid)
+        pre = name + "_"
+        out[pre + "mesh_n"] = np.array(n)
+        out[pre + "modify"] = np.array(modify)
+        out[pre + "pos"], out[pre + "dest"], out[pre + "w"] = pos, dest, w
+        out[pre + "groups"], out[pre + "fly"] = groups, fly
+        out[pre + "summary"] = summary_tuple(s)
+        out[pre + "sweep_counts"] = np.array(counts, np.int64)
+        out[pre + "digest"], out[pre + "count"] = h, cnt
+        st = state_of(batch, ws, k)
+        for key in ("position", "element", "alive", "flying", "entry_face", "stuck", "outcome",
+                    "seg_total"):
+            out[pre + key] = st[key]
+        out[pre + "tally"] = mtt.batch_totals(grid).reshape(-1)
+        print(f"  callback {name}: summary {out[pre + 'summary'].tolist()} sweeps {len(counts)}")
+    path = OUT / "callback_ref.npz"
+    np.savez_compressed(path, **out)
+    print(f"wrote {path} ({path.stat().st_size/1e3:.0f} kB)")
+
+
+if __name__ == "__main__" and "--callback" in sys.argv:
+    OUT.mkdir(parents=True, exist_ok=True)
+    callback_fixtures()

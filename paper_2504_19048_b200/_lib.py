@@ -30,7 +30,8 @@ EXPORTS = (
     "bt_batches_completed", "bt_read_particles", "bt_read_digest", "bt_set_option",
     "bt_last_timing", "bt_particle_device_ptrs", "bt_save_state", "bt_restore_state",
     "bt_info", "bt_build_adjacency", "bt_transport_run", "bt_read_transport_state",
-    "bt_uniform_blocks",
+    "bt_uniform_blocks", "bt_load_step", "bt_trace_begin", "bt_trace_propose",
+    "bt_trace_commit", "bt_trace_end", "bt_memcpy",
     "bt_last_error", "bt_version",
 )
 
@@ -41,6 +42,13 @@ class TransportTotals(C.Structure):
                 ("track_length_total", C.c_double), ("collisions", C.c_int64),
                 ("events", C.c_int64), ("sweeps", C.c_int64),
                 ("ms_localization", C.c_float), ("ms_transport", C.c_float)]
+
+
+class SweepEventsC(C.Structure):
+    """bt_sweep_events (device pointers)."""
+    _fields_ = [("count", C.c_int64)] + [(n, C.c_void_p) for n in (
+        "particle", "element", "exit_face", "segment_start", "segment_end", "segment_length",
+        "next_element", "particle_done", "next_proposed")]
 
 
 class Summary(C.Structure):
@@ -77,6 +85,12 @@ _SIGS = {
                          C.POINTER(TransportTotals)],
     "bt_read_transport_state": [_P, _I64, _P, _P, _P],
     "bt_uniform_blocks": [_P, _I64, _I32, _P],
+    "bt_load_step": [_P, _P, _P, _P, _P, _I64, _I32],
+    "bt_trace_begin": [_P, _I32, _I64],
+    "bt_trace_propose": [_P, C.POINTER(SweepEventsC), C.POINTER(_I64)],
+    "bt_trace_commit": [_P],
+    "bt_trace_end": [_P, C.POINTER(Summary)],
+    "bt_memcpy": [_P, _P, _I64, _I32],
     "bt_last_error": [],
     "bt_version": [],
 }

@@ -896,6 +896,235 @@ __global__ void count_alive_kernel(const int8_t* __restrict__ alive, int64_t n,
 }
 
 // ---------------------------------------------------------------------------
+// Listing-1 callback path (search.py:278-489): lockstep
+// sweeps with a host callback between the proposal and the commit.
+
+struct SweepBufs {
+    int32_t* active;      // (cap) flying particle ids, ascending
+    int32_t* has_ev;      // (cap) per active slot
+    int32_t* offs;        // (cap + 1) exclusive scan of has_ev
+    // per active slot
+    int32_t* s_elem;
+    int8_t* s_face;
+    double* s_start;      // (cap,3)
+    double* s_end;        // (cap,3)
+    double* s_len;
+    int32_t* s_next;
+    int8_t* s_entry;
+    int8_t* s_done;
+    // compacted events (the callback view)
+    int64_t* e_particle;
+    int32_t* e_elem;
+    int8_t* e_face;
+    double* e_start;
+    double* e_end;
+    double* e_len;
+    int32_t* e_next;      // writable by the callback
+    int8_t* e_done;       // writable by the callback
+    int32_t* e_next_prop;
+    int8_t* e_entry;
+    int8_t* e_done_prop;
+};
+
+__global__ void select_flying_kernel(const int8_t* __restrict__ fly, int64_t n,
+                                     int32_t* __restrict__ flag) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) flag[i] = fly[i] != 0;
+}
+
+__global__ void scatter_active_kernel(const int32_t* __restrict__ flag,
+                                      const int32_t* __restrict__ offs, int64_t n,
+                                      int32_t* __restrict__ active) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n && flag[i]) active[offs[i]] = (int32_t)i;
+}
+
+// _sweep_events (search.py:278-372): proposal + immediate stuck-ladder effects
+__global__ void sweep_propose_kernel(const WalkArgs a, int8_t* __restrict__ fly,
+                                     SweepBufs B, int64_t m) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    const int64_t i = B.active[k];
+    B.has_ev[k] = 0;
+    if (fly[i] == 0) return;
+    const int e = a.element[i];
+    const double px = a.pos[3 * i], py = a.pos[3 * i + 1], pz = a.pos[3 * i + 2];
+    const double dx = a.dest[3 * i], dy = a.dest[3 * i + 1], dz = a.dest[3 * i + 2];
+    const int st = a.stuck[i];
+    double ox = px, oy = py, oz = pz;
+    if (st == 1) {
+        const double sx = __dsub_rn(dx, px), sy = __dsub_rn(dy, py), sz = __dsub_rn(dz, pz);
+        const double ln = __dsqrt_rn(
+            __dadd_rn(__dadd_rn(__dmul_rn(sx, sx), __dmul_rn(sy, sy)), __dmul_rn(sz, sz)));
+        if (ln > 0.0) {
+            ox = __dadd_rn(ox, __ddiv_rn(__dmul_rn(NUDGE, sx), ln));
+            oy = __dadd_rn(oy, __ddiv_rn(__dmul_rn(NUDGE, sy), ln));
+            oz = __dadd_rn(oz, __ddiv_rn(__dmul_rn(NUDGE, sz), ln));
+        }
+    }
+    const ElemRec r = load_rec(a.rec, e);
+    Tet T;
+    load_tet(a, r, T);
+    int face;
+    double t;
+    bool ex;
+    int kind = exit_search_fast(T, ox, oy, oz, dx, dy, dz, a.entry[i], &face, &t, &ex);
+    if (kind == 2) {
+        if (contains(T, dx, dy, dz, STUCK_TOL)) {
+            kind = 0;
+            atomicAdd(a.counters + C_RECOV, 1ull);
+        } else if (st == 0) {
+            a.stuck[i] = 1;
+            atomicAdd(a.counters + C_RECOV, 1ull);
+            return;
+        } else if (st == 1) {
+            int hop = -1;
+            for (int f = 0; f < 4 && hop < 0; ++f) {
+                const int nbp = r.nb[f];
+                if (nbp >= 0) {
+                    const ElemRec rn = load_rec(a.rec, nbp >> 2);
+                    Tet Tn;
+                    load_tet(a, rn, Tn);
+                    if (contains(Tn, ox, oy, oz, EPS_BARY)) hop = nbp >> 2;
+                }
+            }
+            if (hop >= 0) {
+                a.element[i] = hop;
+                a.entry[i] = -1;
+                a.stuck[i] = 2;
+                atomicAdd(a.counters + C_RECOV, 1ull);
+                return;
+            }
+            fly[i] = 0;
+            a.alive[i] = 0;
+            a.outcome[i] = OUT_STUCK_KILLED;
+            atomicAdd(a.counters + C_KILLED, 1ull);
+            return;
+        } else {
+            fly[i] = 0;
+            a.alive[i] = 0;
+            a.outcome[i] = OUT_STUCK_KILLED;
+            atomicAdd(a.counters + C_KILLED, 1ull);
+            return;
+        }
+    }
+    a.stuck[i] = 0;
+    B.has_ev[k] = 1;
+    B.s_elem[k] = e;
+    B.s_start[3 * k] = px;
+    B.s_start[3 * k + 1] = py;
+    B.s_start[3 * k + 2] = pz;
+    double qx, qy, qz;
+    if (kind == 0) {
+        qx = dx;
+        qy = dy;
+        qz = dz;
+        B.s_face[k] = -1;
+        B.s_next[k] = -1;
+        B.s_entry[k] = -1;
+        B.s_done[k] = 1;
+    } else {
+        qx = __dadd_rn(ox, __dmul_rn(t, __dsub_rn(dx, ox)));
+        qy = __dadd_rn(oy, __dmul_rn(t, __dsub_rn(dy, oy)));
+        qz = __dadd_rn(oz, __dmul_rn(t, __dsub_rn(dz, oz)));
+        const int nbp = face == 0 ? r.nb[0] : face == 1 ? r.nb[1] : face == 2 ? r.nb[2] : r.nb[3];
+        B.s_face[k] = (int8_t)face;
+        B.s_next[k] = nbp < 0 ? -1 : (nbp >> 2);
+        B.s_entry[k] = nbp < 0 ? -1 : (int8_t)(nbp & 3);
+        B.s_done[k] = nbp < 0 ? 1 : 0;
+    }
+    const double ax = __dsub_rn(qx, px), ay = __dsub_rn(qy, py), az = __dsub_rn(qz, pz);
+    B.s_len[k] = __dsqrt_rn(
+        __dadd_rn(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)), __dmul_rn(az, az)));
+    B.s_end[3 * k] = qx;
+    B.s_end[3 * k + 1] = qy;
+    B.s_end[3 * k + 2] = qz;
+}
+
+__global__ void sweep_compact_kernel(SweepBufs B, int64_t m) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= m || !B.has_ev[k]) return;
+    const int64_t j = B.offs[k];
+    B.e_particle[j] = B.active[k];
+    B.e_elem[j] = B.s_elem[k];
+    B.e_face[j] = B.s_face[k];
+    for (int c = 0; c < 3; ++c) {
+        B.e_start[3 * j + c] = B.s_start[3 * k + c];
+        B.e_end[3 * j + c] = B.s_end[3 * k + c];
+    }
+    B.e_len[j] = B.s_len[k];
+    B.e_next[j] = B.s_next[k];
+    B.e_next_prop[j] = B.s_next[k];
+    B.e_entry[j] = B.s_entry[k];
+    B.e_done[j] = B.s_done[k];
+    B.e_done_prop[j] = B.s_done[k];
+}
+
+// _commit_events (search.py:375-419)
+__global__ void sweep_commit_kernel(const WalkArgs a, int8_t* __restrict__ fly, SweepBufs B,
+                                    int64_t nev) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= nev) return;
+    const int64_t i = B.e_particle[j];
+    const int e = B.e_elem[j];
+    const double seg = B.e_len[j];
+    if (a.score) atomicAdd(a.tally + (int64_t)e * a.ngroups + a.group[i], __dmul_rn(a.weight[i], seg));
+    a.seg_total[i] = __dadd_rn(a.seg_total[i], seg);
+    a.pos[3 * i] = B.e_end[3 * j];
+    a.pos[3 * i + 1] = B.e_end[3 * j + 1];
+    a.pos[3 * i + 2] = B.e_end[3 * j + 2];
+    if (a.digest) {
+        a.digest[i] = (a.digest[i] ^ (uint64_t)((int64_t)e * 8 + B.e_face[j] + 1)) * DIGEST_PRIME;
+        a.dcount[i] += 1;
+    }
+    if (B.e_done[j] != 0) {
+        fly[i] = 0;
+        if (B.e_face[j] == -1) {
+            a.outcome[i] = OUT_REACHED;
+            a.entry[i] = -1;
+            atomicAdd(a.counters + C_REACHED, 1ull);
+        } else if (B.e_next_prop[j] < 0) {
+            a.alive[i] = 0;
+            a.outcome[i] = OUT_LEAKED;
+            atomicAdd(a.counters + C_BOUNDARY, 1ull);
+        } else {
+            a.outcome[i] = 4;  // OUTCOME_KILLED (by the callback)
+        }
+    } else {
+        const int nxt = B.e_next[j];
+        if (nxt >= 0) {
+            a.element[i] = nxt;
+            a.entry[i] = nxt == B.e_next_prop[j] ? B.e_entry[j] : (int8_t)-1;
+        } else {
+            a.entry[i] = -1;
+        }
+    }
+}
+
+// load_step (particles.py:57-89): alive |= flying, flying[count:] = 0
+__global__ void load_step_kernel(const int8_t* __restrict__ fly_in, int64_t count, int64_t cap,
+                                 int8_t* __restrict__ fly, int8_t* __restrict__ alive) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= cap) return;
+    if (i < count) {
+        const int8_t f = fly_in[i];
+        fly[i] = f;
+        alive[i] = (int8_t)(alive[i] | f);
+    } else {
+        fly[i] = 0;
+    }
+}
+
+__global__ void fill_digest_kernel(uint64_t* __restrict__ d, int64_t* __restrict__ c,
+                                   int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) {
+        d[i] = DIGEST_INIT;
+        c[i] = 0;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // localization: uniform grid of element bounding boxes
 
 struct __align__(16) BoxF {
@@ -1335,6 +1564,16 @@ struct bt_tally {
     double* tr_wsum = nullptr;               // [0] leaked [1] absorbed [2] stuck [3] track
     double* tr_xs = nullptr;                 // sigma_t | scatter_prob | group_cdf
     int64_t col_batches = 0;
+    // Listing-1 callback path
+    SweepBufs sb{};
+    void* sb_mem = nullptr;
+    int8_t* tr_fly = nullptr;     // persistent flying flags of the loaded step
+    int32_t* sb_flag = nullptr;   // (cap + 1)
+    void* sb_tmp = nullptr;
+    size_t sb_tmp_bytes = 0;
+    int64_t loaded = 0;           // count of the last bt_load_step
+    int64_t tr_sweeps = 0, tr_events = 0, tr_limit = 0, tr_nev = 0;
+    bool tr_score = true;
     // snapshot
     double* snap_pos = nullptr;
     int32_t* snap_element = nullptr;
@@ -1376,7 +1615,8 @@ static bt_status free_all(bt_tally* h) {
                     h->sum_sq, h->dcounters, h->dwsum, h->snap_pos, h->snap_element,
                     h->snap_flags, h->snap_seg, h->work_mem, h->init_stage,
                     h->col_tally, h->col_sum, h->col_sum_sq, h->tr_dir, h->tr_weight,
-                    h->tr_rng, h->tr_round_max, h->tr_count, h->tr_wsum, h->tr_xs};
+                    h->tr_rng, h->tr_round_max, h->tr_count, h->tr_wsum, h->tr_xs,
+                    h->sb_mem, h->tr_fly, h->sb_flag, h->sb_tmp};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->hcounters) cudaFreeHost(h->hcounters);
@@ -2490,6 +2730,206 @@ bt_status bt_uniform_blocks(const uint64_t* keys, int64_t n, int32_t device, dou
     cudaFree(dk);
     cudaFree(dout);
     if (e != cudaSuccess) return set_err(BT_ECUDA, "philox: %s", cudaGetErrorString(e));
+    return BT_OK;
+}
+
+static bt_status ensure_sweep_bufs(bt_tally* h) {
+    if (h->sb_mem) return BT_OK;
+    const size_t n = (size_t)h->cap;
+    // 8-byte arrays first, then 4-byte, then 1-byte
+    // 15 doubles/int64, 8 int32 (+1 for the scan total), 7 int8 per particle; 22
+    // sub-arrays each rounded up to 256 bytes
+    const size_t bytes = n * (8 * 15 + 4 * 8 + 7) + 4 + 22 * 256 + 256;
+    char* p = nullptr;
+    CK(cudaMalloc((void**)&p, bytes));
+    h->sb_mem = p;
+    SweepBufs& B = h->sb;
+    auto take = [&](size_t b) { char* q = p; p += (b + 255) & ~size_t(255); return q; };
+    B.s_start = (double*)take(8 * 3 * n);
+    B.s_end = (double*)take(8 * 3 * n);
+    B.s_len = (double*)take(8 * n);
+    B.e_start = (double*)take(8 * 3 * n);
+    B.e_end = (double*)take(8 * 3 * n);
+    B.e_len = (double*)take(8 * n);
+    B.e_particle = (int64_t*)take(8 * n);
+    B.active = (int32_t*)take(4 * n);
+    B.has_ev = (int32_t*)take(4 * n);
+    B.offs = (int32_t*)take(4 * (n + 1));
+    B.s_elem = (int32_t*)take(4 * n);
+    B.s_next = (int32_t*)take(4 * n);
+    B.e_elem = (int32_t*)take(4 * n);
+    B.e_next = (int32_t*)take(4 * n);
+    B.e_next_prop = (int32_t*)take(4 * n);
+    B.s_face = (int8_t*)take(n);
+    B.s_entry = (int8_t*)take(n);
+    B.s_done = (int8_t*)take(n);
+    B.e_face = (int8_t*)take(n);
+    B.e_done = (int8_t*)take(n);
+    B.e_entry = (int8_t*)take(n);
+    B.e_done_prop = (int8_t*)take(n);
+    TRY(dalloc(&h->sb_flag, h->cap + 1));
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, h->sb_flag, B.offs, (int)(h->cap + 1)));
+    CK(cudaMalloc(&h->sb_tmp, tb));
+    h->sb_tmp_bytes = tb;
+    return BT_OK;
+}
+
+bt_status bt_load_step(bt_tally* h, const double* destinations, const int8_t* flying,
+                       const double* weights, const int32_t* groups, int64_t count,
+                       int32_t mem_kind) {
+    if (!h) return set_err(BT_EINVAL, "NULL handle");
+    if (count < 0 || count > h->cap)
+        return set_err(BT_EINVAL, "count %lld outside [0, %lld]", (long long)count,
+                       (long long)h->cap);
+    TRY(ensure_device(h));
+    if (count == 0) return BT_OK;
+    if (!destinations || !flying || !weights) return set_err(BT_EINVAL, "NULL array");
+    if (!h->tr_fly) TRY(dalloc(&h->tr_fly, h->cap));
+    const cudaMemcpyKind kind = mem_kind == BT_MEM_HOST ? cudaMemcpyHostToDevice
+                                                        : cudaMemcpyDeviceToDevice;
+    if (groups && mem_kind == BT_MEM_HOST)
+        for (int64_t i = 0; i < count; ++i)
+            if (groups[i] < 0 || groups[i] >= h->ngroups)
+                return set_err(BT_EINDEX, "group %d out of range [0, %d)", groups[i], h->ngroups);
+    CK(cudaMemcpyAsync(h->dest, destinations, sizeof(double) * 3 * count, kind, h->stream));
+    CK(cudaMemcpyAsync(h->fly, flying, count, kind, h->stream));
+    CK(cudaMemcpyAsync(h->weight, weights, sizeof(double) * count, kind, h->stream));
+    if (groups)
+        CK(cudaMemcpyAsync(h->group, groups, sizeof(int32_t) * count, kind, h->stream));
+    load_step_kernel<<<grid_for(h->cap, 256), 256, 0, h->stream>>>(h->fly, count, h->cap,
+                                                                    h->tr_fly, h->alive);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->stream));
+    h->loaded = count;
+    return BT_OK;
+}
+
+__global__ void unlocalized_kernel(const int8_t* __restrict__ fly, const int32_t* __restrict__ el,
+                                   int64_t n, unsigned long long* __restrict__ first) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n && fly[i] && el[i] < 0) atomicMin(first, (unsigned long long)i);
+}
+
+bt_status bt_trace_begin(bt_tally* h, int32_t score, int64_t max_sweeps) {
+    if (!h) return set_err(BT_EINVAL, "NULL handle");
+    TRY(ensure_device(h));
+    if (!h->tr_fly) return set_err(BT_EINVAL, "no step loaded (bt_load_step)");
+    TRY(ensure_sweep_bufs(h));
+    // _check_localized (search.py:440-446)
+    CK(cudaMemsetAsync(h->dcounters + 15, 0xff, sizeof(unsigned long long), h->stream));
+    unlocalized_kernel<<<grid_for(h->cap, 256), 256, 0, h->stream>>>(h->tr_fly, h->element,
+                                                                      h->cap, h->dcounters + 15);
+    unsigned long long first = 0;
+    CK(cudaMemcpyAsync(&first, h->dcounters + 15, sizeof first, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (first != ~0ull)
+        return set_err(BT_EINVAL,
+                       "flying particle %llu is not localized (element = -1); call "
+                       "initialize_locations first", first);
+    CK(cudaMemsetAsync(h->dcounters, 0, sizeof(unsigned long long) * NDCOUNTERS, h->stream));
+    if (h->opt_digest) {
+        // fresh per-call digests (the recorder view of the test harness)
+        fill_digest_kernel<<<grid_for(h->cap, 256), 256, 0, h->stream>>>(h->digest, h->dcount,
+                                                                         h->cap);
+        CK(cudaGetLastError());
+    }
+    h->tr_score = score != 0;
+    h->tr_sweeps = 0;
+    h->tr_events = 0;
+    h->tr_nev = 0;
+    h->tr_limit = max_sweeps >= 0 ? max_sweeps : 2 * h->ne + 1000;
+    return BT_OK;
+}
+
+bt_status bt_trace_propose(bt_tally* h, bt_sweep_events* ev, int64_t* flying) {
+    if (!h || !ev || !flying) return set_err(BT_EINVAL, "NULL argument");
+    TRY(ensure_device(h));
+    const int64_t n = h->cap;
+    SweepBufs& B = h->sb;
+    // compact flying (ascending), search.py:160-166
+    select_flying_kernel<<<grid_for(n, 256), 256, 0, h->stream>>>(h->tr_fly, n, h->sb_flag);
+    CK(cudaMemsetAsync(h->sb_flag + n, 0, sizeof(int32_t), h->stream));
+    size_t tb = h->sb_tmp_bytes;
+    CK(cub::DeviceScan::ExclusiveSum(h->sb_tmp, tb, h->sb_flag, B.offs, (int)(n + 1), h->stream));
+    scatter_active_kernel<<<grid_for(n, 256), 256, 0, h->stream>>>(h->sb_flag, B.offs, n,
+                                                                    B.active);
+    int32_t m32 = 0;
+    CK(cudaMemcpyAsync(&m32, B.offs + n, sizeof m32, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    const int64_t m = m32;
+    *flying = m;
+    memset(ev, 0, sizeof *ev);
+    h->tr_nev = 0;
+    if (m == 0) return BT_OK;
+    WalkArgs a = walk_args(h, h->dest, h->tr_fly, h->weight, h->tr_score);
+    sweep_propose_kernel<<<grid_for(m, 128), 128, 0, h->stream>>>(a, h->tr_fly, B, m);
+    CK(cudaGetLastError());
+    CK(cudaMemsetAsync(B.has_ev + m, 0, sizeof(int32_t), h->stream));
+    tb = h->sb_tmp_bytes;
+    CK(cub::DeviceScan::ExclusiveSum(h->sb_tmp, tb, B.has_ev, B.offs, (int)(m + 1), h->stream));
+    sweep_compact_kernel<<<grid_for(m, 256), 256, 0, h->stream>>>(B, m);
+    CK(cudaGetLastError());
+    int32_t nev = 0;
+    CK(cudaMemcpyAsync(&nev, B.offs + m, sizeof nev, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    h->tr_nev = nev;
+    ev->count = nev;
+    ev->particle = B.e_particle;
+    ev->element = B.e_elem;
+    ev->exit_face = B.e_face;
+    ev->segment_start = B.e_start;
+    ev->segment_end = B.e_end;
+    ev->segment_length = B.e_len;
+    ev->next_element = B.e_next;
+    ev->particle_done = B.e_done;
+    ev->next_proposed = B.e_next_prop;
+    return BT_OK;
+}
+
+bt_status bt_trace_commit(bt_tally* h) {
+    if (!h) return set_err(BT_EINVAL, "NULL handle");
+    TRY(ensure_device(h));
+    const int64_t nev = h->tr_nev;
+    if (nev > 0) {
+        WalkArgs a = walk_args(h, h->dest, h->tr_fly, h->weight, h->tr_score);
+        a.digest = h->opt_digest ? h->digest : nullptr;
+        a.dcount = h->opt_digest ? h->dcount : nullptr;
+        sweep_commit_kernel<<<grid_for(nev, 256), 256, 0, h->stream>>>(a, h->tr_fly, h->sb, nev);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(h->stream));
+    }
+    h->tr_events += nev;
+    h->tr_sweeps += 1;
+    h->tr_nev = 0;
+    if (h->tr_sweeps > h->tr_limit)
+        return set_err(BT_ERUNTIME, "trace did not terminate within %lld sweeps",
+                       (long long)h->tr_limit);
+    return BT_OK;
+}
+
+bt_status bt_trace_end(bt_tally* h, bt_summary* out) {
+    if (!h || !out) return set_err(BT_EINVAL, "NULL argument");
+    TRY(ensure_device(h));
+    CK(cudaMemcpyAsync(h->hcounters, h->dcounters, sizeof(unsigned long long) * NDCOUNTERS,
+                       cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    const unsigned long long* c = h->hcounters + 1;
+    out->sweeps = h->tr_sweeps;
+    out->events = h->tr_events;
+    out->reached = (int64_t)c[C_REACHED];
+    out->boundary_exits = (int64_t)c[C_BOUNDARY];
+    out->stuck_recoveries = (int64_t)c[C_RECOV];
+    out->stuck_terminations = (int64_t)c[C_KILLED];
+    return BT_OK;
+}
+
+bt_status bt_memcpy(void* dst, const void* src, int64_t bytes, int32_t kind) {
+    if (bytes <= 0) return BT_OK;
+    if (!dst || !src) return set_err(BT_EINVAL, "NULL pointer");
+    CK(cudaMemcpy(dst, src, (size_t)bytes,
+                  kind == 0 ? cudaMemcpyDeviceToHost
+                            : (kind == 1 ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice)));
     return BT_OK;
 }
 

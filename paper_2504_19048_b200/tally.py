@@ -364,6 +364,18 @@ class MeshTally:
     def write(self, filename) -> None:
         write_vtk(self._mesh, self.flux(), filename)
 
+    # ------------------------------------------------------- callback path
+    def load_step(self, destinations, flying, weights, groups=None) -> int:
+        """load_step (particles.py:57-89): load a step for ``trace_batch``."""
+        return _mt_load_step(self, destinations, flying, weights, groups)
+
+    def trace_batch(self, callback=None, *, score: bool = True, max_sweeps: int | None = None,
+                    device_events: bool = False) -> TraceSummary:
+        """trace_batch (search.py:453-489): lockstep sweeps over the loaded step
+        with ``callback(SweepEvents)`` between each proposal and commit."""
+        return _mt_trace_batch(self, callback, score=score, max_sweeps=max_sweeps,
+                               device_events=device_events)
+
     # ------------------------------------------------------------------ extras
     def _check_tensor(self, t, itemsize):
         if not t.is_contiguous():
@@ -454,3 +466,135 @@ class MeshTally:
 
     def __exit__(self, *exc):
         self.close()
+
+
+# ---------------------------------------------------------------------------
+# Listing-1 callback path (search.py:95-147, 453-489)
+
+@dataclass(frozen=True)
+class InterfaceEvent:
+    """One element-interface crossing of one particle (search.py:95-105)."""
+
+    particle: int
+    element: int
+    exit_face: int
+    boundary: bool
+    segment_start: np.ndarray
+    segment_end: np.ndarray
+    segment_length: float
+
+
+class SweepEvents:
+    """Batched view of one sweep's events (search.py:108-147).
+
+    Read-only: particle, element, exit_face, boundary, segment_start,
+    segment_end, segment_length.  Writable decisions: next_element and
+    particle_done.  Host numpy copies by default; with
+    ``trace_batch(..., device_events=True)`` the arrays are zero-copy torch
+    CUDA tensors of the library's event buffers.
+    """
+
+    def __init__(self, arrays: dict, count: int):
+        self.count = count
+        for k, v in arrays.items():
+            setattr(self, k, v)
+
+    @property
+    def boundary(self):
+        return (self.next_proposed < 0) & (self.exit_face >= 0)
+
+    def __len__(self) -> int:
+        return self.count
+
+    def event(self, k: int) -> InterfaceEvent:
+        if not 0 <= k < self.count:
+            raise IndexError(k)
+        return InterfaceEvent(
+            particle=int(self.particle[k]), element=int(self.element[k]),
+            exit_face=int(self.exit_face[k]), boundary=bool(self.boundary[k]),
+            segment_start=np.array(self.segment_start[k].tolist()),
+            segment_end=np.array(self.segment_end[k].tolist()),
+            segment_length=float(self.segment_length[k]))
+
+
+_EV_FIELDS = (("particle", np.int64, 1), ("element", np.int32, 1), ("exit_face", np.int8, 1),
+              ("segment_start", np.float64, 3), ("segment_end", np.float64, 3),
+              ("segment_length", np.float64, 1), ("next_element", np.int32, 1),
+              ("particle_done", np.int8, 1), ("next_proposed", np.int32, 1))
+
+
+def _mt_load_step(self, destinations, flying, weights, groups=None) -> int:
+    """load_step (particles.py:57-89) for the callback path."""
+    fly = np.ascontiguousarray(np.asarray(flying).reshape(-1).astype(np.int8, copy=False))
+    count = fly.size
+    dest = np.ascontiguousarray(np.asarray(destinations, dtype=np.float64).reshape(-1))
+    w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64).reshape(-1))
+    if count > self.capacity:
+        raise ValueError(f"count {count} outside [0, {self.capacity}]")
+    if dest.size != 3 * count or w.size != count:
+        raise ValueError(f"array sizes ({dest.size}, {fly.size}, {w.size}) do not match "
+                         f"count {count} (need 3*count, count, count)")
+    gp = None
+    if groups is not None:
+        g = np.ascontiguousarray(np.asarray(groups, dtype=np.int32).reshape(-1))
+        if g.size != count:
+            raise ValueError("groups size mismatch")
+        gp = g.ctypes.data
+    _lib.check(self._L.bt_load_step(self._h, dest.ctypes.data, fly.ctypes.data, w.ctypes.data,
+                                    gp, count, _lib.BT_MEM_HOST))
+    self._count = max(self._count, count)
+    return count
+
+
+def _mt_trace_batch(self, callback=None, *, score: bool = True, max_sweeps: int | None = None,
+                    device_events: bool = False) -> TraceSummary:
+    """trace_batch (search.py:453-489) on the loaded step: one lockstep sweep
+    at a time, ``callback(SweepEvents)`` between proposal and commit."""
+    L = self._L
+    _lib.check(L.bt_trace_begin(self._h, int(bool(score)),
+                                -1 if max_sweeps is None else int(max_sweeps)))
+    ev = _lib.SweepEventsC()
+    flying = C.c_int64()
+    while True:
+        _lib.check(L.bt_trace_propose(self._h, C.byref(ev), C.byref(flying)))
+        if flying.value == 0:
+            break
+        n = int(ev.count)
+        if callback is not None and n > 0:
+            if device_events:
+                import torch
+                from .distributed import _CudaArray
+                dev = torch.device("cuda", self.device)
+                arrays = {}
+                for name, dt, k in _EV_FIELDS:
+                    t = torch.as_tensor(_CudaArray(getattr(ev, name), n * k,
+                                                   np.dtype(dt).str), device=dev)
+                    arrays[name] = t.view(n, 3) if k == 3 else t
+                view = SweepEvents(arrays, n)
+                callback(view)
+                torch.cuda.current_stream(dev).synchronize()
+            else:
+                arrays = {}
+                for name, dt, k in _EV_FIELDS:
+                    a = np.empty(n * k, dtype=dt)
+                    _lib.check(_copy_d2h(a, getattr(ev, name)))
+                    arrays[name] = a.reshape(n, 3) if k == 3 else a
+                view = SweepEvents(arrays, n)
+                callback(view)
+                _lib.check(_copy_h2d(getattr(ev, "next_element"),
+                                     np.ascontiguousarray(view.next_element, dtype=np.int32)))
+                _lib.check(_copy_h2d(getattr(ev, "particle_done"),
+                                     np.ascontiguousarray(view.particle_done, dtype=np.int8)))
+        _lib.check(L.bt_trace_commit(self._h))
+    s = _lib.Summary()
+    _lib.check(L.bt_trace_end(self._h, C.byref(s)))
+    return TraceSummary._from(s)
+
+
+def _copy_d2h(host: np.ndarray, dptr: int) -> int:
+    return _lib.load().bt_memcpy(host.ctypes.data, dptr, host.nbytes, 0)
+
+
+def _copy_h2d(dptr: int, host: np.ndarray) -> int:
+    return _lib.load().bt_memcpy(dptr, host.ctypes.data, host.nbytes, 1)
+

@@ -56,6 +56,12 @@ def test_transport_statistical_parity(gold, name):
             & (fs["position"] == gold[p + "final_position"]).all(axis=1)
             & (fs["group"] == gold[p + "final_group"]))
     frac = same.mean()
+    for key in ("rng_block", "outcome", "group", "position", "direction", "element", "alive"):
+        a, b = fs[key], gold[p + "final_" + key]
+        eq = (a == b) if a.ndim == 1 else (a == b).all(axis=1)
+        if not eq.all():
+            j = int(np.nonzero(~eq)[0][0])
+            print(f"  {name} {key}: {int((~eq).sum())} differ; first #{j}: {a[j]} vs {b[j]}")
     print(f"{name}: bit-identical histories {frac:.4f}; collisions {r.collisions} vs "
           f"{int(gold[p + 'collisions'])}; leaked {r.leaked_weight} vs "
           f"{float(gold[p + 'leaked_weight'])}")

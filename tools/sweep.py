@@ -90,7 +90,7 @@ def run_point(mesh, positions, sigma_t, moves, label, warm=1, chain=False, **mt_
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--which", default="c3,c4,c5")
+    ap.add_argument("--which", default="c3,c4,c5,tr")
     ap.add_argument("--out", default=None)
     ap.add_argument("--max-particles", type=float, default=1e8)
     args = ap.parse_args()
@@ -137,6 +137,38 @@ def main():
                       chain=True)
         r["mesh_build_s"] = build_s
         res.append(r)
+    if "tr" in which:
+        # paper verification physics: 1 cm cube (n=10), source in
+        # 1/8 of the domain, sigma_t = sigma_s = 100 /cm, vacuum boundary
+        from paper_2504_19048_b200 import transport as T
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import oracle as orc
+        m = build_cube_mesh(10)
+        for n in (10_000, 1_000_000):
+            cfg = T.RunConfig(mesh_n=10, num_particles=n, num_batches=2, seed=42)
+            T.run(T.RunConfig(mesh_n=10, num_particles=min(n, 10000), num_batches=1), m)
+            t = time.time()
+            r = T.run(cfg, m)
+            wall = time.time() - t
+            out = {"point": f"transport paper physics N={n}", "elements": m.num_elements,
+                   "particles": n, "batches": 2, "events": r.events,
+                   "collisions": r.collisions, "t_transport_s": r.t_batch,
+                   "t_localization_s": r.t_localization, "wall_s": wall,
+                   "events_per_s": r.events / r.t_batch,
+                   "collisions_per_s": r.collisions / r.t_batch,
+                   "histories_per_s": 2 * n / r.t_batch}
+            print(json.dumps(out), flush=True)
+            res.append(out)
+        # CPU: the oracle restatement of transport.run (serial, the reference's order)
+        k = 2000
+        t = time.time()
+        o = orc.transport_run(m, [100.0], [[100.0]], k, 1, 42, ((0, 0, 0), (0.5, 0.5, 0.5)))
+        dt = time.time() - t
+        out = {"point": f"transport paper physics CPU oracle (1 thread) N={k}",
+               "events": o["events"], "collisions": o["collisions"], "wall_s": dt,
+               "events_per_s": o["events"] / dt, "collisions_per_s": o["collisions"] / dt}
+        print(json.dumps(out), flush=True)
+        res.append(out)
     if args.out:
         Path(args.out).write_text("\n".join(json.dumps(r) for r in res) + "\n")
 
