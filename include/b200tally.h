@@ -214,6 +214,12 @@ bt_status bt_trace_propose(bt_tally *h, bt_sweep_events *events, int64_t *flying
 bt_status bt_trace_commit(bt_tally *h);
 bt_status bt_trace_end(bt_tally *h, bt_summary *summary);
 
+/* Flux of the track-length (estimator 0) or collision (1) tally on the
+ * device (flux, tally.py:123-152): mean (E,G) = (sum/n)/volume, rel_error =
+ * sqrt(var/n)/batch_mean (0 where the mean is 0 or n < 2). */
+bt_status bt_flux(bt_tally *h, int32_t estimator, const double *volumes, double *mean,
+                  double *rel_error);
+
 /* cudaMemcpy for bindings without a CUDA runtime: kind 0 device->host,
  * 1 host->device, 2 device->device. */
 bt_status bt_memcpy(void *dst, const void *src, int64_t bytes, int32_t kind);

@@ -31,7 +31,7 @@ EXPORTS = (
     "bt_last_timing", "bt_particle_device_ptrs", "bt_save_state", "bt_restore_state",
     "bt_info", "bt_build_adjacency", "bt_transport_run", "bt_read_transport_state",
     "bt_uniform_blocks", "bt_load_step", "bt_trace_begin", "bt_trace_propose",
-    "bt_trace_commit", "bt_trace_end", "bt_memcpy",
+    "bt_trace_commit", "bt_trace_end", "bt_memcpy", "bt_flux",
     "bt_last_error", "bt_version",
 )
 
@@ -91,6 +91,7 @@ _SIGS = {
     "bt_trace_commit": [_P],
     "bt_trace_end": [_P, C.POINTER(Summary)],
     "bt_memcpy": [_P, _P, _I64, _I32],
+    "bt_flux": [_P, _I32, _P, _P, _P],
     "bt_last_error": [],
     "bt_version": [],
 }

@@ -316,7 +316,7 @@ __device__ __forceinline__ void begin(Lane& L) {
     L.iters = 0;
     L.dig = DIGEST_INIT;
     L.dcnt = 0;
-    L.alive = 1;          // load_step: alive |= flying
+    L.alive = 1;          // overwritten by the fetch with alive | flying (load_step)
     L.outcome = OUT_NONE;
 }
 
@@ -409,6 +409,7 @@ __global__ void __launch_bounds__(THREADS, MINB) walk_kernel(const WalkArgs a) {
                             L.w = a.score ? a.weight[i] : 0.0;
                             L.g = a.score ? a.group[i] : 0;
                             begin(L);
+                            L.alive = (int8_t)(a.alive[i] | a.fly_in[i]);
                         }
                     }
                 }
@@ -539,6 +540,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
                     L.entry = (int)(signed char)(fl & 0xff);
                     L.st = (fl >> 8) & 0xff;
                     begin(L);
+                    L.alive = (int)(signed char)((fl >> 16) & 0xff);
                 }
             }
             head += take;
@@ -606,7 +608,8 @@ __global__ void stage_kernel(const WalkArgs a, const WorkSoA W, int64_t* __restr
     W.seg[k] = a.seg_total[i];
     W.e[k] = a.element[i];
     W.g[k] = a.score ? a.group[i] : 0;
-    W.fl[k] = ((int)(unsigned char)a.entry[i]) | ((int)(unsigned char)a.stuck[i] << 8);
+    W.fl[k] = ((int)(unsigned char)a.entry[i]) | ((int)(unsigned char)a.stuck[i] << 8) |
+              ((int)(unsigned char)(a.alive[i] | a.fly_in[i]) << 16);  // load_step: alive |= flying
 }
 
 // ---------------------------------------------------------------------------
@@ -1122,6 +1125,26 @@ __global__ void fill_digest_kernel(uint64_t* __restrict__ d, int64_t* __restrict
         d[i] = DIGEST_INIT;
         c[i] = 0;
     }
+}
+
+// flux (tally.py:123-152) on the device: mean = (sum/n)/V, rel = sqrt(var/n)/mean
+__global__ void flux_kernel(const double* __restrict__ sum, const double* __restrict__ sum_sq,
+                            const double* __restrict__ vol, int64_t ne, int32_t ng, int64_t n,
+                            double* __restrict__ mean, double* __restrict__ rel) {
+    const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= ne * ng) return;
+    const double s = sum[b], sq = sum_sq[b];
+    const double dn = (double)n;
+    const double bm = __ddiv_rn(s, dn);
+    mean[b] = __ddiv_rn(bm, vol[b / ng]);
+    double r = 0.0;
+    if (n >= 2) {
+        double var = __ddiv_rn(__dsub_rn(sq, __ddiv_rn(__dmul_rn(s, s), dn)), (double)(n - 1));
+        if (var < 0.0) var = 0.0;
+        const double se = __dsqrt_rn(__ddiv_rn(var, dn));
+        if (bm > 0.0) r = __ddiv_rn(se, bm);
+    }
+    rel[b] = r;
 }
 
 // ---------------------------------------------------------------------------
@@ -2930,6 +2953,42 @@ bt_status bt_memcpy(void* dst, const void* src, int64_t bytes, int32_t kind) {
     CK(cudaMemcpy(dst, src, (size_t)bytes,
                   kind == 0 ? cudaMemcpyDeviceToHost
                             : (kind == 1 ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice)));
+    return BT_OK;
+}
+
+bt_status bt_flux(bt_tally* h, int32_t estimator, const double* volumes, double* mean,
+                  double* rel_error) {
+    if (!h || !volumes || !mean || !rel_error) return set_err(BT_EINVAL, "NULL argument");
+    const double* sm = estimator == 0 ? h->sum : h->col_sum;
+    const double* sq = estimator == 0 ? h->sum_sq : h->col_sum_sq;
+    const int64_t n = estimator == 0 ? h->batches : h->col_batches;
+    if (!sm) return set_err(BT_EINVAL, "no collision estimator on this handle");
+    if (n == 0) return set_err(BT_ERUNTIME, "no batches completed; nothing to normalize");
+    for (int64_t e = 0; e < h->ne; ++e)
+        if (!(volumes[e] > 0.0)) return set_err(BT_EINVAL, "volumes must be positive");
+    TRY(ensure_device(h));
+    const int64_t nb = h->ne * h->ngroups;
+    double *dv = nullptr, *dm = nullptr, *dr = nullptr;
+    TRY(dalloc(&dv, h->ne));
+    TRY(dalloc(&dm, nb));
+    TRY(dalloc(&dr, nb));
+    cudaError_t err = cudaMemcpyAsync(dv, volumes, sizeof(double) * h->ne, cudaMemcpyHostToDevice,
+                                      h->stream);
+    if (err == cudaSuccess) {
+        flux_kernel<<<grid_for(nb, 256), 256, 0, h->stream>>>(sm, sq, dv, h->ne, h->ngroups, n, dm,
+                                                              dr);
+        err = cudaGetLastError();
+    }
+    if (err == cudaSuccess)
+        err = cudaMemcpyAsync(mean, dm, sizeof(double) * nb, cudaMemcpyDeviceToHost, h->stream);
+    if (err == cudaSuccess)
+        err = cudaMemcpyAsync(rel_error, dr, sizeof(double) * nb, cudaMemcpyDeviceToHost,
+                              h->stream);
+    if (err == cudaSuccess) err = cudaStreamSynchronize(h->stream);
+    cudaFree(dv);
+    cudaFree(dm);
+    cudaFree(dr);
+    if (err != cudaSuccess) return set_err(BT_ECUDA, "bt_flux: %s", cudaGetErrorString(err));
     return BT_OK;
 }
 

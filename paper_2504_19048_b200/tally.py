@@ -361,6 +361,16 @@ class MeshTally:
     def flux(self) -> FluxResult:
         return flux(self._grid, self._mesh.volumes)
 
+    def flux_device(self, estimator: str = "track") -> FluxResult:
+        """flux() evaluated on the GPU (bt_flux); estimator 'track' or 'collision'."""
+        ne, ng = self._mesh.num_elements, self.num_groups
+        vol = np.ascontiguousarray(self._mesh.volumes, dtype=np.float64)
+        mean = np.empty((ne, ng))
+        rel = np.empty((ne, ng))
+        _lib.check(self._L.bt_flux(self._h, 0 if estimator == "track" else 1, vol.ctypes.data,
+                                   mean.ctypes.data, rel.ctypes.data))
+        return FluxResult(mean=mean, rel_error=rel)
+
     def write(self, filename) -> None:
         write_vtk(self._mesh, self.flux(), filename)
 

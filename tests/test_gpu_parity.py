@@ -70,6 +70,9 @@ def _check_case(case, localize, **kw):
     assert rel_close(mt.grid.sum_sq, case.batches[-1].sum_sq, TALLY_RTOL)[0]
     fl = mt.flux()
     assert rel_close(fl.mean, case.flux_mean, TALLY_RTOL)[0]
+    fd = mt.flux_device()
+    assert rel_close(fd.mean, fl.mean, 1e-15)[0]
+    assert np.abs(fd.rel_error - fl.rel_error).max() < 1e-12
     # rel_error cancels catastrophically between near-equal batches; see
     # tests/test_oracle_golden.py
     assert np.abs(fl.rel_error - case.flux_rel).max() < 1e-5
