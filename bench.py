@@ -96,32 +96,45 @@ def config(args, world, ne):
 # clocks sampling during the timed region
 
 class Clocks:
+    """nvidia-smi in loop mode (-lms 50) for the duration of the timed region."""
+
     def __init__(self, dev):
         self.dev = dev
         self.samples = []
-        self._stop = threading.Event()
+        self._p = None
         self._t = None
 
     def __enter__(self):
-        def run():
-            cmd = ["nvidia-smi", "-i", str(self.dev),
-                   "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-                   "--format=csv,noheader,nounits"]
-            while not self._stop.is_set():
+        cmd = ["nvidia-smi", "-i", str(self.dev), "-lms", "50",
+               "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+               "--format=csv,noheader,nounits"]
+        try:
+            self._p = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                       text=True)
+        except OSError:
+            self._p = None
+            return self
+
+        def read():
+            for line in self._p.stdout:
                 try:
-                    out = subprocess.run(cmd, capture_output=True, text=True, timeout=5).stdout
-                    a = [x.strip() for x in out.strip().split(",")]
+                    a = [x.strip() for x in line.strip().split(",")]
                     self.samples.append((float(a[0]), float(a[1]), int(a[2], 16)))
-                except Exception:
+                except (ValueError, IndexError):
                     pass
-                self._stop.wait(0.2)
-        self._t = threading.Thread(target=run, daemon=True)
+        self._t = threading.Thread(target=read, daemon=True)
         self._t.start()
+        time.sleep(0.3)  # let the first samples arrive before the region starts
         return self
 
     def __exit__(self, *exc):
-        self._stop.set()
-        self._t.join(timeout=6)
+        if self._p is not None:
+            self._p.terminate()
+            try:
+                self._p.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self._p.kill()
+            self._t.join(timeout=5)
 
     def summary(self):
         if not self.samples:
@@ -130,13 +143,14 @@ class Clocks:
                  0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
                  0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
                  0x100: "display_clock_setting"}
+        busy = [s for s in self.samples if not s[2] & 0x1] or self.samples
         bits = 0
-        for _, _, b in self.samples:
+        for _, _, b in busy:
             bits |= b
-        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+        return {"sm_mhz": statistics.median(s[0] for s in busy),
                 "sm_max_mhz": max(s[1] for s in self.samples),
                 "reasons": [v for k, v in names.items() if bits & k and k != 0x1],
-                "samples": len(self.samples)}
+                "samples": len(self.samples), "samples_under_load": len(busy)}
 
 
 # ---------------------------------------------------------------------------

@@ -147,25 +147,53 @@ struct Lane {
     int64_t idx;  // -1: lane idle
     int e, g, entry, st, iters;
     int outcome, alive;
-    uint64_t dig;
-    int dcnt;
 };
 
+// this thread's digest slot in shared memory (digest mode only; keeps the
+// sequence hash out of the hot loop's registers)
+struct DigestSlot {
+    uint64_t* d;
+    int* c;
+};
+
+// Per-lane event count in a register; the rarer counters live in a
+// CTA-shared array (fewer live registers in the hot loop), flushed once.
+enum { SC_REACHED = 0, SC_BOUNDARY, SC_RECOV, SC_KILLED, SC_MAXIT, SC_ERR, SC_N };
 struct Counters {
-    unsigned events = 0, reached = 0, boundary = 0, recov = 0, killed = 0;
-    int max_iters = 0;
-    int err = 0;
+    unsigned events = 0;
+    unsigned* sh = nullptr;  // SC_N shared counters of the CTA
+};
+
+// Deferred track-length score of the previous step: its square root and
+// atomic are issued after the next step's loads, off the critical path.
+struct Pending {
+    bool has = false;
+    int64_t bin = 0;
+    double val = 0.0;
+    double seg = 0.0;
+    bool seg_pending = false;
 };
 
 // One step of search.py:183-274 for a flying lane.  Returns true when the
-// particle stops (reached, leaked, stuck-killed or sweep guard); sets
-// has_score/bin/val when the step scores a segment.
-__device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& C,
-                                          bool& has_score, int64_t& bin, double& val) {
+// particle stops (reached, leaked, stuck-killed or sweep guard).  When DEFER
+// the segment is left in P (scored by the next step or the loop); otherwise
+// has_score/bin/val are set for an immediate score.
+__device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& C, Pending& P,
+                                          const DigestSlot& DS) {
     const ElemRec r = L.have_nr ? L.nr : load_rec(a.rec, L.e);
     L.have_nr = false;
     Tet T;
     load_tet(a, r, T);
+    // the previous step's score and seg_total update, while this step's
+    // vertex loads are in flight (warp-aggregated mode scores at loop level)
+    if (!a.wagg && P.has) {
+        atomicAdd(a.tally + P.bin, P.val);
+        P.has = false;
+    }
+    if (P.seg_pending) {
+        L.seg = __dadd_rn(L.seg, P.seg);
+        P.seg_pending = false;
+    }
     double ox = L.px, oy = L.py, oz = L.pz;
     if (L.st == 1) {  // search.py:190-196
         const double sx = __dsub_rn(L.dx, L.px), sy = __dsub_rn(L.dy, L.py),
@@ -199,10 +227,10 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
     if (kind == 2) {  // stuck ladder, search.py:199-235
         if (contains(T, L.dx, L.dy, L.dz, STUCK_TOL)) {
             kind = 0;
-            ++C.recov;
+            atomicAdd(C.sh + SC_RECOV, 1u);
         } else if (L.st == 0) {
             L.st = 1;
-            ++C.recov;
+            atomicAdd(C.sh + SC_RECOV, 1u);
             event = false;
         } else if (L.st == 1) {
             int hop = -1;
@@ -222,17 +250,17 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
                 L.e = hop;
                 L.entry = -1;
                 L.st = 2;
-                ++C.recov;
+                atomicAdd(C.sh + SC_RECOV, 1u);
             } else {
                 L.outcome = OUT_STUCK_KILLED;
                 L.alive = 0;
-                ++C.killed;
+                atomicAdd(C.sh + SC_KILLED, 1u);
                 done = true;
             }
         } else {
             L.outcome = OUT_STUCK_KILLED;
             L.alive = 0;
-            ++C.killed;
+            atomicAdd(C.sh + SC_KILLED, 1u);
             event = false;
             done = true;
         }
@@ -241,8 +269,8 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
         ++C.events;
         L.st = 0;
         if (a.digest) {
-            L.dig = (L.dig ^ (uint64_t)((int64_t)L.e * 8 + face + 1)) * DIGEST_PRIME;
-            ++L.dcnt;
+            *DS.d = (*DS.d ^ (uint64_t)((int64_t)L.e * 8 + face + 1)) * DIGEST_PRIME;
+            ++*DS.c;
         }
         double qx, qy, qz;
         if (kind == 0) {
@@ -257,26 +285,25 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
         const double ax = __dsub_rn(qx, L.px), ay = __dsub_rn(qy, L.py), az = __dsub_rn(qz, L.pz);
         const double seg = __dsqrt_rn(
             __dadd_rn(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)), __dmul_rn(az, az)));
-        if (a.score) {
-            has_score = true;
-            bin = (int64_t)L.e * a.ngroups + L.g;
-            val = __dmul_rn(L.w, seg);
-        }
-        L.seg = __dadd_rn(L.seg, seg);
+        P.has = a.score != 0;
+        P.bin = (int64_t)L.e * a.ngroups + L.g;
+        P.val = __dmul_rn(L.w, seg);
+        P.seg = seg;
+        P.seg_pending = true;
         L.px = qx;
         L.py = qy;
         L.pz = qz;
         if (kind == 0) {
             L.entry = -1;
             L.outcome = OUT_REACHED;
-            ++C.reached;
+            atomicAdd(C.sh + SC_REACHED, 1u);
             done = true;
         } else {
             const int nbp = face == 0 ? r.nb[0] : face == 1 ? r.nb[1] : face == 2 ? r.nb[2] : r.nb[3];
             if (nbp < 0) {
                 L.outcome = OUT_LEAKED;
                 L.alive = 0;
-                ++C.boundary;
+                atomicAdd(C.sh + SC_BOUNDARY, 1u);
                 done = true;
             } else {
                 L.e = nbp >> 2;
@@ -286,13 +313,18 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
     }
     ++L.iters;
     if (!done && L.iters > a.max_sweeps) {  // sweep guard, search.py:513-516
-        C.err = 1;
+        atomicOr(C.sh + SC_ERR, 1u);
         done = true;
+    }
+    if (done && P.seg_pending) {  // the final seg_total is written now
+        L.seg = __dadd_rn(L.seg, P.seg);
+        P.seg_pending = false;
     }
     return done;
 }
 
-__device__ __forceinline__ void finish(const WalkArgs& a, Lane& L, Counters& C) {
+__device__ __forceinline__ void finish(const WalkArgs& a, Lane& L, Counters& C,
+                                       const DigestSlot& DS) {
     const int64_t i = L.idx;
     a.pos[3 * i] = L.px;
     a.pos[3 * i + 1] = L.py;
@@ -304,18 +336,20 @@ __device__ __forceinline__ void finish(const WalkArgs& a, Lane& L, Counters& C) 
     a.alive[i] = (int8_t)L.alive;
     a.seg_total[i] = L.seg;
     if (a.digest) {
-        a.digest[i] = L.dig;
-        a.dcount[i] = L.dcnt;
+        a.digest[i] = *DS.d;
+        a.dcount[i] = *DS.c;
     }
-    C.max_iters = max(C.max_iters, L.iters);
+    atomicMax(C.sh + SC_MAXIT, (unsigned)L.iters);
     L.idx = -1;
 }
 
-__device__ __forceinline__ void begin(Lane& L) {
+__device__ __forceinline__ void begin(Lane& L, const WalkArgs& a, const DigestSlot& DS) {
     L.have_nr = false;
     L.iters = 0;
-    L.dig = DIGEST_INIT;
-    L.dcnt = 0;
+    if (a.digest) {
+        *DS.d = DIGEST_INIT;
+        *DS.c = 0;
+    }
     L.alive = 1;          // overwritten by the fetch with alive | flying (load_step)
     L.outcome = OUT_NONE;
 }
@@ -345,23 +379,37 @@ __device__ __forceinline__ void score(const WalkArgs& a, bool has_score, int64_t
     }
 }
 
+// loop level, all lanes: warp-aggregated score of the pending segments, or the
+// plain atomic of lanes that went idle with one pending
+__device__ __forceinline__ void flush_pending(const WalkArgs& a, Pending& P, bool idle) {
+    if (a.wagg) {
+        score(a, P.has, P.bin, P.val);
+        P.has = false;
+    } else if (idle && P.has) {
+        atomicAdd(a.tally + P.bin, P.val);
+        P.has = false;
+    }
+}
+
+__device__ __forceinline__ void counters_init(unsigned* sh) {
+    if (threadIdx.x < SC_N) sh[threadIdx.x] = 0;
+    __syncthreads();
+}
+
+// all threads of the CTA: warp-reduce events, then one atomic per counter per CTA
 __device__ __forceinline__ void flush_counters(const WalkArgs& a, Counters& C) {
     constexpr unsigned FULL = 0xffffffffu;
     const unsigned ev = __reduce_add_sync(FULL, C.events);
-    const unsigned re = __reduce_add_sync(FULL, C.reached);
-    const unsigned bd = __reduce_add_sync(FULL, C.boundary);
-    const unsigned rv = __reduce_add_sync(FULL, C.recov);
-    const unsigned kl = __reduce_add_sync(FULL, C.killed);
-    const int mi = __reduce_max_sync(FULL, C.max_iters);
-    const int er = __reduce_or_sync(FULL, C.err);
-    if ((threadIdx.x & 31) == 0) {
-        if (ev) atomicAdd(a.counters + C_EVENTS, (unsigned long long)ev);
-        if (re) atomicAdd(a.counters + C_REACHED, (unsigned long long)re);
-        if (bd) atomicAdd(a.counters + C_BOUNDARY, (unsigned long long)bd);
-        if (rv) atomicAdd(a.counters + C_RECOV, (unsigned long long)rv);
-        if (kl) atomicAdd(a.counters + C_KILLED, (unsigned long long)kl);
-        if (mi) atomicMax(a.counters + C_SWEEPS, (unsigned long long)mi);
-        if (er) atomicOr(a.counters + C_ERR, 1ull);
+    if ((threadIdx.x & 31) == 0 && ev) atomicAdd(a.counters + C_EVENTS, (unsigned long long)ev);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned* sh = C.sh;
+        if (sh[SC_REACHED]) atomicAdd(a.counters + C_REACHED, (unsigned long long)sh[SC_REACHED]);
+        if (sh[SC_BOUNDARY]) atomicAdd(a.counters + C_BOUNDARY, (unsigned long long)sh[SC_BOUNDARY]);
+        if (sh[SC_RECOV]) atomicAdd(a.counters + C_RECOV, (unsigned long long)sh[SC_RECOV]);
+        if (sh[SC_KILLED]) atomicAdd(a.counters + C_KILLED, (unsigned long long)sh[SC_KILLED]);
+        if (sh[SC_MAXIT]) atomicMax(a.counters + C_SWEEPS, (unsigned long long)sh[SC_MAXIT]);
+        if (sh[SC_ERR]) atomicOr(a.counters + C_ERR, 1ull);
     }
 }
 
@@ -371,9 +419,16 @@ template <int THREADS, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB) walk_kernel(const WalkArgs a) {
     constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
+    __shared__ unsigned shc[SC_N];
+    __shared__ uint64_t sdig[THREADS];
+    __shared__ int scnt[THREADS];
+    counters_init(shc);
+    const DigestSlot DS{sdig + threadIdx.x, scnt + threadIdx.x};
     Lane L;
     L.idx = -1;
     Counters C;
+    C.sh = shc;
+    Pending P;
     bool drained = false;
     while (true) {
         if (!drained) {
@@ -408,7 +463,7 @@ __global__ void __launch_bounds__(THREADS, MINB) walk_kernel(const WalkArgs a) {
                             L.seg = a.seg_total[i];
                             L.w = a.score ? a.weight[i] : 0.0;
                             L.g = a.score ? a.group[i] : 0;
-                            begin(L);
+                            begin(L, a, DS);
                             L.alive = (int8_t)(a.alive[i] | a.fly_in[i]);
                         }
                     }
@@ -416,16 +471,14 @@ __global__ void __launch_bounds__(THREADS, MINB) walk_kernel(const WalkArgs a) {
             }
         }
         if (!__any_sync(FULL, L.idx >= 0)) {
+            flush_pending(a, P, true);
             if (drained) break;
             continue;
         }
-        bool has_score = false;
-        int64_t bin = 0;
-        double val = 0.0;
         if (L.idx >= 0) {
-            if (walk_step(a, L, C, has_score, bin, val)) finish(a, L, C);
+            if (walk_step(a, L, C, P, DS)) finish(a, L, C, DS);
         }
-        score(a, has_score, bin, val);
+        flush_pending(a, P, L.idx < 0);
     }
     flush_counters(a, C);
 }
@@ -493,11 +546,18 @@ __global__ void __launch_bounds__(THREADS, MINB)
     walk_staged_kernel(const WalkArgs a, const WorkSoA W, const int64_t* __restrict__ nwork_p) {
     constexpr unsigned FULL = 0xffffffffu;
     __shared__ WarpStage stages[THREADS / 32][2];
+    __shared__ unsigned shc[SC_N];
+    __shared__ uint64_t sdig[THREADS];
+    __shared__ int scnt[THREADS];
+    counters_init(shc);
+    const DigestSlot DS{sdig + threadIdx.x, scnt + threadIdx.x};
     const int wid = threadIdx.x >> 5;
     const int64_t nwork = *nwork_p;
     Lane L;
     L.idx = -1;
     Counters C;
+    C.sh = shc;
+    Pending P;
     int cur = 0;
     int head = 0;
     int ncur = claim_chunk(a, W, stages[wid][0], nwork);
@@ -539,21 +599,21 @@ __global__ void __launch_bounds__(THREADS, MINB)
                     const int fl = s.fl[j];
                     L.entry = (int)(signed char)(fl & 0xff);
                     L.st = (fl >> 8) & 0xff;
-                    begin(L);
+                    begin(L, a, DS);
                     L.alive = (int)(signed char)((fl >> 16) & 0xff);
                 }
             }
             head += take;
             idle = __ballot_sync(FULL, L.idx < 0);
         }
-        if (!__any_sync(FULL, L.idx >= 0)) break;  // no work left anywhere for this warp
-        bool has_score = false;
-        int64_t bin = 0;
-        double val = 0.0;
-        if (L.idx >= 0) {
-            if (walk_step(a, L, C, has_score, bin, val)) finish(a, L, C);
+        if (!__any_sync(FULL, L.idx >= 0)) {  // no work left anywhere for this warp
+            flush_pending(a, P, true);
+            break;
         }
-        score(a, has_score, bin, val);
+        if (L.idx >= 0) {
+            if (walk_step(a, L, C, P, DS)) finish(a, L, C, DS);
+        }
+        flush_pending(a, P, L.idx < 0);
     }
     cp_async_wait_all();
     flush_counters(a, C);
@@ -728,9 +788,14 @@ __global__ void __launch_bounds__(THREADS, 1) transport_kernel(const TransportAr
     constexpr unsigned FULL = 0xffffffffu;
     const WalkArgs& a = t.w;
     const int lane = threadIdx.x & 31;
+    __shared__ unsigned shc[SC_N];
+    counters_init(shc);
+    const DigestSlot DS{nullptr, nullptr};
     Lane L;
     L.idx = -1;
     Counters C;
+    C.sh = shc;
+    Pending P;
     double ux = 0, uy = 0, uz = 0;  // direction
     uint32_t rb = 0;
     int rounds = 0;
@@ -772,12 +837,10 @@ __global__ void __launch_bounds__(THREADS, 1) transport_kernel(const TransportAr
             }
         }
         if (!__any_sync(FULL, L.idx >= 0)) {
+            flush_pending(a, P, true);
             if (drained) break;
             continue;
         }
-        bool has_score = false;
-        int64_t bin = 0;
-        double val = 0.0;
         if (L.idx >= 0) {
             if (need_flight) {  // _flight (transport.py:213-226)
                 double u[4];
@@ -794,7 +857,7 @@ __global__ void __launch_bounds__(THREADS, 1) transport_kernel(const TransportAr
                 ++rounds;
                 need_flight = false;
             }
-            if (walk_step(a, L, C, has_score, bin, val)) {
+            if (walk_step(a, L, C, P, DS)) {
                 // flight over: its walk took L.iters sweeps in round `rounds`
                 if (rounds <= MAX_ROUNDS_TRACKED) atomicMax(t.round_max + rounds - 1, (unsigned)L.iters);
                 bool stop = true;
@@ -817,7 +880,7 @@ __global__ void __launch_bounds__(THREADS, 1) transport_kernel(const TransportAr
                         stop = false;
                         need_flight = true;
                         if (rounds >= t.max_rounds) {  // _MAX_ROUNDS guard (transport.py:531-533)
-                            C.err = 1;
+                            atomicOr(C.sh + SC_ERR, 1u);
                             stop = true;
                         }
                     } else {
@@ -850,7 +913,7 @@ __global__ void __launch_bounds__(THREADS, 1) transport_kernel(const TransportAr
                 }
             }
         }
-        score(a, has_score, bin, val);
+        flush_pending(a, P, L.idx < 0);
     }
     // reduce the per-lane totals (tally sums are order-free up to rounding)
     for (int o = 16; o > 0; o >>= 1) {

@@ -33,7 +33,9 @@ Documented deviations from the reference:
 
 from __future__ import annotations
 
+import atexit
 import ctypes as C
+import weakref
 from dataclasses import dataclass
 from pathlib import Path
 
@@ -202,6 +204,16 @@ def write_flux_csv(flux_result: FluxResult, filename) -> None:
                 fh.write(f"{e},{g},{_fmt(mean[e, g])},{_fmt(rel[e, g])}\n")
 
 
+_LIVE = weakref.WeakSet()
+
+
+@atexit.register
+def _close_all() -> None:
+    """Release device memory of handles still alive at interpreter exit."""
+    for mt in list(_LIVE):
+        mt.close()
+
+
 class MeshTally:
     """Batched track-length tally on a tet mesh, computed on one B200."""
 
@@ -241,6 +253,7 @@ class MeshTally:
                                self.capacity, self.num_groups, self.device, C.byref(h)))
         self._h = h
         self._L = L
+        _LIVE.add(self)
         self.set_option(_lib.BT_OPT_DIGEST, int(digest))
         self.set_option(_lib.BT_OPT_SORT, int(sort))
         self.set_option(_lib.BT_OPT_WARP_AGG, int(warp_aggregate))
