@@ -96,15 +96,45 @@ def config(args, world, ne):
 # clocks sampling during the timed region
 
 class Clocks:
-    """nvidia-smi in loop mode (-lms 50) for the duration of the timed region."""
+    """SM clock and clock-event reasons sampled every 10 ms by NVML (a
+    background thread) for the duration of the timed region; nvidia-smi in
+    loop mode if NVML is unavailable."""
+
+    NAMES = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+             0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+             0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+             0x100: "display_clock_setting"}
 
     def __init__(self, dev):
         self.dev = dev
         self.samples = []
-        self._p = None
+        self.max_mhz = None
+        self._stop = threading.Event()
         self._t = None
+        self._p = None
+
+    def _nvml_loop(self, nv, h):
+        while not self._stop.is_set():
+            try:
+                self.samples.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                                     int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))))
+            except Exception:
+                pass
+            self._stop.wait(0.01)
 
     def __enter__(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.dev]) if vis else self.dev
+            h = nv.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self._t = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
+            self._t.start()
+            return self
+        except Exception:
+            pass
         cmd = ["nvidia-smi", "-i", str(self.dev), "-lms", "50",
                "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
                "--format=csv,noheader,nounits"]
@@ -112,44 +142,44 @@ class Clocks:
             self._p = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
                                        text=True)
         except OSError:
-            self._p = None
             return self
 
         def read():
             for line in self._p.stdout:
                 try:
                     a = [x.strip() for x in line.strip().split(",")]
-                    self.samples.append((float(a[0]), float(a[1]), int(a[2], 16)))
+                    self.max_mhz = float(a[1])
+                    self.samples.append((float(a[0]), int(a[2], 16)))
                 except (ValueError, IndexError):
                     pass
         self._t = threading.Thread(target=read, daemon=True)
         self._t.start()
-        time.sleep(0.3)  # let the first samples arrive before the region starts
+        t0 = time.time()
+        while not self.samples and time.time() - t0 < 5.0:  # first sample before the region
+            time.sleep(0.01)
         return self
 
     def __exit__(self, *exc):
+        self._stop.set()
         if self._p is not None:
             self._p.terminate()
             try:
                 self._p.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self._p.kill()
+        if self._t is not None:
             self._t.join(timeout=5)
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        names = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
-                 0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
-                 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
-                 0x100: "display_clock_setting"}
-        busy = [s for s in self.samples if not s[2] & 0x1] or self.samples
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        busy = [s for s in self.samples if not s[1] & 0x1] or self.samples
         bits = 0
-        for _, _, b in busy:
+        for _, b in busy:
             bits |= b
         return {"sm_mhz": statistics.median(s[0] for s in busy),
-                "sm_max_mhz": max(s[1] for s in self.samples),
-                "reasons": [v for k, v in names.items() if bits & k and k != 0x1],
+                "sm_max_mhz": self.max_mhz,
+                "reasons": [v for k, v in self.NAMES.items() if bits & k and k != 0x1],
                 "samples": len(self.samples), "samples_under_load": len(busy)}
 
 

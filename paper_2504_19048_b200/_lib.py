@@ -9,10 +9,13 @@ search.py:513-516, tally.py:275-277).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libb200tally.so"
+# BT_LIB_PATH: an alternative build of the same library (tools/build_variant.sh
+# experiments); there is no non-native path either way
+LIB_PATH = Path(os.environ.get("BT_LIB_PATH") or PKG / "libb200tally.so")
 
 BT_OK, BT_EINVAL, BT_ERUNTIME, BT_ECUDA, BT_EINDEX, BT_ENOMEM = range(6)
 BT_MEM_HOST, BT_MEM_DEVICE = 0, 1

@@ -137,16 +137,39 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // ---------------------------------------------------------------------------
 // walk kernels: the fused sweep (search.py:169-275) run to completion per lane
 
-constexpr int DEFAULT_VARIANT = 1;  // see run_walk's variant table
+constexpr int DEFAULT_VARIANT = 6;  // see run_walk's variant table
 
-// one particle's walk state, held in registers while it flies
+// Cold per-lane state (read at events and at the end of a walk) lives in
+// shared memory, one slot per thread: fewer live registers in the hot loop.
+constexpr int MAX_CTA_THREADS = 256;
+__shared__ double s_lane_w[MAX_CTA_THREADS];
+__shared__ double s_lane_seg[MAX_CTA_THREADS];
+__shared__ int64_t s_lane_idx[MAX_CTA_THREADS];
+__shared__ int s_lane_g[MAX_CTA_THREADS];
+__shared__ double s_lane_d[3][MAX_CTA_THREADS];  // destination
+__shared__ int8_t s_lane_outcome[MAX_CTA_THREADS];
+__shared__ int8_t s_lane_alive[MAX_CTA_THREADS];
+
+// one particle's walk state while it flies
 struct Lane {
     ElemRec nr;   // prefetched record of the element entered next
     bool have_nr;
-    double px, py, pz, dx, dy, dz, w, seg;
-    int64_t idx;  // -1: lane idle
-    int e, g, entry, st, iters;
-    int outcome, alive;
+    bool busy;    // false: lane idle
+    double px, py, pz;
+    int e, entry, st, iters;
+    __device__ __forceinline__ double& w() { return s_lane_w[threadIdx.x]; }
+    __device__ __forceinline__ double& seg() { return s_lane_seg[threadIdx.x]; }
+    __device__ __forceinline__ int64_t& idx() { return s_lane_idx[threadIdx.x]; }
+    __device__ __forceinline__ int& g() { return s_lane_g[threadIdx.x]; }
+    __device__ __forceinline__ int8_t& outcome() { return s_lane_outcome[threadIdx.x]; }
+    __device__ __forceinline__ int8_t& alive() { return s_lane_alive[threadIdx.x]; }
+    __device__ __forceinline__ double& dx() { return s_lane_d[0][threadIdx.x]; }
+    __device__ __forceinline__ double& dy() { return s_lane_d[1][threadIdx.x]; }
+    __device__ __forceinline__ double& dz() { return s_lane_d[2][threadIdx.x]; }
+    __device__ __forceinline__ void set_idx(int64_t i) {
+        idx() = i;
+        busy = true;
+    }
 };
 
 // this thread's digest slot in shared memory (digest mode only; keeps the
@@ -191,13 +214,13 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
         P.has = false;
     }
     if (P.seg_pending) {
-        L.seg = __dadd_rn(L.seg, P.seg);
+        L.seg() = __dadd_rn(L.seg(), P.seg);
         P.seg_pending = false;
     }
     double ox = L.px, oy = L.py, oz = L.pz;
     if (L.st == 1) {  // search.py:190-196
-        const double sx = __dsub_rn(L.dx, L.px), sy = __dsub_rn(L.dy, L.py),
-                     sz = __dsub_rn(L.dz, L.pz);
+        const double sx = __dsub_rn(L.dx(), L.px), sy = __dsub_rn(L.dy(), L.py),
+                     sz = __dsub_rn(L.dz(), L.pz);
         const double ln = __dsqrt_rn(
             __dadd_rn(__dadd_rn(__dmul_rn(sx, sx), __dmul_rn(sy, sy)), __dmul_rn(sz, sz)));
         if (ln > 0.0) {
@@ -209,7 +232,7 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
     int face;
     double t;
     bool exact_used, need_t;
-    int kind = exit_search_fast(T, ox, oy, oz, L.dx, L.dy, L.dz, L.entry, &face, &t, &exact_used,
+    int kind = exit_search_fast(T, ox, oy, oz, L.dx(), L.dy(), L.dz(), L.entry, &face, &t, &exact_used,
                                 true, &need_t);
     if (kind == 1) {
         // issue the next element's record load now: it lands while the exact
@@ -220,12 +243,12 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
             L.have_nr = true;
         }
         if (need_t)
-            t = exact_t(T, face, ox, oy, oz, rn_sub(L.dx, ox), rn_sub(L.dy, oy), rn_sub(L.dz, oz));
+            t = exact_t(T, face, ox, oy, oz, rn_sub(L.dx(), ox), rn_sub(L.dy(), oy), rn_sub(L.dz(), oz));
     }
     bool done = false;
     bool event = true;
     if (kind == 2) {  // stuck ladder, search.py:199-235
-        if (contains(T, L.dx, L.dy, L.dz, STUCK_TOL)) {
+        if (contains(T, L.dx(), L.dy(), L.dz(), STUCK_TOL)) {
             kind = 0;
             atomicAdd(C.sh + SC_RECOV, 1u);
         } else if (L.st == 0) {
@@ -252,14 +275,14 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
                 L.st = 2;
                 atomicAdd(C.sh + SC_RECOV, 1u);
             } else {
-                L.outcome = OUT_STUCK_KILLED;
-                L.alive = 0;
+                L.outcome() = OUT_STUCK_KILLED;
+                L.alive() = 0;
                 atomicAdd(C.sh + SC_KILLED, 1u);
                 done = true;
             }
         } else {
-            L.outcome = OUT_STUCK_KILLED;
-            L.alive = 0;
+            L.outcome() = OUT_STUCK_KILLED;
+            L.alive() = 0;
             atomicAdd(C.sh + SC_KILLED, 1u);
             event = false;
             done = true;
@@ -274,20 +297,20 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
         }
         double qx, qy, qz;
         if (kind == 0) {
-            qx = L.dx;
-            qy = L.dy;
-            qz = L.dz;
+            qx = L.dx();
+            qy = L.dy();
+            qz = L.dz();
         } else {
-            qx = __dadd_rn(ox, __dmul_rn(t, __dsub_rn(L.dx, ox)));
-            qy = __dadd_rn(oy, __dmul_rn(t, __dsub_rn(L.dy, oy)));
-            qz = __dadd_rn(oz, __dmul_rn(t, __dsub_rn(L.dz, oz)));
+            qx = __dadd_rn(ox, __dmul_rn(t, __dsub_rn(L.dx(), ox)));
+            qy = __dadd_rn(oy, __dmul_rn(t, __dsub_rn(L.dy(), oy)));
+            qz = __dadd_rn(oz, __dmul_rn(t, __dsub_rn(L.dz(), oz)));
         }
         const double ax = __dsub_rn(qx, L.px), ay = __dsub_rn(qy, L.py), az = __dsub_rn(qz, L.pz);
         const double seg = __dsqrt_rn(
             __dadd_rn(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)), __dmul_rn(az, az)));
         P.has = a.score != 0;
-        P.bin = (int64_t)L.e * a.ngroups + L.g;
-        P.val = __dmul_rn(L.w, seg);
+        P.bin = (int64_t)L.e * a.ngroups + L.g();
+        P.val = __dmul_rn(L.w(), seg);
         P.seg = seg;
         P.seg_pending = true;
         L.px = qx;
@@ -295,14 +318,14 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
         L.pz = qz;
         if (kind == 0) {
             L.entry = -1;
-            L.outcome = OUT_REACHED;
+            L.outcome() = OUT_REACHED;
             atomicAdd(C.sh + SC_REACHED, 1u);
             done = true;
         } else {
             const int nbp = face == 0 ? r.nb[0] : face == 1 ? r.nb[1] : face == 2 ? r.nb[2] : r.nb[3];
             if (nbp < 0) {
-                L.outcome = OUT_LEAKED;
-                L.alive = 0;
+                L.outcome() = OUT_LEAKED;
+                L.alive() = 0;
                 atomicAdd(C.sh + SC_BOUNDARY, 1u);
                 done = true;
             } else {
@@ -317,7 +340,7 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
         done = true;
     }
     if (done && P.seg_pending) {  // the final seg_total is written now
-        L.seg = __dadd_rn(L.seg, P.seg);
+        L.seg() = __dadd_rn(L.seg(), P.seg);
         P.seg_pending = false;
     }
     return done;
@@ -325,22 +348,22 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
 
 __device__ __forceinline__ void finish(const WalkArgs& a, Lane& L, Counters& C,
                                        const DigestSlot& DS) {
-    const int64_t i = L.idx;
+    const int64_t i = L.idx();
     a.pos[3 * i] = L.px;
     a.pos[3 * i + 1] = L.py;
     a.pos[3 * i + 2] = L.pz;
     a.element[i] = L.e;
     a.entry[i] = (int8_t)L.entry;
     a.stuck[i] = (int8_t)L.st;
-    a.outcome[i] = (int8_t)L.outcome;
-    a.alive[i] = (int8_t)L.alive;
-    a.seg_total[i] = L.seg;
+    a.outcome[i] = (int8_t)L.outcome();
+    a.alive[i] = (int8_t)L.alive();
+    a.seg_total[i] = L.seg();
     if (a.digest) {
         a.digest[i] = *DS.d;
         a.dcount[i] = *DS.c;
     }
     atomicMax(C.sh + SC_MAXIT, (unsigned)L.iters);
-    L.idx = -1;
+    L.busy = false;
 }
 
 __device__ __forceinline__ void begin(Lane& L, const WalkArgs& a, const DigestSlot& DS) {
@@ -350,8 +373,8 @@ __device__ __forceinline__ void begin(Lane& L, const WalkArgs& a, const DigestSl
         *DS.d = DIGEST_INIT;
         *DS.c = 0;
     }
-    L.alive = 1;          // overwritten by the fetch with alive | flying (load_step)
-    L.outcome = OUT_NONE;
+    L.alive() = 1;          // overwritten by the fetch with alive | flying (load_step)
+    L.outcome() = OUT_NONE;
 }
 
 __device__ __forceinline__ void score(const WalkArgs& a, bool has_score, int64_t bin, double val) {
@@ -417,6 +440,7 @@ __device__ __forceinline__ void flush_counters(const WalkArgs& a, Counters& C) {
 // warp per refill); the fetch's global loads sit on the step's critical path.
 template <int THREADS, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB) walk_kernel(const WalkArgs a) {
+    static_assert(THREADS <= MAX_CTA_THREADS, "one shared lane slot per thread");
     constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     __shared__ unsigned shc[SC_N];
@@ -425,21 +449,21 @@ __global__ void __launch_bounds__(THREADS, MINB) walk_kernel(const WalkArgs a) {
     counters_init(shc);
     const DigestSlot DS{sdig + threadIdx.x, scnt + threadIdx.x};
     Lane L;
-    L.idx = -1;
+    L.busy = false;
     Counters C;
     C.sh = shc;
     Pending P;
     bool drained = false;
     while (true) {
         if (!drained) {
-            const unsigned idle = __ballot_sync(FULL, L.idx < 0);
+            const unsigned idle = __ballot_sync(FULL, !L.busy);
             if (idle) {
                 const unsigned nidle = __popc(idle);
                 unsigned long long base = 0;
                 if (lane == 0) base = atomicAdd(a.queue, (unsigned long long)nidle);
                 base = __shfl_sync(FULL, base, 0);
                 if (base + nidle >= (unsigned long long)a.count) drained = true;
-                if (L.idx < 0) {
+                if (!L.busy) {
                     const unsigned long long q = base + __popc(idle & lanemask_lt());
                     if (q < (unsigned long long)a.count) {
                         const int64_t i = a.order ? (int64_t)a.order[q] : (int64_t)q;
@@ -450,35 +474,35 @@ __global__ void __launch_bounds__(THREADS, MINB) walk_kernel(const WalkArgs a) {
                         const bool unloc = a.fly_in[i] != 0 && a.element[i] < 0;
                         if (unloc) atomicAdd(a.counters + C_UNLOC, 1ull);
                         if (a.fly_in[i] != 0 && !unloc) {
-                            L.idx = i;
+                            L.set_idx(i);
                             L.e = a.element[i];
                             L.px = a.pos[3 * i];
                             L.py = a.pos[3 * i + 1];
                             L.pz = a.pos[3 * i + 2];
-                            L.dx = a.dest[3 * i];
-                            L.dy = a.dest[3 * i + 1];
-                            L.dz = a.dest[3 * i + 2];
+                            L.dx() = a.dest[3 * i];
+                            L.dy() = a.dest[3 * i + 1];
+                            L.dz() = a.dest[3 * i + 2];
                             L.entry = a.entry[i];
                             L.st = a.stuck[i];
-                            L.seg = a.seg_total[i];
-                            L.w = a.score ? a.weight[i] : 0.0;
-                            L.g = a.score ? a.group[i] : 0;
+                            L.seg() = a.seg_total[i];
+                            L.w() = a.score ? a.weight[i] : 0.0;
+                            L.g() = a.score ? a.group[i] : 0;
                             begin(L, a, DS);
-                            L.alive = (int8_t)(a.alive[i] | a.fly_in[i]);
+                            L.alive() = (int8_t)(a.alive[i] | a.fly_in[i]);
                         }
                     }
                 }
             }
         }
-        if (!__any_sync(FULL, L.idx >= 0)) {
+        if (!__any_sync(FULL, L.busy)) {
             flush_pending(a, P, true);
             if (drained) break;
             continue;
         }
-        if (L.idx >= 0) {
+        if (L.busy) {
             if (walk_step(a, L, C, P, DS)) finish(a, L, C, DS);
         }
-        flush_pending(a, P, L.idx < 0);
+        flush_pending(a, P, !L.busy);
     }
     flush_counters(a, C);
 }
@@ -544,8 +568,12 @@ __device__ __forceinline__ int claim_chunk(const WalkArgs& a, const WorkSoA& W, 
 template <int THREADS, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB)
     walk_staged_kernel(const WalkArgs a, const WorkSoA W, const int64_t* __restrict__ nwork_p) {
+    static_assert(THREADS <= MAX_CTA_THREADS, "one shared lane slot per thread");
     constexpr unsigned FULL = 0xffffffffu;
-    __shared__ WarpStage stages[THREADS / 32][2];
+    // the warps' double-buffered stages: dynamic shared memory (with the lane
+    // slots the CTA exceeds the 48 KB static limit)
+    extern __shared__ __align__(16) unsigned char dyn_smem[];
+    WarpStage(*stages)[2] = reinterpret_cast<WarpStage(*)[2]>(dyn_smem);
     __shared__ unsigned shc[SC_N];
     __shared__ uint64_t sdig[THREADS];
     __shared__ int scnt[THREADS];
@@ -554,7 +582,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     const int wid = threadIdx.x >> 5;
     const int64_t nwork = *nwork_p;
     Lane L;
-    L.idx = -1;
+    L.busy = false;
     Counters C;
     C.sh = shc;
     Pending P;
@@ -567,7 +595,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     cp_async_wait_all();
     __syncwarp();
     while (true) {
-        unsigned idle = __ballot_sync(FULL, L.idx < 0);
+        unsigned idle = __ballot_sync(FULL, !L.busy);
         while (idle) {
             if (head == ncur) {  // current stage used up: switch to the prefetched one
                 if (nnext == 0) break;
@@ -580,40 +608,40 @@ __global__ void __launch_bounds__(THREADS, MINB)
                 nnext = (ncur == 32) ? claim_chunk(a, W, stages[wid][cur ^ 1], nwork) : 0;
             }
             const int take = min((int)__popc(idle), ncur - head);
-            if (L.idx < 0) {
+            if (!L.busy) {
                 const int rk = __popc(idle & lanemask_lt());
                 if (rk < take) {
                     const WarpStage& s = stages[wid][cur];
                     const int j = head + rk;
-                    L.idx = s.idx[j];
+                    L.set_idx(s.idx[j]);
                     L.px = s.px[j];
                     L.py = s.py[j];
                     L.pz = s.pz[j];
-                    L.dx = s.dx[j];
-                    L.dy = s.dy[j];
-                    L.dz = s.dz[j];
-                    L.w = s.w[j];
-                    L.seg = s.seg[j];
+                    L.dx() = s.dx[j];
+                    L.dy() = s.dy[j];
+                    L.dz() = s.dz[j];
+                    L.w() = s.w[j];
+                    L.seg() = s.seg[j];
                     L.e = s.e[j];
-                    L.g = s.g[j];
+                    L.g() = s.g[j];
                     const int fl = s.fl[j];
                     L.entry = (int)(signed char)(fl & 0xff);
                     L.st = (fl >> 8) & 0xff;
                     begin(L, a, DS);
-                    L.alive = (int)(signed char)((fl >> 16) & 0xff);
+                    L.alive() = (int)(signed char)((fl >> 16) & 0xff);
                 }
             }
             head += take;
-            idle = __ballot_sync(FULL, L.idx < 0);
+            idle = __ballot_sync(FULL, !L.busy);
         }
-        if (!__any_sync(FULL, L.idx >= 0)) {  // no work left anywhere for this warp
+        if (!__any_sync(FULL, L.busy)) {  // no work left anywhere for this warp
             flush_pending(a, P, true);
             break;
         }
-        if (L.idx >= 0) {
+        if (L.busy) {
             if (walk_step(a, L, C, P, DS)) finish(a, L, C, DS);
         }
-        flush_pending(a, P, L.idx < 0);
+        flush_pending(a, P, !L.busy);
     }
     cp_async_wait_all();
     flush_counters(a, C);
@@ -785,6 +813,7 @@ __global__ void transport_source_kernel(TransportArgs a, double box0, double box
 // one history per lane, persistent; refill from a global counter
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS, 1) transport_kernel(const TransportArgs t) {
+    static_assert(THREADS <= MAX_CTA_THREADS, "one shared lane slot per thread");
     constexpr unsigned FULL = 0xffffffffu;
     const WalkArgs& a = t.w;
     const int lane = threadIdx.x & 31;
@@ -792,7 +821,7 @@ __global__ void __launch_bounds__(THREADS, 1) transport_kernel(const TransportAr
     counters_init(shc);
     const DigestSlot DS{nullptr, nullptr};
     Lane L;
-    L.idx = -1;
+    L.busy = false;
     Counters C;
     C.sh = shc;
     Pending P;
@@ -805,25 +834,25 @@ __global__ void __launch_bounds__(THREADS, 1) transport_kernel(const TransportAr
     bool need_flight = false;
     while (true) {
         if (!drained) {
-            const unsigned idle = __ballot_sync(FULL, L.idx < 0);
+            const unsigned idle = __ballot_sync(FULL, !L.busy);
             if (idle) {
                 const unsigned nidle = __popc(idle);
                 unsigned long long base = 0;
                 if (lane == 0) base = atomicAdd(t.queue, (unsigned long long)nidle);
                 base = __shfl_sync(FULL, base, 0);
                 if (base + nidle >= (unsigned long long)t.n) drained = true;
-                if (L.idx < 0) {
+                if (!L.busy) {
                     const unsigned long long q = base + __popc(idle & lanemask_lt());
                     if (q < (unsigned long long)t.n && a.alive[q]) {
                         const int64_t i = (int64_t)q;
-                        L.idx = i;
+                        L.set_idx(i);
                         L.e = a.element[i];
                         L.px = a.pos[3 * i];
                         L.py = a.pos[3 * i + 1];
                         L.pz = a.pos[3 * i + 2];
-                        L.seg = 0.0;
-                        L.w = t.weight_rw[i];
-                        L.g = t.group_rw[i];
+                        L.seg() = 0.0;
+                        L.w() = t.weight_rw[i];
+                        L.g() = t.group_rw[i];
                         ux = t.dir[3 * i];
                         uy = t.dir[3 * i + 1];
                         uz = t.dir[3 * i + 2];
@@ -836,24 +865,24 @@ __global__ void __launch_bounds__(THREADS, 1) transport_kernel(const TransportAr
                 }
             }
         }
-        if (!__any_sync(FULL, L.idx >= 0)) {
+        if (!__any_sync(FULL, L.busy)) {
             flush_pending(a, P, true);
             if (drained) break;
             continue;
         }
-        if (L.idx >= 0) {
+        if (L.busy) {
             if (need_flight) {  // _flight (transport.py:213-226)
                 double u[4];
-                uniform_block(t.seed, t.batch, (uint64_t)L.idx, rb, u);
+                uniform_block(t.seed, t.batch, (uint64_t)L.idx(), rb, u);
                 ++rb;
-                const double lc = __ddiv_rn(-log(u[0]), t.xs.sigma_t[L.g]);
-                L.dx = __dadd_rn(L.px, __dmul_rn(lc, ux));
-                L.dy = __dadd_rn(L.py, __dmul_rn(lc, uy));
-                L.dz = __dadd_rn(L.pz, __dmul_rn(lc, uz));
+                const double lc = __ddiv_rn(-log(u[0]), t.xs.sigma_t[L.g()]);
+                L.dx() = __dadd_rn(L.px, __dmul_rn(lc, ux));
+                L.dy() = __dadd_rn(L.py, __dmul_rn(lc, uy));
+                L.dz() = __dadd_rn(L.pz, __dmul_rn(lc, uz));
                 L.have_nr = false;
                 L.iters = 0;
-                L.outcome = OUT_NONE;
-                L.alive = 1;
+                L.outcome() = OUT_NONE;
+                L.alive() = 1;
                 ++rounds;
                 need_flight = false;
             }
@@ -861,13 +890,13 @@ __global__ void __launch_bounds__(THREADS, 1) transport_kernel(const TransportAr
                 // flight over: its walk took L.iters sweeps in round `rounds`
                 if (rounds <= MAX_ROUNDS_TRACKED) atomicMax(t.round_max + rounds - 1, (unsigned)L.iters);
                 bool stop = true;
-                if (L.outcome == OUT_REACHED) {  // _collide (transport.py:229-275)
-                    const int g = L.g;
+                if (L.outcome() == OUT_REACHED) {  // _collide (transport.py:229-275)
+                    const int g = L.g();
                     const double st_g = t.xs.sigma_t[g];
-                    atomicAdd(t.col_tally + (int64_t)L.e * t.xs.ng + g, __ddiv_rn(L.w, st_g));
+                    atomicAdd(t.col_tally + (int64_t)L.e * t.xs.ng + g, __ddiv_rn(L.w(), st_g));
                     ++collisions;
                     double u[4];
-                    uniform_block(t.seed, t.batch, (uint64_t)L.idx, rb, u);
+                    uniform_block(t.seed, t.batch, (uint64_t)L.idx(), rb, u);
                     ++rb;
                     if (u[0] <= t.xs.scatter_prob[g]) {
                         int gp = 0;
@@ -876,7 +905,7 @@ __global__ void __launch_bounds__(THREADS, 1) transport_kernel(const TransportAr
                             if (u[1] <= t.xs.group_cdf[g * t.xs.ng + j]) break;
                         }
                         iso_dir(u[2], u[3], ux, uy, uz);
-                        L.g = gp;
+                        L.g() = gp;
                         stop = false;
                         need_flight = true;
                         if (rounds >= t.max_rounds) {  // _MAX_ROUNDS guard (transport.py:531-533)
@@ -884,36 +913,36 @@ __global__ void __launch_bounds__(THREADS, 1) transport_kernel(const TransportAr
                             stop = true;
                         }
                     } else {
-                        L.alive = 0;
-                        L.outcome = 5;  // OUTCOME_ABSORBED
-                        absorbed += L.w;
+                        L.alive() = 0;
+                        L.outcome() = 5;  // OUTCOME_ABSORBED
+                        absorbed += L.w();
                     }
-                } else if (L.outcome == OUT_LEAKED) {
-                    leaked += L.w;
-                } else if (L.outcome == OUT_STUCK_KILLED) {
-                    stuck_w += L.w;
+                } else if (L.outcome() == OUT_LEAKED) {
+                    leaked += L.w();
+                } else if (L.outcome() == OUT_STUCK_KILLED) {
+                    stuck_w += L.w();
                 }
                 if (stop) {
-                    const int64_t i = L.idx;
+                    const int64_t i = L.idx();
                     a.pos[3 * i] = L.px;
                     a.pos[3 * i + 1] = L.py;
                     a.pos[3 * i + 2] = L.pz;
                     a.element[i] = L.e;
                     a.entry[i] = (int8_t)L.entry;
                     a.stuck[i] = (int8_t)L.st;
-                    a.outcome[i] = (int8_t)L.outcome;
-                    a.alive[i] = (int8_t)L.alive;
-                    a.seg_total[i] = L.seg;
+                    a.outcome[i] = (int8_t)L.outcome();
+                    a.alive[i] = (int8_t)L.alive();
+                    a.seg_total[i] = L.seg();
                     t.dir[3 * i] = ux;
                     t.dir[3 * i + 1] = uy;
                     t.dir[3 * i + 2] = uz;
                     t.rng_block[i] = rb;
-                    t.group_rw[i] = L.g;
-                    L.idx = -1;
+                    t.group_rw[i] = L.g();
+                    L.busy = false;
                 }
             }
         }
-        flush_pending(a, P, L.idx < 0);
+        flush_pending(a, P, !L.busy);
     }
     // reduce the per-lane totals (tally sums are order-free up to rounding)
     for (int o = 16; o > 0; o >>= 1) {
@@ -2120,8 +2149,10 @@ static bt_status walk_enqueue(bt_tally* h, WalkArgs a, int64_t lo, int64_t hi, i
                                                                        : DEFAULT_VARIANT) - 1;
     const Variant& V = kVariants[vi];
     const void* kptr = staged ? (const void*)V.staged : (const void*)V.plain;
+    const size_t dyn = staged ? sizeof(WarpStage) * 2 * (V.threads / 32) : 0;
+    if (staged) CK(cudaFuncSetAttribute(kptr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     int bps = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kptr, V.threads, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kptr, V.threads, dyn));
     bps = std::max(1, bps);
     const int64_t want = (count + V.threads - 1) / V.threads;
     const unsigned blocks =
@@ -2142,7 +2173,7 @@ static bt_status walk_enqueue(bt_tally* h, WalkArgs a, int64_t lo, int64_t hi, i
         h->walk_first = false;
     }
     if (staged)
-        V.staged<<<blocks, V.threads, 0, h->stream>>>(a, W, nwork);
+        V.staged<<<blocks, V.threads, dyn, h->stream>>>(a, W, nwork);
     else
         V.plain<<<blocks, V.threads, 0, h->stream>>>(a);
     CK(cudaGetLastError());

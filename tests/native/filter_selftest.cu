@@ -14,8 +14,9 @@ extern "C" int bt_filter_selftest(const double* vertices, const int32_t* element
                                   const int32_t* adj_elem, const int8_t* adj_face,
                                   const int32_t* start_elem, const double* start_pos,
                                   const double* dest, int64_t n, int64_t max_steps,
-                                  int64_t* stats /* steps, mismatches, fallbacks, stuck */) {
-    int64_t steps = 0, mism = 0, fb = 0, stuck = 0;
+                                  int64_t* stats /* steps, mismatches, fallbacks, stuck,
+                                                    fp32-undecided */) {
+    int64_t steps = 0, mism = 0, fb = 0, stuck = 0, und32 = 0;
     for (int64_t i = 0; i < n; ++i) {
         int e = start_elem[i];
         if (e < 0) continue;
@@ -37,6 +38,18 @@ extern "C" int bt_filter_selftest(const double* vertices, const int32_t* element
             const int k2 = exit_search_fast(T, ox, oy, oz, dx, dy, dz, entry, &f2, &t2, &ex);
             ++steps;
             if (ex) ++fb;
+            {
+                int f3 = -1;
+                unsigned q3 = 0;
+                if (exit_filter32(T, ox, oy, oz, dx, dy, dz, entry, &f3, &q3) == XF_EXACT) ++und32;
+                // the fp64 filter (BT_F64_STAGE builds) against the literal result
+                int f4 = -1;
+                unsigned q4 = 0;
+                const int x4 = exit_filter(T, ox, oy, oz, dx, dy, dz, entry, &f4, &q4);
+                if ((x4 == XF_REACHED && k1 != 0) || (x4 == XF_EXIT && (k1 != 1 || f4 != f1)) ||
+                    (x4 == XF_MULTI && (k1 != 1 || !((q4 >> f1) & 1u))))
+                    ++mism;
+            }
             if (k1 != k2 || f1 != f2 || std::memcmp(&t1, &t2, sizeof t1) != 0) ++mism;
             if (k1 != 1) {
                 if (k1 == 2) ++stuck;
@@ -58,6 +71,7 @@ extern "C" int bt_filter_selftest(const double* vertices, const int32_t* element
     stats[1] = mism;
     stats[2] = fb;
     stats[3] = stuck;
+    stats[4] = und32;
     return 0;
 }
 

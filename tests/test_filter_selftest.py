@@ -32,12 +32,12 @@ def run(L, mesh, elem, pos, dest, max_steps=100000):
     pos = np.ascontiguousarray(pos, dtype=np.float64)
     dest = np.ascontiguousarray(dest, dtype=np.float64)
     elem = np.ascontiguousarray(elem, dtype=np.int32)
-    st = np.zeros(4, np.int64)
+    st = np.zeros(5, np.int64)
     L.bt_filter_selftest(mesh.vertices.ctypes.data, mesh.elements.ctypes.data,
                          mesh.adj_elem.ctypes.data, mesh.adj_face.ctypes.data,
                          elem.ctypes.data, pos.ctypes.data, dest.ctypes.data,
                          pos.shape[0], max_steps, st.ctypes.data)
-    return dict(zip(("steps", "mismatches", "fallbacks", "stuck"), st.tolist()))
+    return dict(zip(("steps", "mismatches", "fallbacks", "stuck", "undecided32"), st.tolist()))
 
 
 def _locate(mesh, pts):
@@ -56,6 +56,8 @@ def test_random_walks_cube(lib):
     assert r["steps"] > 100000
     assert r["mismatches"] == 0, r
     assert r["fallbacks"] < 1e-3 * r["steps"], r
+    # the fp32 pre-filter decides almost every generic step
+    assert r["undecided32"] < 5e-3 * r["steps"], r
 
 
 def test_adversarial_grid_planes(lib):
@@ -126,3 +128,19 @@ def test_contains_fast_matches_exact(lib, tol):
     mism = L.bt_contains_selftest(m.vertices.ctypes.data, m.elements.ctypes.data,
                                   m.num_elements, pts.ctypes.data, k, tol, fb.ctypes.data)
     assert mism == 0
+
+
+@pytest.mark.parametrize("scale,offset", [(1e-2, 1e4), (1e3, -5e5), (1e9, 0.0), (1e11, 3e12)])
+def test_scaled_translated_meshes(lib, scale, offset):
+    """The fp32 pre-filter's bounds are scale-free inside its range guard and
+    hand everything outside it (tiny or huge meshes) to the fp64 filter."""
+    from paper_2504_19048_b200 import TetMesh
+    m0 = build_cube_mesh(6)
+    m = TetMesh.from_arrays(m0.vertices * scale + offset, m0.elements)
+    gen = np.random.default_rng(6)
+    k = 4000
+    pos = synth.uniform_box(gen, k) * scale + offset
+    dest = pos + gen.normal(size=pos.shape) * 0.4 * scale
+    r = run(lib, m, _locate(m, pos), pos, dest)
+    assert r["steps"] > 4000
+    assert r["mismatches"] == 0, r
