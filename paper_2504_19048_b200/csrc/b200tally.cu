@@ -24,6 +24,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -1667,6 +1668,7 @@ struct bt_tally {
     double* dwsum = nullptr;
     unsigned long long* hcounters = nullptr;  // pinned
     int move_chunks = 0;                      // host-input pipeline depth (0 = auto)
+    std::vector<double> host_sel;             // host scratch: weights of flying particles
     // transport (allocated on first bt_transport_run)
     double* col_tally = nullptr;
     double* col_sum = nullptr;
@@ -1865,6 +1867,53 @@ static double pairwise_sum(const double* a, int64_t n) {
         n2 -= n2 % 8;
         return pairwise_sum(a, n2) + pairwise_sum(a + n2, n - n2);
     }
+}
+
+// The same summation tree with its top `depth` levels' left subtrees on
+// their own threads: bit-identical to pairwise_sum.
+static double pairwise_sum_par(const double* a, int64_t n, int depth) {
+    if (depth <= 0 || n <= (1 << 16)) return pairwise_sum(a, n);
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    double left = 0.0;
+    std::thread t([&] { left = pairwise_sum_par(a, n2, depth - 1); });
+    const double right = pairwise_sum_par(a + n2, n - n2, depth - 1);
+    t.join();
+    return left + right;
+}
+
+// weights[flying != 0] (numpy boolean-mask order) into `out`, in parallel
+// blocks; returns the selected count, or -1 (out untouched) when every
+// particle is flying and the weights can be summed in place
+static int64_t select_flying(const double* w, const int8_t* fly, int64_t n, double* out,
+                             int nthreads) {
+    const int64_t nb = std::max<int64_t>(1, std::min<int64_t>(nthreads, n >> 16));
+    std::vector<int64_t> cnt((size_t)nb + 1, 0);
+    auto count_block = [&](int64_t b) {
+        const int64_t lo = n * b / nb, hi = n * (b + 1) / nb;
+        int64_t c = 0;
+        for (int64_t i = lo; i < hi; ++i) c += fly[i] != 0;
+        cnt[(size_t)b + 1] = c;
+    };
+    {
+        std::vector<std::thread> th;
+        for (int64_t b = 1; b < nb; ++b) th.emplace_back(count_block, b);
+        count_block(0);
+        for (auto& t : th) t.join();
+    }
+    for (int64_t b = 0; b < nb; ++b) cnt[(size_t)b + 1] += cnt[(size_t)b];
+    if (cnt[(size_t)nb] == n) return -1;
+    auto copy_block = [&](int64_t b) {
+        const int64_t lo = n * b / nb, hi = n * (b + 1) / nb;
+        double* o = out + cnt[(size_t)b];
+        for (int64_t i = lo; i < hi; ++i)
+            if (fly[i] != 0) *o++ = w[i];
+    };
+    std::vector<std::thread> th;
+    for (int64_t b = 1; b < nb; ++b) th.emplace_back(copy_block, b);
+    copy_block(0);
+    for (auto& t : th) t.join();
+    return cnt[(size_t)nb];
 }
 
 
@@ -2344,18 +2393,19 @@ bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, cons
         const double* w;
         const int8_t* fly;
         int64_t n;
+        double* sel;  // persistent host scratch (no page faults per call)
         double out;
-    } job{weights, flying, count, 0.0};
+    } job{weights, flying, count, nullptr, 0.0};
     HostOverlap ov;
     if (host && need_w) {
+        if ((int64_t)h->host_sel.size() < count) h->host_sel.assign((size_t)h->cap, 0.0);
+        job.sel = h->host_sel.data();
         ov.ctx = &job;
         ov.fn = [](void* c) {
             WJob* j = static_cast<WJob*>(c);
-            std::vector<double> sel;
-            sel.reserve((size_t)j->n);
-            for (int64_t i = 0; i < j->n; ++i)
-                if (j->fly[i] != 0) sel.push_back(j->w[i]);
-            j->out = pairwise_sum(sel.data(), (int64_t)sel.size());
+            const int nt = (int)std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+            const int64_t m = select_flying(j->w, j->fly, j->n, j->sel, nt);
+            j->out = m < 0 ? pairwise_sum_par(j->w, j->n, 3) : pairwise_sum_par(j->sel, m, 3);
         };
     }
     bt_status s;

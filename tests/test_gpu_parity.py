@@ -244,3 +244,22 @@ def test_gpu_adjacency_matches_host():
             M.build_adjacency(els, 6, device=0)
         with pytest.raises(M.MalformedMeshError):
             M.build_adjacency(els, 6)
+
+
+@pytest.mark.parametrize("frac_flying", [1.0, 0.83])
+def test_recorded_source_weight_is_numpy_sum(frac_flying):
+    """The recorded source weight of a host-input move equals the reference's
+    weights[flying].sum() (numpy pairwise order) bit for bit, also when the
+    selection and the summation tree run on several host threads."""
+    m = build_cube_mesh(6)
+    gen = np.random.default_rng(11)
+    n = 700_000
+    pos = synth.uniform_box(gen, n)
+    dest = synth.flight_destinations(gen, pos, 20.0)
+    fly = (gen.random(n) < frac_flying).astype(np.int8)
+    w = 0.5 + gen.random(n)
+    mt = MeshTally(m, n)
+    mt.initialize_particle_location(pos)
+    mt.move_to_next_location(dest, fly, w)
+    assert mt.source_weight == w[fly != 0].sum()
+    mt.close()
