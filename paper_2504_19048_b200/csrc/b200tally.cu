@@ -1346,67 +1346,103 @@ struct LocateArgs {
     double bbox[6];
     double c0[3];
     int64_t count;
+    int64_t lo;  // locate_grid_kernel: first particle of this launch
 };
 
-// One warp per particle: 32 candidates tested at a time; candidates are in
-// ascending element order, so the lowest set ballot bit is the lowest-id
-// containing element (pkg/tests/oracles.py:36-57 semantics).
-// One thread per particle: candidates in ascending element order, a float
-// bounding-box test (rounded outward, expanded like the grid insertion)
-// before the exact-equivalent containment filter; the first hit is the
-// lowest-id containing element (pkg/tests/oracles.py:36-57 semantics).
-__global__ void __launch_bounds__(256) locate_grid_kernel(const LocateArgs a) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= a.count) return;
-    const double p0 = a.target[3 * i], p1 = a.target[3 * i + 1], p2 = a.target[3 * i + 2];
-    const bool inside = p0 >= a.bbox[0] && p0 <= a.bbox[3] && p1 >= a.bbox[1] &&
+// Warp-parallel grid search (the north star's localization kernel): a group
+// of G lanes serves one particle (32/G particles per warp).  The group's
+// lanes take G of the cell's candidates at a time -- ascending element ids --
+// so the candidate, bounding-box and vertex gathers of one particle are in
+// flight together instead of one after another; candidates whose float box
+// (rounded outward, expanded like the grid insertion) holds the point run
+// the exact-equivalent containment filter.  The lowest lane with a hit in
+// the first chunk that has one is the lowest-id containing element
+// (pkg/tests/oracles.py:36-57 semantics), for every G.
+constexpr int LOCATE_THREADS = 256;
+template <int G>
+__global__ void __launch_bounds__(LOCATE_THREADS) locate_grid_kernel(const LocateArgs a) {
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr unsigned GMASK = G == 32 ? FULL : ((1u << G) - 1u);
+    const int lane = threadIdx.x & 31;
+    const int gl = lane % G, gid = lane / G;
+    const int64_t i =
+        a.lo + (blockIdx.x * (int64_t)LOCATE_THREADS + threadIdx.x) / G;  // this group's particle
+    const bool valid = i < a.count;
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+    if (valid) {
+        p0 = a.target[3 * i];
+        p1 = a.target[3 * i + 1];
+        p2 = a.target[3 * i + 2];
+    }
+    const bool inside = valid && p0 >= a.bbox[0] && p0 <= a.bbox[3] && p1 >= a.bbox[1] &&
                         p1 <= a.bbox[4] && p2 >= a.bbox[2] && p2 <= a.bbox[5];
-    int found = -1;
+    int s0 = 0, s1 = 0;
     if (inside) {
         const int ci = grid_axis(p0, a.G.org[0], a.G.cs[0], a.G.dims[0]);
         const int cj = grid_axis(p1, a.G.org[1], a.G.cs[1], a.G.dims[1]);
         const int ck = grid_axis(p2, a.G.org[2], a.G.cs[2], a.G.dims[2]);
         const int64_t cell = ((int64_t)ci * a.G.dims[1] + cj) * a.G.dims[2] + ck;
-        const int s0 = __ldg(a.G.cell_start + cell), s1 = __ldg(a.G.cell_start + cell + 1);
-        for (int k = s0; k < s1; ++k) {
-            const int c = __ldg(a.G.cand + k);
+        s0 = __ldg(a.G.cell_start + cell);
+        s1 = __ldg(a.G.cell_start + cell + 1);
+    }
+    int found = -1;
+    bool done = false;
+    for (int k0 = s0;; k0 += G) {
+        const bool act = !done && k0 < s1;  // group-uniform
+        if (!__any_sync(FULL, act)) break;
+        int c = -1;
+        bool hit = false;
+        const int k = k0 + gl;
+        if (act && k < s1) {
+            c = __ldg(a.G.cand + k);
             const float4 lo = __ldg(reinterpret_cast<const float4*>(a.ebox + c));
             const float4 hi = __ldg(reinterpret_cast<const float4*>(a.ebox + c) + 1);
-            if (p0 < lo.x || p0 > hi.x || p1 < lo.y || p1 > hi.y || p2 < lo.z || p2 > hi.z)
-                continue;
-            const ElemRec r = load_rec(a.rec, c);
-            Tet T;
+            if (!(p0 < lo.x || p0 > hi.x || p1 < lo.y || p1 > hi.y || p2 < lo.z || p2 > hi.z)) {
+                const ElemRec r = load_rec(a.rec, c);
+                Tet T;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const double2* vp = reinterpret_cast<const double2*>(a.vtx + r.v[j]);
-                const double2 xy = __ldg(vp);
-                const double2 zw = __ldg(vp + 1);
-                T.x[j] = xy.x;
-                T.y[j] = xy.y;
-                T.z[j] = zw.x;
-            }
-            if (contains_fast(T, p0, p1, p2, EPS_BARY)) {
-                found = c;
-                break;
+                for (int j = 0; j < 4; ++j) {
+                    const double2* vp = reinterpret_cast<const double2*>(a.vtx + r.v[j]);
+                    const double2 xy = __ldg(vp);
+                    const double2 zw = __ldg(vp + 1);
+                    T.x[j] = xy.x;
+                    T.y[j] = xy.y;
+                    T.z[j] = zw.x;
+                }
+                hit = contains_fast(T, p0, p1, p2, EPS_BARY);
             }
         }
+        const unsigned gm = (__ballot_sync(FULL, hit) >> (gid * G)) & GMASK;
+        const int src = gm ? gid * G + __ffs(gm) - 1 : lane;
+        const int fc = __shfl_sync(FULL, c, src);
+        if (act && gm) {
+            found = fc;
+            done = true;
+        }
     }
-    a.element[i] = found;
-    a.alive[i] = found >= 0 ? 1 : 0;
-    if (found >= 0 || inside) {
-        a.pos[3 * i] = p0;
-        a.pos[3 * i + 1] = p1;
-        a.pos[3 * i + 2] = p2;
-    } else {  // outside the bbox: the reference leaves centroid 0
-        a.pos[3 * i] = a.c0[0];
-        a.pos[3 * i + 1] = a.c0[1];
-        a.pos[3 * i + 2] = a.c0[2];
+    if (!valid) return;
+    if (gl < 3 && gl < G) {
+        const double pv = gl == 0 ? p0 : gl == 1 ? p1 : p2;
+        // outside the bbox the reference leaves centroid 0 (search.py:579-583)
+        a.pos[3 * i + gl] = (found >= 0 || inside) ? pv : a.c0[gl];
     }
-    a.entry[i] = -1;
-    a.stuck[i] = 0;
-    a.outcome[i] = found >= 0 ? OUT_REACHED : (inside ? OUT_LEAKED : OUT_NONE);
-    a.seg_total[i] = 0.0;
+    if (G < 3) {  // narrow groups: the group's first lane writes the rest of pos
+        if (gl == 0)
+            for (int d = G; d < 3; ++d) {
+                const double pv = d == 1 ? p1 : p2;
+                a.pos[3 * i + d] = (found >= 0 || inside) ? pv : a.c0[d];
+            }
+    }
+    if (gl == G - 1) {
+        a.element[i] = found;
+        a.alive[i] = found >= 0 ? 1 : 0;
+        a.entry[i] = -1;
+        a.stuck[i] = 0;
+        a.outcome[i] = found >= 0 ? OUT_REACHED : (inside ? OUT_LEAKED : OUT_NONE);
+        a.seg_total[i] = 0.0;
+    }
 }
+
 
 // walk-mode localization, step 1: search.py:577-591
 __global__ void init_walk_prep_kernel(LocateArgs a, int8_t* __restrict__ fly) {
@@ -1668,6 +1704,7 @@ struct bt_tally {
     double* dwsum = nullptr;
     unsigned long long* hcounters = nullptr;  // pinned
     int move_chunks = 0;                      // host-input pipeline depth (0 = auto)
+    int locate_lanes = 0;                     // grid search lanes per particle (0 = default)
     std::vector<double> host_sel;             // host scratch: weights of flying particles
     // transport (allocated on first bt_transport_run)
     double* col_tally = nullptr;
@@ -2094,6 +2131,12 @@ bt_status bt_set_option(bt_tally* h, int32_t key, int64_t value) {
         case BT_OPT_BLOCKS_PER_SM: h->blocks_per_sm = (int)value; break;
         case BT_OPT_STAGED: h->opt_staged = value != 0; break;
         case BT_OPT_MOVE_CHUNKS: h->move_chunks = (int)value; break;
+        case BT_OPT_LOCATE_LANES:
+            if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8 &&
+                value != 16 && value != 32)
+                return set_err(BT_EINVAL, "locate lanes must be 0, 1, 2, 4, 8, 16 or 32");
+            h->locate_lanes = (int)value;
+            break;
         default: return set_err(BT_EINVAL, "unknown option %d", key);
     }
     return BT_OK;
@@ -2270,6 +2313,26 @@ static bt_status run_walk(bt_tally* h, const double* dest, const int8_t* fly, co
     return walk_end(h, a.max_sweeps, summary, overlap);
 }
 
+// lanes per particle of the grid search (BT_OPT_LOCATE_LANES; 0 = default)
+constexpr int DEFAULT_LOCATE_LANES = 2;  // measured best on C2 and the 10M-tet cube (tools/locate_sweep.py)
+static bt_status launch_locate(bt_tally* h, const LocateArgs& la, int64_t n) {
+    const int g = h->locate_lanes > 0 ? h->locate_lanes : DEFAULT_LOCATE_LANES;
+    const int64_t threads = n * g;
+    const unsigned blocks = (unsigned)((threads + LOCATE_THREADS - 1) / LOCATE_THREADS);
+    switch (g) {
+        case 1: locate_grid_kernel<1><<<blocks, LOCATE_THREADS, 0, h->stream>>>(la); break;
+        case 2: locate_grid_kernel<2><<<blocks, LOCATE_THREADS, 0, h->stream>>>(la); break;
+        case 4: locate_grid_kernel<4><<<blocks, LOCATE_THREADS, 0, h->stream>>>(la); break;
+        case 8: locate_grid_kernel<8><<<blocks, LOCATE_THREADS, 0, h->stream>>>(la); break;
+        case 16: locate_grid_kernel<16><<<blocks, LOCATE_THREADS, 0, h->stream>>>(la); break;
+        case 32: locate_grid_kernel<32><<<blocks, LOCATE_THREADS, 0, h->stream>>>(la); break;
+        default: return set_err(BT_EINVAL, "locate lanes must be 1, 2, 4, 8, 16 or 32");
+    }
+    CK(cudaGetLastError());
+    h->kernels += 1;
+    return BT_OK;
+}
+
 static LocateArgs locate_args(bt_tally* h, const double* target, int64_t count) {
     LocateArgs a;
     a.rec = h->rec;
@@ -2287,6 +2350,7 @@ static LocateArgs locate_args(bt_tally* h, const double* target, int64_t count) 
     memcpy(a.bbox, h->bbox, sizeof a.bbox);
     memcpy(a.c0, h->c0, sizeof a.c0);
     a.count = count;
+    a.lo = 0;
     return a;
 }
 
@@ -2317,16 +2381,24 @@ bt_status bt_initialize_particle_location(bt_tally* h, const double* positions, 
         // return as soon as the caller's buffer has been read: the
         // localization kernel runs on while the next call's copies proceed
         // (every later kernel or readout is ordered after it on `stream`).
+        // Chunked: chunk c's localization starts as soon as its positions
+        // have landed, while the next chunks are still being copied.
         if (!h->init_stage) TRY(dalloc(&h->init_stage, 3 * h->cap));
         CK(cudaStreamWaitEvent(h->cstream, h->ev_loc, 0));  // previous localization done
-        CK(cudaMemcpyAsync(h->init_stage, positions, sizeof(double) * 3 * count,
-                           cudaMemcpyHostToDevice, h->cstream));
-        CK(cudaEventRecord(h->evc0, h->cstream));
-        CK(cudaStreamWaitEvent(h->stream, h->evc0, 0));
+        const int nch = (int)std::min<int64_t>(count >= (4 << 20) ? 4 : 1, count);
         LocateArgs la = locate_args(h, h->init_stage, count);
-        locate_grid_kernel<<<grid_for(count, 256), 256, 0, h->stream>>>(la);
-        CK(cudaGetLastError());
-        h->kernels += 1;
+        for (int c = 0; c < nch; ++c) {
+            const int64_t lo = count * c / nch, hi = count * (c + 1) / nch;
+            CK(cudaMemcpyAsync(h->init_stage + 3 * lo, positions + 3 * lo,
+                               sizeof(double) * 3 * (hi - lo), cudaMemcpyHostToDevice,
+                               h->cstream));
+            CK(cudaEventRecord(h->evchunk[c], h->cstream));
+            CK(cudaStreamWaitEvent(h->stream, h->evchunk[c], 0));
+            la.lo = lo;
+            la.count = hi;
+            TRY(launch_locate(h, la, hi - lo));
+        }
+        CK(cudaEventRecord(h->evc0, h->cstream));
         CK(cudaEventRecord(h->ev_loc, h->stream));
         CK(cudaEventRecord(h->ev3, h->stream));
         CK(cudaEventSynchronize(h->evc0));
@@ -2340,9 +2412,7 @@ bt_status bt_initialize_particle_location(bt_tally* h, const double* positions, 
     }
     LocateArgs la = locate_args(h, target, count);
     if (mode == BT_LOCATE_GRID) {
-        locate_grid_kernel<<<grid_for(count, 256), 256, 0, h->stream>>>(la);
-        CK(cudaGetLastError());
-        h->kernels += 1;
+        TRY(launch_locate(h, la, count));
     } else {
         init_walk_prep_kernel<<<grid_for(count, 256), 256, 0, h->stream>>>(la, h->fly);
         CK(cudaGetLastError());
@@ -2807,7 +2877,7 @@ bt_status bt_transport_run(bt_tally* h, const double* sigma_t, const double* sig
             t, box[0], box[1], box[2], box[3], box[4], box[5], fixed, fdx, fdy, fdz,
             h->init_stage);
         CK(cudaGetLastError());
-        locate_grid_kernel<<<grid_for(n, 256), 256, 0, h->stream>>>(la);
+        TRY(launch_locate(h, la, n));
         CK(cudaGetLastError());
         CK(cudaEventRecord(h->ev0, h->stream));
         count_alive_kernel<<<std::min<int64_t>(grid_for(n, 256), 1024), 256, 0, h->stream>>>(

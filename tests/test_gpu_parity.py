@@ -11,7 +11,7 @@ import pytest
 
 import oracle as orc
 from golden_cases import GOLDEN, STATE_KEYS, WALK_CASES, load_walk_case, rel_close
-from paper_2504_19048_b200 import MeshTally, build_cube_mesh, synth
+from paper_2504_19048_b200 import MeshTally, _lib, build_cube_mesh, synth
 
 pytestmark = pytest.mark.gpu
 
@@ -98,7 +98,8 @@ def test_walk_options_keep_parity(opts):
     _check_case(load_walk_case("n6_uniform_g3"), "grid", **opts)
 
 
-def test_localize_pathologies():
+@pytest.mark.parametrize("lanes", [0, 1, 2, 4, 8, 16, 32])
+def test_localize_pathologies(lanes):
     d = np.load(GOLDEN / "localize_ref.npz")
     m = build_cube_mesh(10)
     pts = d["points"]
@@ -110,7 +111,9 @@ def test_localize_pathologies():
     assert np.array_equal(st.alive, d["alive"])
     assert np.array_equal(st.outcome, d["outcome"])
     assert np.array_equal(st.position, d["position"])
-    # grid mode: lowest-id containing element everywhere (finds what the walk loses)
+    # grid mode: lowest-id containing element everywhere (finds what the walk loses),
+    # for every lane-group width of the warp-parallel search
+    mt.set_option(_lib.BT_OPT_LOCATE_LANES, lanes)
     mt.initialize_particle_location(pts, mode="grid")
     st = mt.read_particles()
     low = orc.locate_exhaustive(m, pts)
@@ -120,15 +123,21 @@ def test_localize_pathologies():
     assert np.array_equal(st.position[found], pts[found])
 
 
-def test_grid_localize_random_meshes():
+@pytest.mark.parametrize("lanes", [1, 4, 8, 32])
+def test_grid_localize_random_meshes(lanes):
     gen = np.random.default_rng(5)
     for n in (1, 3, 7, 16):
         m = build_cube_mesh(n)
-        pts = gen.uniform(-0.1, 1.1, (5000, 3))
+        pts = gen.uniform(-0.1, 1.1, (5003, 3))
         mt = MeshTally(m, pts.shape[0])
+        mt.set_option(_lib.BT_OPT_LOCATE_LANES, lanes)
         mt.initialize_particle_location(pts)
         st = mt.read_particles()
         assert np.array_equal(st.element, orc.locate_exhaustive(m, pts))
+        found = st.element >= 0
+        assert np.array_equal(st.position[found], pts[found])
+    with pytest.raises(ValueError):
+        mt.set_option(_lib.BT_OPT_LOCATE_LANES, 3)
 
 
 @pytest.mark.parametrize("sigma_t", [2.0, 100.0])
