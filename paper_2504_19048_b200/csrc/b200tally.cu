@@ -812,8 +812,8 @@ __global__ void transport_source_kernel(TransportArgs a, double box0, double box
 }
 
 // one history per lane, persistent; refill from a global counter
-template <int THREADS>
-__global__ void __launch_bounds__(THREADS, 1) transport_kernel(const TransportArgs t) {
+template <int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) transport_kernel(const TransportArgs t) {
     static_assert(THREADS <= MAX_CTA_THREADS, "one shared lane slot per thread");
     constexpr unsigned FULL = 0xffffffffu;
     const WalkArgs& a = t.w;
@@ -2858,11 +2858,16 @@ bt_status bt_transport_run(bt_tally* h, const double* sigma_t, const double* sig
     const int fixed = fixed_direction != nullptr;
     const double fdx = fixed ? fixed_direction[0] : 0.0, fdy = fixed ? fixed_direction[1] : 0.0,
                  fdz = fixed ? fixed_direction[2] : 0.0;
+    // launch variant: BT_OPT_BLOCKS_PER_SM = 1 -> 256 threads x 1 CTA/SM (<= 255 registers),
+    // otherwise 192 x 2 (<= 168 registers, the walk's default shape)
+    const bool wide = h->blocks_per_sm == 1;
+    const int tthreads = wide ? 256 : 192;
+    const void* tk = wide ? (const void*)transport_kernel<256, 1> : (const void*)transport_kernel<192, 2>;
     int bps = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, transport_kernel<256>, 256, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, tk, tthreads, 0));
     bps = std::max(1, bps);
     const unsigned blocks = (unsigned)std::max<int64_t>(
-        1, std::min<int64_t>((n + 255) / 256, (int64_t)bps * h->num_sms));
+        1, std::min<int64_t>((n + tthreads - 1) / tthreads, (int64_t)bps * h->num_sms));
     LocateArgs la = locate_args(h, h->init_stage, n);
     h->kernels = 0;
     float loc_ms = 0.f, batch_ms = 0.f;
@@ -2882,7 +2887,10 @@ bt_status bt_transport_run(bt_tally* h, const double* sigma_t, const double* sig
         CK(cudaEventRecord(h->ev0, h->stream));
         count_alive_kernel<<<std::min<int64_t>(grid_for(n, 256), 1024), 256, 0, h->stream>>>(
             h->alive, n, h->tr_count + 2);
-        transport_kernel<256><<<blocks, 256, 0, h->stream>>>(t);
+        if (wide)
+            transport_kernel<256, 1><<<blocks, 256, 0, h->stream>>>(t);
+        else
+            transport_kernel<192, 2><<<blocks, 192, 0, h->stream>>>(t);
         CK(cudaGetLastError());
         sum_rounds_kernel<<<256, 256, 0, h->stream>>>(h->tr_round_max, MAX_ROUNDS_TRACKED,
                                                       h->tr_count + 1);
