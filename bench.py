@@ -55,7 +55,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--sort", type=int, default=0)
-    p.add_argument("--warp-agg", type=int, default=0)
+    p.add_argument("--warp-agg", type=int, default=-1,
+                   help="tally atomics: -1 adaptive aggregation (default), 0 never, 1 always")
     p.add_argument("--blocks-per-sm", type=int, default=0)
     p.add_argument("--staged", type=int, default=1)
     return p.parse_args()
@@ -87,7 +88,8 @@ def config(args, world, ne):
         "parallelism": f"dp{world} (particle shards, mesh replicated, tally all-reduce)",
         "l2": "particle state ~1 GB/GPU streamed per step (> 126 MB L2, no flush needed); "
               "mesh 38 MB stays L2-resident by design",
-        "options": {"sort": bool(args.sort), "warp_agg": bool(args.warp_agg),
+        "options": {"sort": bool(args.sort),
+                    "warp_agg": ("adaptive" if args.warp_agg < 0 else bool(args.warp_agg)),
                     "staged": bool(args.staged), "blocks_per_sm": args.blocks_per_sm or "default"},
     }
 
@@ -302,7 +304,8 @@ def run_ours(args):
     pos, dest = workload(P, args.sigma_t, rank)
 
     mt = MeshTally(mesh, P, device=local, sort=bool(args.sort),
-                   warp_aggregate=bool(args.warp_agg), staged=bool(args.staged))
+                   warp_aggregate=None if args.warp_agg < 0 else bool(args.warp_agg),
+                   staged=bool(args.staged))
     if args.blocks_per_sm:
         mt.set_option(_lib.BT_OPT_BLOCKS_PER_SM, args.blocks_per_sm)
     d_pos = torch.from_numpy(pos).to(dev)

@@ -68,7 +68,9 @@ enum {
     BT_OPT_MAX_SWEEPS = 0,   /* sweep guard; <0 -> 2*E + 1000 (search.py:449-450) */
     BT_OPT_DIGEST = 1,       /* 1: record per-particle (element, face) digests */
     BT_OPT_SORT = 2,         /* 1: hand particles to warps in element order */
-    BT_OPT_WARP_AGG = 3,     /* 1: __match_any_sync aggregation of tally atomics */
+    BT_OPT_WARP_AGG = 3,     /* __match_any_sync aggregation of tally atomics:
+                                0 adaptive (default: when a warp's lanes score the same
+                                bins), 1 always, 2 never */
     BT_OPT_BLOCKS_PER_SM = 4, /* walk register budget: 1..3 resident 256-thread CTAs/SM */
     BT_OPT_STAGED = 5,        /* 1: compact flying particles + cp.async-prefetched refill */
     BT_OPT_MOVE_CHUNKS = 6,   /* host inputs: copy/walk pipeline depth (0 = auto, <= 16) */

@@ -80,6 +80,9 @@ enum { C_EVENTS = 0, C_REACHED, C_BOUNDARY, C_RECOV, C_KILLED, C_SWEEPS, C_ERR, 
 constexpr int MAX_CHUNKS = 16;
 constexpr int NDCOUNTERS = 48;
 
+// __match_any_sync aggregation of the tally atomics (BT_OPT_WARP_AGG)
+enum { WAGG_ADAPTIVE = 0, WAGG_ALWAYS = 1, WAGG_NEVER = 2 };
+
 struct WalkArgs {
     const ElemRec* __restrict__ rec;
     const Vtx* __restrict__ vtx;
@@ -104,7 +107,7 @@ struct WalkArgs {
     int64_t max_sweeps;
     int32_t ngroups;
     int32_t score;
-    int32_t wagg;    // __match_any_sync aggregation of tally atomics
+    int32_t wagg;    // tally atomics: WAGG_ADAPTIVE / WAGG_ALWAYS / WAGG_NEVER
 };
 
 __device__ __forceinline__ void load_tet(const WalkArgs& a, const ElemRec& r, Tet& T) {
@@ -210,7 +213,7 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
     load_tet(a, r, T);
     // the previous step's score and seg_total update, while this step's
     // vertex loads are in flight (warp-aggregated mode scores at loop level)
-    if (!a.wagg && P.has) {
+    if (P.has) {  // not taken by an aggregated flush at loop level
         atomicAdd(a.tally + P.bin, P.val);
         P.has = false;
     }
@@ -378,9 +381,11 @@ __device__ __forceinline__ void begin(Lane& L, const WalkArgs& a, const DigestSl
     L.outcome() = OUT_NONE;
 }
 
-__device__ __forceinline__ void score(const WalkArgs& a, bool has_score, int64_t bin, double val) {
+// all lanes: one atomic per distinct bin of the warp's pending scores
+__device__ __forceinline__ void score_aggregated(const WalkArgs& a, bool has_score, int64_t bin,
+                                                 double val) {
     constexpr unsigned FULL = 0xffffffffu;
-    if (a.wagg) {
+    {
         const int lane = threadIdx.x & 31;
         const unsigned m = __ballot_sync(FULL, has_score);
         if (has_score) {
@@ -398,16 +403,28 @@ __device__ __forceinline__ void score(const WalkArgs& a, bool has_score, int64_t
             }
             if (lane == leader) atomicAdd(a.tally + bin, sum);
         }
-    } else if (has_score) {
-        atomicAdd(a.tally + bin, val);
     }
 }
 
-// loop level, all lanes: warp-aggregated score of the pending segments, or the
-// plain atomic of lanes that went idle with one pending
+// Loop level, all lanes converged.  Pending scores are normally left for the
+// lane's next step to issue (after its loads, off the critical path).  They are
+// aggregated here instead when the warp's lanes are scoring the same bins:
+// always (WAGG_ALWAYS), or -- adaptive -- when a cheap probe (each lane's
+// pending bin against the next lane's) finds a duplicate, which is what a point
+// source with short flights produces (6x fewer contended atomics, measured in
+// profiles/r01_options.jsonl).  Idle lanes flush their pending score.
 __device__ __forceinline__ void flush_pending(const WalkArgs& a, Pending& P, bool idle) {
-    if (a.wagg) {
-        score(a, P.has, P.bin, P.val);
+    constexpr unsigned FULL = 0xffffffffu;
+    bool agg = a.wagg == WAGG_ALWAYS;
+    if (a.wagg == WAGG_ADAPTIVE) {
+        const int lane = threadIdx.x & 31;
+        const unsigned hm = __ballot_sync(FULL, P.has);
+        const long long nxt = __shfl_down_sync(FULL, (long long)P.bin, 1);
+        const bool dup = P.has && lane < 31 && ((hm >> (lane + 1)) & 1u) && nxt == P.bin;
+        agg = __any_sync(FULL, dup);
+    }
+    if (agg) {
+        score_aggregated(a, P.has, P.bin, P.val);
         P.has = false;
     } else if (idle && P.has) {
         atomicAdd(a.tally + P.bin, P.val);
@@ -1738,7 +1755,7 @@ struct bt_tally {
     int64_t max_sweeps = -1;
     bool opt_digest = false;
     bool opt_sort = false;
-    bool opt_wagg = false;
+    int opt_wagg = WAGG_ADAPTIVE;
     bool opt_staged = true;
     WorkSoA work{};
     void* work_mem = nullptr;
@@ -2127,7 +2144,11 @@ bt_status bt_set_option(bt_tally* h, int32_t key, int64_t value) {
                 h->sort_tmp_bytes = b;
             }
             break;
-        case BT_OPT_WARP_AGG: h->opt_wagg = value != 0; break;
+        case BT_OPT_WARP_AGG:
+            if (value < 0 || value > 2)
+                return set_err(BT_EINVAL, "warp aggregation must be 0 (adaptive), 1 or 2");
+            h->opt_wagg = (int)value;
+            break;
         case BT_OPT_BLOCKS_PER_SM: h->blocks_per_sm = (int)value; break;
         case BT_OPT_STAGED: h->opt_staged = value != 0; break;
         case BT_OPT_MOVE_CHUNKS: h->move_chunks = (int)value; break;
@@ -2206,7 +2227,7 @@ static WalkArgs walk_args(bt_tally* h, const double* dest, const int8_t* fly, co
     a.max_sweeps = h->max_sweeps >= 0 ? h->max_sweeps : 2 * h->ne + 1000;
     a.ngroups = h->ngroups;
     a.score = score ? 1 : 0;
-    a.wagg = h->opt_wagg ? 1 : 0;
+    a.wagg = h->opt_wagg;
     return a;
 }
 
@@ -2257,6 +2278,14 @@ static bt_status walk_enqueue(bt_tally* h, WalkArgs a, int64_t lo, int64_t hi, i
         W.px += lo; W.py += lo; W.pz += lo; W.dx += lo; W.dy += lo; W.dz += lo;
         W.w += lo; W.seg += lo; W.idx += lo; W.e += lo; W.g += lo; W.fl += lo;
         stage_kernel<<<grid_for(count, 256), 256, 0, h->stream>>>(a, W, nwork, lo, wsum);
+        CK(cudaGetLastError());
+        h->kernels += 1;
+    }
+    if (!staged && wsum) {  // the unstaged kernel has no stage pass to sum the weights in
+        CK(cudaMemsetAsync(h->dcounters + 15, 0, sizeof(unsigned long long), h->stream));
+        prepare_kernel<<<grid_for(count, 256), 256, 0, h->stream>>>(
+            a.fly_in + lo, h->element + lo, nullptr, h->ngroups, a.weight + lo, count,
+            h->dcounters + 15, wsum);
         CK(cudaGetLastError());
         h->kernels += 1;
     }

@@ -219,7 +219,7 @@ class MeshTally:
 
     def __init__(self, mesh, num_particles: int, num_groups: int = 1, threads: int = 1, *,
                  device: int = 0, localize: str = "grid", digest: bool = False,
-                 sort: bool = False, warp_aggregate: bool = False, staged: bool = True,
+                 sort: bool = False, warp_aggregate: bool | None = None, staged: bool = True,
                  move_chunks: int = 0):
         if isinstance(mesh, (str, Path)):
             mesh = read_tetmesh(mesh)
@@ -256,7 +256,9 @@ class MeshTally:
         _LIVE.add(self)
         self.set_option(_lib.BT_OPT_DIGEST, int(digest))
         self.set_option(_lib.BT_OPT_SORT, int(sort))
-        self.set_option(_lib.BT_OPT_WARP_AGG, int(warp_aggregate))
+        # None: adaptive (aggregate while a warp's lanes score the same bins)
+        self.set_option(_lib.BT_OPT_WARP_AGG,
+                        0 if warp_aggregate is None else (1 if warp_aggregate else 2))
         self.set_option(_lib.BT_OPT_STAGED, int(staged))
         self.set_option(_lib.BT_OPT_MOVE_CHUNKS, int(move_chunks))
         self._grid = TallyGrid(self)

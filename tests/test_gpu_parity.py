@@ -92,7 +92,8 @@ def test_walk_matches_reference_grid_localize(name):
 @pytest.mark.parametrize("opts", [dict(sort=True), dict(warp_aggregate=True),
                                   dict(staged=False), dict(staged=False, sort=True,
                                                            warp_aggregate=True),
-                                  dict(move_chunks=3), dict(move_chunks=16, warp_aggregate=True)])
+                                  dict(move_chunks=3), dict(move_chunks=16, warp_aggregate=True),
+                                  dict(warp_aggregate=False)])
 def test_walk_options_keep_parity(opts):
     _check_case(load_walk_case("c1_point_s2"), "grid", **opts)
     _check_case(load_walk_case("n6_uniform_g3"), "grid", **opts)
@@ -174,13 +175,15 @@ def test_full_size_c2_against_oracle(sigma_t):
     assert abs(tot - float((w * st.seg_total).sum())) <= 1e-9 * tot
 
 
-def test_device_pointer_path_equals_host_path():
+@pytest.mark.parametrize("opts", [{}, dict(sort=True), dict(staged=False),
+                                  dict(warp_aggregate=True), dict(warp_aggregate=False)])
+def test_device_pointer_path_equals_host_path(opts):
     torch = pytest.importorskip("torch")
     case = load_walk_case("n6_uniform_g3")
     b = case.batches[0]
     mv = b.moves[0]
-    host = MeshTally(case.mesh, case.capacity, case.num_groups, digest=True)
-    dev = MeshTally(case.mesh, case.capacity, case.num_groups, digest=True)
+    host = MeshTally(case.mesh, case.capacity, case.num_groups, digest=True, **opts)
+    dev = MeshTally(case.mesh, case.capacity, case.num_groups, digest=True, **opts)
     host.initialize_particle_location(b.init_positions)
     dev.initialize_particle_location(torch.from_numpy(b.init_positions).cuda())
     s1 = host.move_to_next_location(mv.dest, mv.flying, mv.weights, mv.groups)
@@ -194,6 +197,10 @@ def test_device_pointer_path_equals_host_path():
         assert np.array_equal(getattr(a, k), getattr(c, k))
     assert rel_close(host.batch_totals(), dev.batch_totals(), TALLY_RTOL)[0]
     assert host.source_weight == pytest.approx(dev.source_weight, rel=1e-14)
+    assert dev.source_weight > 0.0  # recorded on every device-input path
+    host.finalize_batch()
+    dev.finalize_batch()
+    assert rel_close(host.grid.sum, dev.grid.sum, TALLY_RTOL)[0]
 
 
 def test_error_behaviour():
