@@ -1260,9 +1260,20 @@ __global__ void flux_kernel(const double* __restrict__ sum, const double* __rest
 // ---------------------------------------------------------------------------
 // localization: uniform grid of element bounding boxes
 
-struct __align__(16) BoxF {
-    float lo[3], pad0, hi[3], pad1;  // element bbox, rounded outward
+// Barycentric pre-filter record of an element (64 bytes, fp32):
+// lambda_k(p) = w_k . (p - c) + lc_k for k = 1..3, lambda_0 = 1 - l1 - l2 - l3,
+// with w_k the rows of the inverse of [v1-v0 v2-v0 v3-v0] (fp64, then rounded)
+// and c the rounded centroid.  K bounds the reference's own rounding of its
+// Cramer quotients relative to sum|lambda| (1e-14 x the element's quality
+// ratio A^3/|det|); +inf for poorly conditioned or degenerate elements, whose
+// candidates always take the exact test.
+struct __align__(16) ElemLam {
+    float4 w1;  // w_1.xyz, lc_1
+    float4 w2;
+    float4 w3;
+    float4 c;   // c.xyz, K
 };
+static_assert(sizeof(ElemLam) == 64, "two 32-byte sectors per element");
 
 struct GridDev {
     double org[3];
@@ -1281,7 +1292,7 @@ __device__ __forceinline__ int grid_axis(double p, double org, double cs, int di
 __global__ void elem_cells_count_kernel(const ElemRec* __restrict__ rec,
                                         const Vtx* __restrict__ vtx, int64_t ne, GridDev G,
                                         int* __restrict__ counts, int4* __restrict__ ranges_lo,
-                                        int4* __restrict__ ranges_hi, BoxF* __restrict__ ebox) {
+                                        int4* __restrict__ ranges_hi) {
     int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= ne) return;
     const ElemRec r = rec[e];
@@ -1302,15 +1313,58 @@ __global__ void elem_cells_count_kernel(const ElemRec* __restrict__ rec,
         b[k] = grid_axis(hi[k] + delta, G.org[k], G.cs[k], G.dims[k]);
     }
     counts[e] = (b[0] - a[0] + 1) * (b[1] - a[1] + 1) * (b[2] - a[2] + 1);
-    BoxF bx;
-    for (int k = 0; k < 3; ++k) {
-        bx.lo[k] = __double2float_rd(lo[k] - delta);
-        bx.hi[k] = __double2float_ru(hi[k] + delta);
-    }
-    bx.pad0 = bx.pad1 = 0.f;
-    ebox[e] = bx;
     ranges_lo[e] = make_int4(a[0], a[1], a[2], 0);
     ranges_hi[e] = make_int4(b[0], b[1], b[2], 0);
+}
+
+__global__ void elem_lambda_kernel(const ElemRec* __restrict__ rec, const Vtx* __restrict__ vtx,
+                                   int64_t ne, ElemLam* __restrict__ lam) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= ne) return;
+    const ElemRec r = rec[e];
+    double x[4], y[4], z[4];
+    for (int j = 0; j < 4; ++j) {
+        const Vtx v = vtx[r.v[j]];
+        x[j] = v.x;
+        y[j] = v.y;
+        z[j] = v.z;
+    }
+    double a[3][3];  // a[k] = v_{k+1} - v0
+    for (int k = 0; k < 3; ++k) {
+        a[k][0] = x[k + 1] - x[0];
+        a[k][1] = y[k + 1] - y[0];
+        a[k][2] = z[k + 1] - z[0];
+    }
+    auto cross = [](const double* u, const double* v, double* o) {
+        o[0] = u[1] * v[2] - u[2] * v[1];
+        o[1] = u[2] * v[0] - u[0] * v[2];
+        o[2] = u[0] * v[1] - u[1] * v[0];
+    };
+    double n[3][3];
+    cross(a[1], a[2], n[0]);  // w_1 * det
+    cross(a[2], a[0], n[1]);  // w_2 * det
+    cross(a[0], a[1], n[2]);  // w_3 * det
+    const double det = a[0][0] * n[0][0] + a[0][1] * n[0][1] + a[0][2] * n[0][2];
+    double A = 0.0;
+    for (int k = 0; k < 3; ++k) A = fmax(A, fabs(a[k][0]) + fabs(a[k][1]) + fabs(a[k][2]));
+    const double q = A * A * A / fabs(det);
+    const float cx = (float)((x[0] + x[1] + x[2] + x[3]) * 0.25);
+    const float cy = (float)((y[0] + y[1] + y[2] + y[3]) * 0.25);
+    const float cz = (float)((z[0] + z[1] + z[2] + z[3]) * 0.25);
+    float4 w[3];
+    for (int k = 0; k < 3; ++k) {
+        const double wx = n[k][0] / det, wy = n[k][1] / det, wz = n[k][2] / det;
+        const double lc = wx * ((double)cx - x[0]) + wy * ((double)cy - y[0]) +
+                          wz * ((double)cz - z[0]);
+        w[k] = make_float4((float)wx, (float)wy, (float)wz, (float)lc);
+    }
+    const float K = (q <= 1e6) ? __double2float_ru(1e-14 * q) : INFINITY;  // NaN q -> inf
+    ElemLam L;
+    L.w1 = w[0];
+    L.w2 = w[1];
+    L.w3 = w[2];
+    L.c = make_float4(cx, cy, cz, K);
+    lam[e] = L;
 }
 
 __global__ void elem_cells_emit_kernel(int64_t ne, GridDev G, const int* __restrict__ offs,
@@ -1350,7 +1404,7 @@ __global__ void cell_start_kernel(const unsigned long long* __restrict__ keys, i
 struct LocateArgs {
     const ElemRec* __restrict__ rec;
     const Vtx* __restrict__ vtx;
-    const BoxF* __restrict__ ebox;
+    const ElemLam* __restrict__ lam;
     GridDev G;
     const double* __restrict__ target;  // (count,3)
     double* __restrict__ pos;
@@ -1366,13 +1420,56 @@ struct LocateArgs {
     int64_t lo;  // locate_grid_kernel: first particle of this launch
 };
 
+// elem_contains(p, EPS_BARY) (geometry.py:149-154) decided from the element's
+// fp32 barycentric record: +1 certainly contained, -1 certainly not, 0 unsure
+// (run the exact-equivalent test).  Error of lambda_k^f against the exact
+// barycentric of the reference's fp64 vectors: the point's rounding to fp32
+// (u T_k, T_k = sum|w_ki||p_i|), d = p - c and the FMA chain (<= 4 u S_k,
+// S_k = sum|w_ki||d_i|), w's rounding (1.01 u S_k) and lc's (u|lc_k|); lambda_0
+// adds three subtractions.  The reference's own quotients differ from the
+// exact barycentrics by <= K sum|lambda| (K from the element's conditioning).
+// Decisions need 1.25x that margin beyond -EPS_BARY.
+__device__ __forceinline__ int lambda_prefilter(const ElemLam* __restrict__ L, float q0, float q1,
+                                                float q2) {
+    constexpr float u = 5.9604645e-8f;
+    const float4 W1 = __ldg(&L->w1), W2 = __ldg(&L->w2), W3 = __ldg(&L->w3), C = __ldg(&L->c);
+    const float d0 = q0 - C.x, d1 = q1 - C.y, d2 = q2 - C.z;
+    const float ad0 = fabsf(d0), ad1 = fabsf(d1), ad2 = fabsf(d2);
+    const float ap0 = fabsf(q0), ap1 = fabsf(q1), ap2 = fabsf(q2);
+    float l[3], e[3];
+    const float4 Ws[3] = {W1, W2, W3};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float4 W = Ws[k];
+        l[k] = __fmaf_rn(W.x, d0, __fmaf_rn(W.y, d1, __fmaf_rn(W.z, d2, W.w)));
+        const float S = __fmaf_rn(fabsf(W.x), ad0, __fmaf_rn(fabsf(W.y), ad1, fabsf(W.z) * ad2));
+        const float T = __fmaf_rn(fabsf(W.x), ap0, __fmaf_rn(fabsf(W.y), ap1, fabsf(W.z) * ap2));
+        e[k] = u * __fmaf_rn(1.02f, T, __fmaf_rn(5.1f, S, 4.1f * fabsf(W.w)));
+    }
+    const float l0 = ((1.0f - l[0]) - l[1]) - l[2];
+    const float sl = fabsf(l[0]) + fabsf(l[1]) + fabsf(l[2]);
+    const float ref = C.w * (1.0f + sl + fabsf(l0));  // K * sum|lambda|, inf when K is
+    const float e0 = e[0] + e[1] + e[2] + 3.03f * u * (1.0f + sl);
+    constexpr float tol = (float)EPS_BARY;
+    bool pass = true, fail = false;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float lk = k == 0 ? l0 : l[k - 1];
+        const float m = 1.25f * ((k == 0 ? e0 : e[k - 1]) + ref);
+        pass &= lk + tol > m;
+        fail |= lk + tol < -m;
+    }
+    return fail ? -1 : (pass ? 1 : 0);
+}
+
 // Warp-parallel grid search (the north star's localization kernel): a group
 // of G lanes serves one particle (32/G particles per warp).  The group's
 // lanes take G of the cell's candidates at a time -- ascending element ids --
-// so the candidate, bounding-box and vertex gathers of one particle are in
-// flight together instead of one after another; candidates whose float box
-// (rounded outward, expanded like the grid insertion) holds the point run
-// the exact-equivalent containment filter.  The lowest lane with a hit in
+// so the candidates' gathers of one particle are in flight together instead
+// of one after another.  Each candidate is decided from its 64-byte fp32
+// barycentric record (lambda_prefilter, no vertex gathers); only candidates
+// within rounding distance of a face run the exact-equivalent containment
+// filter on the fp64 vertices.  The lowest lane with a hit in
 // the first chunk that has one is the lowest-id containing element
 // (pkg/tests/oracles.py:36-57 semantics), for every G.
 constexpr int LOCATE_THREADS = 256;
@@ -1393,6 +1490,7 @@ __global__ void __launch_bounds__(LOCATE_THREADS) locate_grid_kernel(const Locat
     }
     const bool inside = valid && p0 >= a.bbox[0] && p0 <= a.bbox[3] && p1 >= a.bbox[1] &&
                         p1 <= a.bbox[4] && p2 >= a.bbox[2] && p2 <= a.bbox[5];
+    const float q0 = __double2float_rn(p0), q1 = __double2float_rn(p1), q2 = __double2float_rn(p2);
     int s0 = 0, s1 = 0;
     if (inside) {
         const int ci = grid_axis(p0, a.G.org[0], a.G.cs[0], a.G.dims[0]);
@@ -1412,9 +1510,9 @@ __global__ void __launch_bounds__(LOCATE_THREADS) locate_grid_kernel(const Locat
         const int k = k0 + gl;
         if (act && k < s1) {
             c = __ldg(a.G.cand + k);
-            const float4 lo = __ldg(reinterpret_cast<const float4*>(a.ebox + c));
-            const float4 hi = __ldg(reinterpret_cast<const float4*>(a.ebox + c) + 1);
-            if (!(p0 < lo.x || p0 > hi.x || p1 < lo.y || p1 > hi.y || p2 < lo.z || p2 > hi.z)) {
+            const int pre = lambda_prefilter(a.lam + c, q0, q1, q2);
+            hit = pre > 0;
+            if (pre == 0) {
                 const ElemRec r = load_rec(a.rec, c);
                 Tet T;
 #pragma unroll
@@ -1671,6 +1769,8 @@ struct bt_tally {
     int num_sms = 148;
     cudaStream_t stream = nullptr;   // kernels
     cudaStream_t cstream = nullptr;  // host-to-device copies (overlap with kernels)
+    cudaStream_t stream2 = nullptr;  // odd chunks of a pipelined move (overlap the tails)
+    cudaEvent_t ev_s1 = nullptr, ev_s2 = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
     cudaEvent_t evc0 = nullptr, evc1 = nullptr, ev_loc = nullptr;
     cudaEvent_t evchunk[MAX_CHUNKS] = {};
@@ -1686,7 +1786,7 @@ struct bt_tally {
     GridDev grid{};
     int* cell_start = nullptr;
     int* cand = nullptr;
-    BoxF* ebox = nullptr;
+    ElemLam* lam = nullptr;
     int64_t grid_m = 0;
     // particles (persistent)
     double* pos = nullptr;
@@ -1779,7 +1879,7 @@ static bt_status ensure_device(bt_tally* h) {
     } while (0)
 
 static bt_status free_all(bt_tally* h) {
-    void* ptrs[] = {h->rec, h->vtx, h->cell_start, h->cand, h->ebox, h->pos, h->element, h->alive,
+    void* ptrs[] = {h->rec, h->vtx, h->cell_start, h->cand, h->lam, h->pos, h->element, h->alive,
                     h->entry, h->stuck, h->outcome, h->seg_total, h->group, h->dest, h->fly,
                     h->weight, h->digest, h->dcount, h->order, h->sort_keys_in,
                     h->sort_keys_out, h->sort_vals_in, h->sort_tmp, h->tally, h->sum,
@@ -1802,6 +1902,9 @@ static bt_status free_all(bt_tally* h) {
         if (e) cudaEventDestroy(e);
     if (h->stream) cudaStreamDestroy(h->stream);
     if (h->cstream) cudaStreamDestroy(h->cstream);
+    if (h->stream2) cudaStreamDestroy(h->stream2);
+    if (h->ev_s1) cudaEventDestroy(h->ev_s1);
+    if (h->ev_s2) cudaEventDestroy(h->ev_s2);
     return BT_OK;
 }
 
@@ -1849,10 +1952,11 @@ static bt_status build_grid(bt_tally* h) {
     TRY(dalloc(&rlo, h->ne));
     TRY(dalloc(&rhi, h->ne));
     CK(cudaMemsetAsync(counts + h->ne, 0, sizeof(int), h->stream));
-    TRY(dalloc(&h->ebox, h->ne));
+    TRY(dalloc(&h->lam, h->ne));
     elem_cells_count_kernel<<<grid_for(h->ne, 256), 256, 0, h->stream>>>(h->rec, h->vtx, h->ne,
-                                                                         G, counts, rlo, rhi,
-                                                                         h->ebox);
+                                                                         G, counts, rlo, rhi);
+    CK(cudaGetLastError());
+    elem_lambda_kernel<<<grid_for(h->ne, 256), 256, 0, h->stream>>>(h->rec, h->vtx, h->ne, h->lam);
     CK(cudaGetLastError());
     size_t tmp_bytes = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, offs, (int)(h->ne + 1),
@@ -2037,6 +2141,9 @@ bt_status bt_create(const double* vertices, int64_t num_vertices, const int32_t*
     CKF(cudaEventCreate(&h->ev2));
     CKF(cudaEventCreate(&h->ev3));
     CKF(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
+    CKF(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
+    CKF(cudaEventCreateWithFlags(&h->ev_s1, cudaEventDisableTiming));
+    CKF(cudaEventCreateWithFlags(&h->ev_s2, cudaEventDisableTiming));
     CKF(cudaEventCreateWithFlags(&h->evc0, cudaEventDisableTiming));
     CKF(cudaEventCreateWithFlags(&h->evc1, cudaEventDisableTiming));
     CKF(cudaEventCreateWithFlags(&h->ev_loc, cudaEventDisableTiming));
@@ -2241,19 +2348,20 @@ static bt_status walk_begin(bt_tally* h) {
 // enqueue stage + walk of particles [lo, hi) as chunk `chunk` (staged path),
 // or the whole range with the v1 kernel / element-sorted hand-out
 static bt_status walk_enqueue(bt_tally* h, WalkArgs a, int64_t lo, int64_t hi, int chunk,
-                              double* wsum) {
+                              double* wsum, cudaStream_t st = nullptr) {
+    if (!st) st = h->stream;
     const int64_t count = hi - lo;
     a.count = count;
     a.queue = h->dcounters + 16 + chunk;
     const bool staged = h->opt_staged;
     if (h->opt_sort && a.score) {  // whole move only (lo == 0)
-        iota_keys_kernel<<<grid_for(count, 256), 256, 0, h->stream>>>(
+        iota_keys_kernel<<<grid_for(count, 256), 256, 0, st>>>(
             h->element, count, h->sort_keys_in, h->sort_vals_in);
         CK(cudaGetLastError());
         size_t b = h->sort_tmp_bytes;
         CK(cub::DeviceRadixSort::SortPairs(h->sort_tmp, b, h->sort_keys_in, h->sort_keys_out,
                                            h->sort_vals_in, h->order, (int)count, 0, 32,
-                                           h->stream));
+                                           st));
         a.order = h->order;
         h->kernels += 5;
     }
@@ -2277,26 +2385,26 @@ static bt_status walk_enqueue(bt_tally* h, WalkArgs a, int64_t lo, int64_t hi, i
         W = h->work;
         W.px += lo; W.py += lo; W.pz += lo; W.dx += lo; W.dy += lo; W.dz += lo;
         W.w += lo; W.seg += lo; W.idx += lo; W.e += lo; W.g += lo; W.fl += lo;
-        stage_kernel<<<grid_for(count, 256), 256, 0, h->stream>>>(a, W, nwork, lo, wsum);
+        stage_kernel<<<grid_for(count, 256), 256, 0, st>>>(a, W, nwork, lo, wsum);
         CK(cudaGetLastError());
         h->kernels += 1;
     }
     if (!staged && wsum) {  // the unstaged kernel has no stage pass to sum the weights in
-        CK(cudaMemsetAsync(h->dcounters + 15, 0, sizeof(unsigned long long), h->stream));
-        prepare_kernel<<<grid_for(count, 256), 256, 0, h->stream>>>(
+        CK(cudaMemsetAsync(h->dcounters + 15, 0, sizeof(unsigned long long), st));
+        prepare_kernel<<<grid_for(count, 256), 256, 0, st>>>(
             a.fly_in + lo, h->element + lo, nullptr, h->ngroups, a.weight + lo, count,
             h->dcounters + 15, wsum);
         CK(cudaGetLastError());
         h->kernels += 1;
     }
     if (h->walk_first) {
-        CK(cudaEventRecord(h->ev0, h->stream));
+        CK(cudaEventRecord(h->ev0, st));
         h->walk_first = false;
     }
     if (staged)
-        V.staged<<<blocks, V.threads, dyn, h->stream>>>(a, W, nwork);
+        V.staged<<<blocks, V.threads, dyn, st>>>(a, W, nwork);
     else
-        V.plain<<<blocks, V.threads, 0, h->stream>>>(a);
+        V.plain<<<blocks, V.threads, 0, st>>>(a);
     CK(cudaGetLastError());
     h->kernels += 1;
     return BT_OK;
@@ -2366,7 +2474,7 @@ static LocateArgs locate_args(bt_tally* h, const double* target, int64_t count) 
     LocateArgs a;
     a.rec = h->rec;
     a.vtx = h->vtx;
-    a.ebox = h->ebox;
+    a.lam = h->lam;
     a.G = h->grid;
     a.target = target;
     a.pos = h->pos;
@@ -2509,17 +2617,31 @@ bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, cons
     }
     bt_status s;
     if (host) {
-        // pipeline: chunk c's input copies (copy stream) overlap chunk c-1's walk
+        // pipeline: chunk c's input copies (copy stream) overlap chunk c-1's walk.
+        // Chunks grow geometrically (1/2^nch, then 1/2^(nch-1-c) cumulative:
+        // 1/8, 3/8, 1/2 for three) so the first walk starts after a short copy
+        // and every later copy still finishes inside the previous chunk's walk.
         WalkArgs a = walk_args(h, h->dest, h->fly, h->weight, true);
         int nch = 1;
         if (h->opt_staged && !h->opt_sort) {
-            nch = h->move_chunks > 0 ? h->move_chunks : (count >= (4 << 20) ? 4 : 1);
+            nch = h->move_chunks > 0 ? h->move_chunks : (count >= (4 << 20) ? 3 : 1);
             nch = (int)std::min<int64_t>(std::min(nch, MAX_CHUNKS), count);
         }
+        auto bound = [&](int c) -> int64_t {  // end of chunk c
+            if (c + 1 >= nch) return count;
+            const int sh = c == 0 ? nch : nch - 1 - c;
+            return (int64_t)((double)count / (double)(1ll << sh));
+        };
         TRY(walk_begin(h));
+        // odd chunks go to a second stream, so chunk c+1's CTAs take the SMs
+        // that chunk c's tail frees instead of waiting for its last walk
+        CK(cudaEventRecord(h->ev_s1, h->stream));
+        CK(cudaStreamWaitEvent(h->stream2, h->ev_s1, 0));
         for (int c = 0; c < nch; ++c) {
-            const int64_t lo = count * c / nch, hi = count * (c + 1) / nch;
+            const int64_t lo = c == 0 ? 0 : bound(c - 1), hi = bound(c);
             const int64_t n = hi - lo;
+            if (n <= 0) continue;
+            cudaStream_t st = (c & 1) ? h->stream2 : h->stream;
             CK(cudaMemcpyAsync(h->dest + 3 * lo, destinations + 3 * lo, sizeof(double) * 3 * n,
                                cudaMemcpyHostToDevice, h->cstream));
             CK(cudaMemcpyAsync(h->fly + lo, flying + lo, n, cudaMemcpyHostToDevice, h->cstream));
@@ -2529,9 +2651,11 @@ bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, cons
                 CK(cudaMemcpyAsync(h->group + lo, groups + lo, sizeof(int32_t) * n,
                                    cudaMemcpyHostToDevice, h->cstream));
             CK(cudaEventRecord(h->evchunk[c], h->cstream));
-            CK(cudaStreamWaitEvent(h->stream, h->evchunk[c], 0));
-            TRY(walk_enqueue(h, a, lo, hi, c, nullptr));
+            CK(cudaStreamWaitEvent(st, h->evchunk[c], 0));
+            TRY(walk_enqueue(h, a, lo, hi, c, nullptr, st));
         }
+        CK(cudaEventRecord(h->ev_s2, h->stream2));
+        CK(cudaStreamWaitEvent(h->stream, h->ev_s2, 0));
         s = walk_end(h, a.max_sweeps, summary, ov);
         if (need_w) h->source_weight = job.out;
     } else {

@@ -141,6 +141,48 @@ def test_grid_localize_random_meshes(lanes):
         mt.set_option(_lib.BT_OPT_LOCATE_LANES, 3)
 
 
+@pytest.mark.parametrize("scale,offset", [(1.0, 0.0), (1e-2, 1e4), (1e3, -5e5)])
+def test_grid_localize_boundary_points(scale, offset):
+    """Points on mesh vertices, edges, faces and within 1e-11 (relative) of
+    them, on scaled/translated cubes and the torus shell: the fp32 barycentric
+    pre-filter must hand every borderline candidate to the exact test."""
+    from paper_2504_19048_b200 import TetMesh, build_torus_shell_mesh
+    gen = np.random.default_rng(17)
+    m0 = build_cube_mesh(7)
+    meshes = [TetMesh.from_arrays(m0.vertices * scale + offset, m0.elements)]
+    if scale == 1.0:
+        meshes.append(build_torus_shell_mesh(2, 8, 12))
+    for m in meshes:
+        V, E = m.vertices, m.elements
+        k = 6000
+        el = gen.integers(0, E.shape[0], k)
+        bc = gen.dirichlet(np.ones(4), k)
+        kind = gen.integers(0, 4, k)          # 0 vertex, 1 edge, 2 face, 3 interior
+        bc[kind == 0] = np.eye(4)[gen.integers(0, 4, (kind == 0).sum())]
+        for sel, nz in ((kind == 1, 2), (kind == 2, 3)):
+            idx = np.where(sel)[0]
+            for i in idx:
+                keep = gen.choice(4, nz, replace=False)
+                b = np.zeros(4)
+                b[keep] = gen.dirichlet(np.ones(nz))
+                bc[i] = b
+        pts = np.einsum("ij,ijk->ik", bc, V[E[el]])
+        near = gen.random(k) < 0.3
+        span = np.ptp(V, axis=0).max()
+        pts[near] += gen.normal(size=(near.sum(), 3)) * 1e-11 * span
+        mt = MeshTally(m, k)
+        mt.initialize_particle_location(pts)
+        st = mt.read_particles()
+        # points outside the (inclusive) bounding box are not searched by the
+        # reference (search.py:574-583), even when within EPS_BARY of a face
+        bb = m.bounding_box
+        inside = ((pts >= bb[0]) & (pts <= bb[1])).all(axis=1)
+        assert (~inside).any()  # the set does probe that rule
+        expect = np.where(inside, orc.locate_exhaustive(m, pts), -1)
+        assert np.array_equal(st.element, expect)
+        mt.close()
+
+
 @pytest.mark.parametrize("sigma_t", [2.0, 100.0])
 def test_full_size_c2_against_oracle(sigma_t):
     """C2 mesh (998,250 tets); 2e5 particles checked exhaustively against the
