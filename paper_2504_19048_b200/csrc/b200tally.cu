@@ -153,6 +153,12 @@ __shared__ int s_lane_g[MAX_CTA_THREADS];
 __shared__ double s_lane_d[3][MAX_CTA_THREADS];  // destination
 __shared__ int8_t s_lane_outcome[MAX_CTA_THREADS];
 __shared__ int8_t s_lane_alive[MAX_CTA_THREADS];
+#ifndef BT_TET_SHARED
+#define BT_TET_SHARED 0
+#endif
+#if BT_TET_SHARED
+__shared__ Tet s_lane_tet[MAX_CTA_THREADS];  // the current element's vertices
+#endif
 
 // one particle's walk state while it flies
 struct Lane {
@@ -209,8 +215,17 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
                                           const DigestSlot& DS) {
     const ElemRec r = L.have_nr ? L.nr : load_rec(a.rec, L.e);
     L.have_nr = false;
+#if BT_TET_SHARED
+    Tet& T = s_lane_tet[threadIdx.x];
+    {
+        Tet Tl;
+        load_tet(a, r, Tl);
+        T = Tl;
+    }
+#else
     Tet T;
     load_tet(a, r, T);
+#endif
     // the previous step's score and seg_total update, while this step's
     // vertex loads are in flight (warp-aggregated mode scores at loop level)
     if (P.has) {  // not taken by an aggregated flush at loop level
