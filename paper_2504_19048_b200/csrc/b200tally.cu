@@ -153,12 +153,6 @@ __shared__ int s_lane_g[MAX_CTA_THREADS];
 __shared__ double s_lane_d[3][MAX_CTA_THREADS];  // destination
 __shared__ int8_t s_lane_outcome[MAX_CTA_THREADS];
 __shared__ int8_t s_lane_alive[MAX_CTA_THREADS];
-#ifndef BT_TET_SHARED
-#define BT_TET_SHARED 0
-#endif
-#if BT_TET_SHARED
-__shared__ Tet s_lane_tet[MAX_CTA_THREADS];  // the current element's vertices
-#endif
 
 // one particle's walk state while it flies
 struct Lane {
@@ -194,6 +188,7 @@ struct DigestSlot {
 enum { SC_REACHED = 0, SC_BOUNDARY, SC_RECOV, SC_KILLED, SC_MAXIT, SC_ERR, SC_N };
 struct Counters {
     unsigned events = 0;
+    unsigned maxit = 0;      // longest walk (sweeps) finished by this lane
     unsigned* sh = nullptr;  // SC_N shared counters of the CTA
 };
 
@@ -211,21 +206,14 @@ struct Pending {
 // particle stops (reached, leaked, stuck-killed or sweep guard).  When DEFER
 // the segment is left in P (scored by the next step or the loop); otherwise
 // has_score/bin/val are set for an immediate score.
+// DIG = false compiles the per-particle digest bookkeeping out of the loop.
+template <bool DIG = true>
 __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& C, Pending& P,
                                           const DigestSlot& DS) {
     const ElemRec r = L.have_nr ? L.nr : load_rec(a.rec, L.e);
     L.have_nr = false;
-#if BT_TET_SHARED
-    Tet& T = s_lane_tet[threadIdx.x];
-    {
-        Tet Tl;
-        load_tet(a, r, Tl);
-        T = Tl;
-    }
-#else
     Tet T;
     load_tet(a, r, T);
-#endif
     // the previous step's score and seg_total update, while this step's
     // vertex loads are in flight (warp-aggregated mode scores at loop level)
     if (P.has) {  // not taken by an aggregated flush at loop level
@@ -253,10 +241,11 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
     bool exact_used, need_t;
     int kind = exit_search_fast(T, ox, oy, oz, L.dx(), L.dy(), L.dz(), L.entry, &face, &t, &exact_used,
                                 true, &need_t);
+    // (neighbour << 2) | its face across the exit face, -1 on the boundary
+    const int nbp = face == 0 ? r.nb[0] : face == 1 ? r.nb[1] : face == 2 ? r.nb[2] : r.nb[3];
     if (kind == 1) {
         // issue the next element's record load now: it lands while the exact
         // t division and the commit below run
-        const int nbp = face == 0 ? r.nb[0] : face == 1 ? r.nb[1] : face == 2 ? r.nb[2] : r.nb[3];
         if (nbp >= 0) {
             L.nr = load_rec(a.rec, nbp >> 2);
             L.have_nr = true;
@@ -310,7 +299,7 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
     if (event) {  // search.py:236-274
         ++C.events;
         L.st = 0;
-        if (a.digest) {
+        if (DIG && a.digest) {
             *DS.d = (*DS.d ^ (uint64_t)((int64_t)L.e * 8 + face + 1)) * DIGEST_PRIME;
             ++*DS.c;
         }
@@ -341,7 +330,6 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
             atomicAdd(C.sh + SC_REACHED, 1u);
             done = true;
         } else {
-            const int nbp = face == 0 ? r.nb[0] : face == 1 ? r.nb[1] : face == 2 ? r.nb[2] : r.nb[3];
             if (nbp < 0) {
                 L.outcome() = OUT_LEAKED;
                 L.alive() = 0;
@@ -365,6 +353,7 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
     return done;
 }
 
+template <bool DIG = true>
 __device__ __forceinline__ void finish(const WalkArgs& a, Lane& L, Counters& C,
                                        const DigestSlot& DS) {
     const int64_t i = L.idx();
@@ -377,18 +366,19 @@ __device__ __forceinline__ void finish(const WalkArgs& a, Lane& L, Counters& C,
     a.outcome[i] = (int8_t)L.outcome();
     a.alive[i] = (int8_t)L.alive();
     a.seg_total[i] = L.seg();
-    if (a.digest) {
+    if (DIG && a.digest) {
         a.digest[i] = *DS.d;
         a.dcount[i] = *DS.c;
     }
-    atomicMax(C.sh + SC_MAXIT, (unsigned)L.iters);
+    C.maxit = max(C.maxit, (unsigned)L.iters);
     L.busy = false;
 }
 
+template <bool DIG = true>
 __device__ __forceinline__ void begin(Lane& L, const WalkArgs& a, const DigestSlot& DS) {
     L.have_nr = false;
     L.iters = 0;
-    if (a.digest) {
+    if (DIG && a.digest) {
         *DS.d = DIGEST_INIT;
         *DS.c = 0;
     }
@@ -457,6 +447,8 @@ __device__ __forceinline__ void flush_counters(const WalkArgs& a, Counters& C) {
     constexpr unsigned FULL = 0xffffffffu;
     const unsigned ev = __reduce_add_sync(FULL, C.events);
     if ((threadIdx.x & 31) == 0 && ev) atomicAdd(a.counters + C_EVENTS, (unsigned long long)ev);
+    const unsigned mx = __reduce_max_sync(FULL, C.maxit);
+    if ((threadIdx.x & 31) == 0 && mx) atomicMax(C.sh + SC_MAXIT, mx);
     __syncthreads();
     if (threadIdx.x == 0) {
         const unsigned* sh = C.sh;
@@ -550,10 +542,12 @@ __global__ void __launch_bounds__(THREADS, MINB) walk_kernel(const WalkArgs a) {
 struct WorkSoA {
     double *px, *py, *pz, *dx, *dy, *dz, *w, *seg;
     int *idx, *e, *g, *fl;  // fl = entry (low byte, signed) | stuck << 8
+    int4 *r0, *r1;          // the starting element's record (vertex ids | adjacency)
 };
 
 struct __align__(16) WarpStage {
     double px[32], py[32], pz[32], dx[32], dy[32], dz[32], w[32], seg[32];
+    int4 r0[32], r1[32];
     int idx[32], e[32], g[32], fl[32];
 };
 
@@ -565,6 +559,10 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
@@ -593,12 +591,14 @@ __device__ __forceinline__ int claim_chunk(const WalkArgs& a, const WorkSoA& W, 
         cp_async4(&st.e[lane], W.e + k);
         cp_async4(&st.g[lane], W.g + k);
         cp_async4(&st.fl[lane], W.fl + k);
+        cp_async16(&st.r0[lane], W.r0 + k);
+        cp_async16(&st.r1[lane], W.r1 + k);
     }
     cp_async_commit();
     return n;
 }
 
-template <int THREADS, int MINB>
+template <int THREADS, int MINB, bool DIG>
 __global__ void __launch_bounds__(THREADS, MINB)
     walk_staged_kernel(const WalkArgs a, const WorkSoA W, const int64_t* __restrict__ nwork_p) {
     static_assert(THREADS <= MAX_CTA_THREADS, "one shared lane slot per thread");
@@ -660,8 +660,13 @@ __global__ void __launch_bounds__(THREADS, MINB)
                     const int fl = s.fl[j];
                     L.entry = (int)(signed char)(fl & 0xff);
                     L.st = (fl >> 8) & 0xff;
-                    begin(L, a, DS);
+                    begin<DIG>(L, a, DS);
                     L.alive() = (int)(signed char)((fl >> 16) & 0xff);
+                    // the first step's record came with the stage: no dependent load
+                    const int4 q0 = s.r0[j], q1 = s.r1[j];
+                    L.nr.v[0] = q0.x; L.nr.v[1] = q0.y; L.nr.v[2] = q0.z; L.nr.v[3] = q0.w;
+                    L.nr.nb[0] = q1.x; L.nr.nb[1] = q1.y; L.nr.nb[2] = q1.z; L.nr.nb[3] = q1.w;
+                    L.have_nr = true;
                 }
             }
             head += take;
@@ -672,7 +677,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
             break;
         }
         if (L.busy) {
-            if (walk_step(a, L, C, P, DS)) finish(a, L, C, DS);
+            if (walk_step<DIG>(a, L, C, P, DS)) finish<DIG>(a, L, C, DS);
         }
         flush_pending(a, P, !L.busy);
     }
@@ -731,6 +736,9 @@ __global__ void stage_kernel(const WalkArgs a, const WorkSoA W, int64_t* __restr
     W.g[k] = a.score ? a.group[i] : 0;
     W.fl[k] = ((int)(unsigned char)a.entry[i]) | ((int)(unsigned char)a.stuck[i] << 8) |
               ((int)(unsigned char)(a.alive[i] | a.fly_in[i]) << 16);  // load_step: alive |= flying
+    const int4* rp = reinterpret_cast<const int4*>(a.rec + a.element[i]);
+    W.r0[k] = __ldg(rp);
+    W.r1[k] = __ldg(rp + 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -919,7 +927,7 @@ __global__ void __launch_bounds__(THREADS, MINB) transport_kernel(const Transpor
                 ++rounds;
                 need_flight = false;
             }
-            if (walk_step(a, L, C, P, DS)) {
+            if (walk_step<false>(a, L, C, P, DS)) {
                 // flight over: its walk took L.iters sweeps in round `rounds`
                 if (rounds <= MAX_ROUNDS_TRACKED) atomicMax(t.round_max + rounds - 1, (unsigned)L.iters);
                 bool stop = true;
@@ -2289,13 +2297,15 @@ static bt_status ensure_work(bt_tally* h) {
     if (h->work_mem) return BT_OK;
     const size_t n = (size_t)h->cap;
     char* p = nullptr;
-    CK(cudaMalloc((void**)&p, n * (8 * sizeof(double) + 4 * sizeof(int)) + 256));
+    CK(cudaMalloc((void**)&p, n * (8 * sizeof(double) + 2 * sizeof(int4) + 4 * sizeof(int)) + 256));
     h->work_mem = p;
     WorkSoA& W = h->work;
     double* d = reinterpret_cast<double*>(p);
     W.px = d; W.py = d + n; W.pz = d + 2 * n; W.dx = d + 3 * n; W.dy = d + 4 * n;
     W.dz = d + 5 * n; W.w = d + 6 * n; W.seg = d + 7 * n;
-    int* q = reinterpret_cast<int*>(d + 8 * n);
+    int4* r = reinterpret_cast<int4*>(d + 8 * n);
+    W.r0 = r; W.r1 = r + n;
+    int* q = reinterpret_cast<int*>(r + 2 * n);
     W.idx = q; W.e = q + n; W.g = q + 2 * n; W.fl = q + 3 * n;
     return BT_OK;
 }
@@ -2310,16 +2320,17 @@ struct HostOverlap {
 static const struct Variant {
     int threads;
     void (*plain)(const WalkArgs);
-    void (*staged)(const WalkArgs, const WorkSoA, const int64_t*);
+    void (*staged)(const WalkArgs, const WorkSoA, const int64_t*);      // digests off
+    void (*staged_dig)(const WalkArgs, const WorkSoA, const int64_t*);  // digests on
 } kVariants[] = {
     // launch variant (CTA size, resident CTAs per SM = register budget);
     // BT_OPT_BLOCKS_PER_SM selects it, 0 = the tuned default
-    {256, walk_kernel<256, 1>, walk_staged_kernel<256, 1>},  // 1: <=255 regs
-    {256, walk_kernel<256, 2>, walk_staged_kernel<256, 2>},  // 2: <=128 regs
-    {256, walk_kernel<256, 3>, walk_staged_kernel<256, 3>},  // 3: <=80 regs
-    {128, walk_kernel<128, 3>, walk_staged_kernel<128, 3>},  // 4: <=168 regs
-    {128, walk_kernel<128, 4>, walk_staged_kernel<128, 4>},  // 5: <=128 regs
-    {192, walk_kernel<192, 2>, walk_staged_kernel<192, 2>},  // 6: <=168 regs
+    {256, walk_kernel<256, 1>, walk_staged_kernel<256, 1, false>, walk_staged_kernel<256, 1, true>},  // 1: <=255 regs
+    {256, walk_kernel<256, 2>, walk_staged_kernel<256, 2, false>, walk_staged_kernel<256, 2, true>},  // 2: <=128 regs
+    {256, walk_kernel<256, 3>, walk_staged_kernel<256, 3, false>, walk_staged_kernel<256, 3, true>},  // 3: <=80 regs
+    {128, walk_kernel<128, 3>, walk_staged_kernel<128, 3, false>, walk_staged_kernel<128, 3, true>},  // 4: <=168 regs
+    {128, walk_kernel<128, 4>, walk_staged_kernel<128, 4, false>, walk_staged_kernel<128, 4, true>},  // 5: <=128 regs
+    {192, walk_kernel<192, 2>, walk_staged_kernel<192, 2, false>, walk_staged_kernel<192, 2, true>},  // 6: <=168 regs
 };
 
 static WalkArgs walk_args(bt_tally* h, const double* dest, const int8_t* fly, const double* w,
@@ -2384,7 +2395,8 @@ static bt_status walk_enqueue(bt_tally* h, WalkArgs a, int64_t lo, int64_t hi, i
     const int vi = (h->blocks_per_sm >= 1 && h->blocks_per_sm <= NVAR ? h->blocks_per_sm
                                                                        : DEFAULT_VARIANT) - 1;
     const Variant& V = kVariants[vi];
-    const void* kptr = staged ? (const void*)V.staged : (const void*)V.plain;
+    auto* staged_k = a.digest ? V.staged_dig : V.staged;
+    const void* kptr = staged ? (const void*)staged_k : (const void*)V.plain;
     const size_t dyn = staged ? sizeof(WarpStage) * 2 * (V.threads / 32) : 0;
     if (staged) CK(cudaFuncSetAttribute(kptr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     int bps = 0;
@@ -2399,6 +2411,7 @@ static bt_status walk_enqueue(bt_tally* h, WalkArgs a, int64_t lo, int64_t hi, i
         TRY(ensure_work(h));
         W = h->work;
         W.px += lo; W.py += lo; W.pz += lo; W.dx += lo; W.dy += lo; W.dz += lo;
+        W.r0 += lo; W.r1 += lo;
         W.w += lo; W.seg += lo; W.idx += lo; W.e += lo; W.g += lo; W.fl += lo;
         stage_kernel<<<grid_for(count, 256), 256, 0, st>>>(a, W, nwork, lo, wsum);
         CK(cudaGetLastError());
@@ -2417,7 +2430,7 @@ static bt_status walk_enqueue(bt_tally* h, WalkArgs a, int64_t lo, int64_t hi, i
         h->walk_first = false;
     }
     if (staged)
-        V.staged<<<blocks, V.threads, dyn, st>>>(a, W, nwork);
+        staged_k<<<blocks, V.threads, dyn, st>>>(a, W, nwork);
     else
         V.plain<<<blocks, V.threads, 0, st>>>(a);
     CK(cudaGetLastError());

@@ -16,6 +16,7 @@ from sweep import run_point  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--out", default=None)
 ap.add_argument("--particles", type=int, default=10_000_000)
+ap.add_argument("--only", default=None, help="comma-separated option names to run")
 args = ap.parse_args()
 
 import torch  # noqa: E402
@@ -37,6 +38,8 @@ res = []
 for src_name, src in (("uniform", uniform), ("point", point)):
     for sigma in (2.0, 100.0):
         for name, kw in OPTS:
+            if args.only and name not in args.only.split(","):
+                continue
             r = run_point(m, src, sigma, 1, f"C2 {src_name} sigma_t={sigma:g} {name}", **kw)
             r.update(source=src_name, option=name)
             res.append(r)
