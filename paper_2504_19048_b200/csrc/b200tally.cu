@@ -105,6 +105,7 @@ struct WalkArgs {
     unsigned long long* counters;        // C_NCOUNTERS
     int64_t count;
     int64_t max_sweeps;
+    int32_t max_sweeps32;  // min(max_sweeps, INT32_MAX): the per-step guard's bound
     int32_t ngroups;
     int32_t score;
     int32_t wagg;    // tally atomics: WAGG_ADAPTIVE / WAGG_ALWAYS / WAGG_NEVER
@@ -200,6 +201,8 @@ struct Pending {
     double val = 0.0;
     double seg = 0.0;
     bool seg_pending = false;
+    int probe = 0;      // loop iterations to the next contention probe
+    bool agg = false;   // warp-uniform: aggregate the pending scores
 };
 
 // One step of search.py:183-274 for a flying lane.  Returns true when the
@@ -210,7 +213,8 @@ struct Pending {
 template <bool DIG = true>
 __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& C, Pending& P,
                                           const DigestSlot& DS) {
-    const ElemRec r = L.have_nr ? L.nr : load_rec(a.rec, L.e);
+    if (!L.have_nr) L.nr = load_rec(a.rec, L.e);  // not prefetched: first step after a hop
+    const ElemRec r = L.nr;
     L.have_nr = false;
     Tet T;
     load_tet(a, r, T);
@@ -225,7 +229,7 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
         P.seg_pending = false;
     }
     double ox = L.px, oy = L.py, oz = L.pz;
-    if (L.st == 1) {  // search.py:190-196
+    if (__builtin_expect(L.st == 1, 0)) {  // search.py:190-196
         const double sx = __dsub_rn(L.dx(), L.px), sy = __dsub_rn(L.dy(), L.py),
                      sz = __dsub_rn(L.dz(), L.pz);
         const double ln = __dsqrt_rn(
@@ -242,7 +246,7 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
     int kind = exit_search_fast(T, ox, oy, oz, L.dx(), L.dy(), L.dz(), L.entry, &face, &t, &exact_used,
                                 true, &need_t);
     // (neighbour << 2) | its face across the exit face, -1 on the boundary
-    const int nbp = face == 0 ? r.nb[0] : face == 1 ? r.nb[1] : face == 2 ? r.nb[2] : r.nb[3];
+    const int nbp = (face & 2) ? ((face & 1) ? r.nb[3] : r.nb[2]) : ((face & 1) ? r.nb[1] : r.nb[0]);
     if (kind == 1) {
         // issue the next element's record load now: it lands while the exact
         // t division and the commit below run
@@ -342,7 +346,7 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
         }
     }
     ++L.iters;
-    if (!done && L.iters > a.max_sweeps) {  // sweep guard, search.py:513-516
+    if (L.iters > a.max_sweeps32 && !done) {  // sweep guard, search.py:513-516
         atomicOr(C.sh + SC_ERR, 1u);
         done = true;
     }
@@ -422,11 +426,17 @@ __device__ __forceinline__ void flush_pending(const WalkArgs& a, Pending& P, boo
     constexpr unsigned FULL = 0xffffffffu;
     bool agg = a.wagg == WAGG_ALWAYS;
     if (a.wagg == WAGG_ADAPTIVE) {
-        const int lane = threadIdx.x & 31;
-        const unsigned hm = __ballot_sync(FULL, P.has);
-        const long long nxt = __shfl_down_sync(FULL, (long long)P.bin, 1);
-        const bool dup = P.has && lane < 31 && ((hm >> (lane + 1)) & 1u) && nxt == P.bin;
-        agg = __any_sync(FULL, dup);
+        // probe every 4th iteration; the decision holds in between (warp-uniform)
+        if (--P.probe <= 0) {
+            const int lane = threadIdx.x & 31;
+            const unsigned hm = __ballot_sync(FULL, P.has);
+            const int nxt = __shfl_down_sync(FULL, (int)P.bin, 1);
+            // low 32 bits: a false match only aggregates, which stays exact
+            const bool dup = P.has && lane < 31 && ((hm >> (lane + 1)) & 1u) && nxt == (int)P.bin;
+            P.agg = __any_sync(FULL, dup);
+            P.probe = 4;
+        }
+        agg = P.agg;
     }
     if (agg) {
         score_aggregated(a, P.has, P.bin, P.val);
@@ -2358,6 +2368,7 @@ static WalkArgs walk_args(bt_tally* h, const double* dest, const int8_t* fly, co
     a.counters = h->dcounters + 1;
     a.count = 0;
     a.max_sweeps = h->max_sweeps >= 0 ? h->max_sweeps : 2 * h->ne + 1000;
+    a.max_sweeps32 = (int32_t)std::min<int64_t>(a.max_sweeps, 0x7fffffff);
     a.ngroups = h->ngroups;
     a.score = score ? 1 : 0;
     a.wagg = h->opt_wagg;
