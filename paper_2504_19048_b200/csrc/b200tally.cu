@@ -555,10 +555,20 @@ struct WorkSoA {
     int4 *r0, *r1;          // the starting element's record (vertex ids | adjacency)
 };
 
+// work items per stage chunk (one per lane at most).  Smaller chunks leave
+// more of the SM's 256 KB to the L1 that caches the mesh gathers, but 8 and 16
+// measured no faster than 32 on C2 (tools/build_variant.sh -DBT_STAGE_N=...)
+#ifndef BT_STAGE_N
+#define BT_STAGE_N 32
+#endif
+constexpr int STAGE_N = BT_STAGE_N;
+static_assert(STAGE_N >= 1 && STAGE_N <= 32, "a stage chunk refills at most one warp");
+
 struct __align__(16) WarpStage {
-    double px[32], py[32], pz[32], dx[32], dy[32], dz[32], w[32], seg[32];
-    int4 r0[32], r1[32];
-    int idx[32], e[32], g[32], fl[32];
+    double px[STAGE_N], py[STAGE_N], pz[STAGE_N], dx[STAGE_N], dy[STAGE_N], dz[STAGE_N],
+        w[STAGE_N], seg[STAGE_N];
+    int4 r0[STAGE_N], r1[STAGE_N];
+    int idx[STAGE_N], e[STAGE_N], g[STAGE_N], fl[STAGE_N];
 };
 
 
@@ -583,10 +593,10 @@ __device__ __forceinline__ int claim_chunk(const WalkArgs& a, const WorkSoA& W, 
                                            int64_t nwork) {
     const int lane = threadIdx.x & 31;
     unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(a.queue, 32ull);
+    if (lane == 0) base = atomicAdd(a.queue, (unsigned long long)STAGE_N);
     base = __shfl_sync(0xffffffffu, base, 0);
     const int64_t left = nwork - (int64_t)base;
-    const int n = left <= 0 ? 0 : (left >= 32 ? 32 : (int)left);
+    const int n = left <= 0 ? 0 : (left >= STAGE_N ? STAGE_N : (int)left);
     if (lane < n) {
         const int64_t k = (int64_t)base + lane;
         cp_async8(&st.px[lane], W.px + k);
@@ -632,7 +642,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     int cur = 0;
     int head = 0;
     int ncur = claim_chunk(a, W, stages[wid][0], nwork);
-    int nnext = ncur == 32 ? claim_chunk(a, W, stages[wid][1], nwork) : 0;
+    int nnext = ncur == STAGE_N ? claim_chunk(a, W, stages[wid][1], nwork) : 0;
     // only the first group must have landed; wait_group 1 would do, but the
     // second claim may be empty -- a full wait costs one DRAM latency once
     cp_async_wait_all();
@@ -648,7 +658,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
                 head = 0;
                 ncur = nnext;
                 // the stage just emptied is free: prefetch the chunk after next
-                nnext = (ncur == 32) ? claim_chunk(a, W, stages[wid][cur ^ 1], nwork) : 0;
+                nnext = (ncur == STAGE_N) ? claim_chunk(a, W, stages[wid][cur ^ 1], nwork) : 0;
             }
             const int take = min((int)__popc(idle), ncur - head);
             if (!L.busy) {
