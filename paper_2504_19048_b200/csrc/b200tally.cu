@@ -333,6 +333,10 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
             L.outcome() = OUT_REACHED;
             atomicAdd(C.sh + SC_REACHED, 1u);
             done = true;
+            // the particle stays in this element: a following flight (transport)
+            // starts without the dependent record load
+            L.nr = r;
+            L.have_nr = true;
         } else {
             if (nbp < 0) {
                 L.outcome() = OUT_LEAKED;
@@ -920,6 +924,7 @@ __global__ void __launch_bounds__(THREADS, MINB) transport_kernel(const Transpor
                         rb = t.rng_block[i];
                         L.entry = -1;
                         L.st = 0;
+                        L.have_nr = false;  // a new history: load its element's record
                         rounds = 0;
                         need_flight = true;
                     }
@@ -940,7 +945,6 @@ __global__ void __launch_bounds__(THREADS, MINB) transport_kernel(const Transpor
                 L.dx() = __dadd_rn(L.px, __dmul_rn(lc, ux));
                 L.dy() = __dadd_rn(L.py, __dmul_rn(lc, uy));
                 L.dz() = __dadd_rn(L.pz, __dmul_rn(lc, uz));
-                L.have_nr = false;
                 L.iters = 0;
                 L.outcome() = OUT_NONE;
                 L.alive() = 1;
