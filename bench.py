@@ -455,7 +455,7 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_src,
-                         "kernel": "walk_kernel", "kernel_ms_per_step": stats["walk_ms"] / args.steps,
+                         "kernel": "walk_staged_kernel", "kernel_ms_per_step": stats["walk_ms"] / args.steps,
                          "algorithmic_bytes": "133 B/crossing + 100 B/move (SURVEY.md §8d)"},
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
