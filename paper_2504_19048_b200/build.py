@@ -15,7 +15,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 SRC = PKG / "csrc" / "b200tally.cu"
-DEPS = [SRC, PKG / "csrc" / "geometry.cuh", ROOT / "include" / "b200tally.h"]
+DEPS = [SRC, *sorted((PKG / "csrc").glob("*.cuh")), ROOT / "include" / "b200tally.h"]
 LIB = PKG / "libb200tally.so"
 
 NVCC_FLAGS = [

@@ -1,0 +1,82 @@
+// layout.cuh -- device data layout of the walk: element records, vertices, walk arguments, loads.
+// Part of libb200tally (included by b200tally.cu, one translation unit).
+#pragma once
+
+// ---------------------------------------------------------------------------
+// device data layout
+
+struct __align__(32) ElemRec {
+    int v[4];   // global vertex ids, reference local order (mesh.py:126-132)
+    int nb[4];  // (neighbour << 2) | neighbour's local face, -1 on the boundary
+};
+static_assert(sizeof(ElemRec) == 32, "one 32-byte sector per element");
+
+struct __align__(32) Vtx {
+    double x, y, z, pad;
+};
+static_assert(sizeof(Vtx) == 32, "one 32-byte sector per vertex");
+
+enum { C_EVENTS = 0, C_REACHED, C_BOUNDARY, C_RECOV, C_KILLED, C_SWEEPS, C_ERR, C_UNLOC, C_NCOUNTERS };
+// dcounters layout (unsigned long long): [1..8] counters, [15] flags,
+// [16 + c] queue of chunk c, [32 + c] work count of chunk c, c < MAX_CHUNKS
+constexpr int MAX_CHUNKS = 16;
+constexpr int NDCOUNTERS = 48;
+
+// __match_any_sync aggregation of the tally atomics (BT_OPT_WARP_AGG)
+enum { WAGG_ADAPTIVE = 0, WAGG_ALWAYS = 1, WAGG_NEVER = 2 };
+
+struct WalkArgs {
+    const ElemRec* __restrict__ rec;
+    const Vtx* __restrict__ vtx;
+    double* __restrict__ pos;            // (N,3) persistent
+    const double* __restrict__ dest;     // (count,3) this move's destinations
+    const int8_t* __restrict__ fly_in;   // (count) this move's flying flags
+    const double* __restrict__ weight;   // (count) this move's weights (nullable if !score)
+    const int32_t* __restrict__ group;   // (N) persistent groups
+    int32_t* __restrict__ element;
+    int8_t* __restrict__ alive;
+    int8_t* __restrict__ entry;
+    int8_t* __restrict__ stuck;
+    int8_t* __restrict__ outcome;
+    double* __restrict__ seg_total;
+    double* __restrict__ tally;          // (E*G)
+    uint64_t* __restrict__ digest;       // (N) nullable
+    int64_t* __restrict__ dcount;        // (N) nullable
+    const int32_t* __restrict__ order;   // (count) nullable: hand-out permutation
+    unsigned long long* queue;
+    unsigned long long* counters;        // C_NCOUNTERS
+    int64_t count;
+    int64_t max_sweeps;
+    int32_t max_sweeps32;  // min(max_sweeps, INT32_MAX): the per-step guard's bound
+    int32_t ngroups;
+    int32_t score;
+    int32_t wagg;    // tally atomics: WAGG_ADAPTIVE / WAGG_ALWAYS / WAGG_NEVER
+};
+
+__device__ __forceinline__ void load_tet(const WalkArgs& a, const ElemRec& r, Tet& T) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const double2* p = reinterpret_cast<const double2*>(a.vtx + r.v[j]);
+        const double2 xy = __ldg(p);
+        const double2 zw = __ldg(p + 1);
+        T.x[j] = xy.x;
+        T.y[j] = xy.y;
+        T.z[j] = zw.x;
+    }
+}
+
+__device__ __forceinline__ ElemRec load_rec(const ElemRec* __restrict__ rec, int e) {
+    const int4* p = reinterpret_cast<const int4*>(rec + e);
+    const int4 a = __ldg(p);
+    const int4 b = __ldg(p + 1);
+    ElemRec r;
+    r.v[0] = a.x; r.v[1] = a.y; r.v[2] = a.z; r.v[3] = a.w;
+    r.nb[0] = b.x; r.nb[1] = b.y; r.nb[2] = b.z; r.nb[3] = b.w;
+    return r;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}

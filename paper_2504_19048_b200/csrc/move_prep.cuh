@@ -1,0 +1,47 @@
+// move_prep.cuh -- move preparation, finalize, element-ordered hand-out keys.
+// Part of libb200tally (included by b200tally.cu, one translation unit).
+#pragma once
+
+// ---------------------------------------------------------------------------
+// move preparation: localization check (+ group range + source weight for
+// device-resident inputs)
+
+__global__ void prepare_kernel(const int8_t* __restrict__ fly, const int32_t* __restrict__ element,
+                               const int32_t* __restrict__ groups, int32_t ngroups,
+                               const double* __restrict__ weight, int64_t count,
+                               unsigned long long* __restrict__ flags,
+                               double* __restrict__ wsum) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    bool unloc = false, badg = false;
+    double wv = 0.0;
+    if (i < count) {
+        const bool f = fly[i] != 0;
+        unloc = f && element[i] < 0;
+        if (groups) badg = groups[i] < 0 || groups[i] >= ngroups;
+        if (wsum && f) wv = weight[i];
+    }
+    if (__any_sync(0xffffffffu, unloc) && (threadIdx.x & 31) == 0) atomicOr(flags, 1ull);
+    if (__any_sync(0xffffffffu, badg) && (threadIdx.x & 31) == 0) atomicOr(flags, 2ull);
+    if (wsum) {
+        for (int o = 16; o > 0; o >>= 1) wv += __shfl_xor_sync(0xffffffffu, wv, o);
+        if ((threadIdx.x & 31) == 0 && wv != 0.0) atomicAdd(wsum, wv);
+    }
+}
+
+__global__ void finalize_kernel(double* __restrict__ acc, double* __restrict__ sum,
+                                double* __restrict__ sum_sq, int64_t nbins, double w) {
+    int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= nbins) return;
+    const double x = __ddiv_rn(acc[b], w);
+    acc[b] = 0.0;
+    sum[b] = __dadd_rn(sum[b], x);
+    sum_sq[b] = __dadd_rn(sum_sq[b], __dmul_rn(x, x));
+}
+
+__global__ void iota_keys_kernel(const int32_t* __restrict__ element, int64_t count,
+                                 unsigned* __restrict__ keys, int32_t* __restrict__ vals) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    keys[i] = (unsigned)(element[i] + 1);
+    vals[i] = (int32_t)i;
+}

@@ -1,0 +1,629 @@
+// walk.cuh -- the walk kernels: lane state, walk_step, the staged persistent kernel, staging.
+// Part of libb200tally (included by b200tally.cu, one translation unit).
+#pragma once
+
+// ---------------------------------------------------------------------------
+// walk kernels: the fused sweep (search.py:169-275) run to completion per lane
+
+constexpr int DEFAULT_VARIANT = 6;  // see run_walk's variant table
+
+// Cold per-lane state (read at events and at the end of a walk) lives in
+// shared memory, one slot per thread: fewer live registers in the hot loop.
+constexpr int MAX_CTA_THREADS = 256;
+__shared__ double s_lane_w[MAX_CTA_THREADS];
+__shared__ double s_lane_seg[MAX_CTA_THREADS];
+__shared__ int64_t s_lane_idx[MAX_CTA_THREADS];
+__shared__ int s_lane_g[MAX_CTA_THREADS];
+__shared__ double s_lane_d[3][MAX_CTA_THREADS];  // destination
+__shared__ int8_t s_lane_outcome[MAX_CTA_THREADS];
+__shared__ int8_t s_lane_alive[MAX_CTA_THREADS];
+
+// one particle's walk state while it flies
+struct Lane {
+    ElemRec nr;   // prefetched record of the element entered next
+    bool have_nr;
+    bool busy;    // false: lane idle
+    double px, py, pz;
+    int e, entry, st, iters;
+    __device__ __forceinline__ double& w() { return s_lane_w[threadIdx.x]; }
+    __device__ __forceinline__ double& seg() { return s_lane_seg[threadIdx.x]; }
+    __device__ __forceinline__ int64_t& idx() { return s_lane_idx[threadIdx.x]; }
+    __device__ __forceinline__ int& g() { return s_lane_g[threadIdx.x]; }
+    __device__ __forceinline__ int8_t& outcome() { return s_lane_outcome[threadIdx.x]; }
+    __device__ __forceinline__ int8_t& alive() { return s_lane_alive[threadIdx.x]; }
+    __device__ __forceinline__ double& dx() { return s_lane_d[0][threadIdx.x]; }
+    __device__ __forceinline__ double& dy() { return s_lane_d[1][threadIdx.x]; }
+    __device__ __forceinline__ double& dz() { return s_lane_d[2][threadIdx.x]; }
+    __device__ __forceinline__ void set_idx(int64_t i) {
+        idx() = i;
+        busy = true;
+    }
+};
+
+// this thread's digest slot in shared memory (digest mode only; keeps the
+// sequence hash out of the hot loop's registers)
+struct DigestSlot {
+    uint64_t* d;
+    int* c;
+};
+
+// Per-lane event count in a register; the rarer counters live in a
+// CTA-shared array (fewer live registers in the hot loop), flushed once.
+enum { SC_REACHED = 0, SC_BOUNDARY, SC_RECOV, SC_KILLED, SC_MAXIT, SC_ERR, SC_N };
+struct Counters {
+    unsigned events = 0;
+    unsigned maxit = 0;      // longest walk (sweeps) finished by this lane
+    unsigned* sh = nullptr;  // SC_N shared counters of the CTA
+};
+
+// Deferred track-length score of the previous step: its square root and
+// atomic are issued after the next step's loads, off the critical path.
+struct Pending {
+    bool has = false;
+    int64_t bin = 0;
+    double val = 0.0;
+    double seg = 0.0;
+    bool seg_pending = false;
+    int probe = 0;      // loop iterations to the next contention probe
+    bool agg = false;   // warp-uniform: aggregate the pending scores
+};
+
+// One step of search.py:183-274 for a flying lane.  Returns true when the
+// particle stops (reached, leaked, stuck-killed or sweep guard).  When DEFER
+// the segment is left in P (scored by the next step or the loop); otherwise
+// has_score/bin/val are set for an immediate score.
+// DIG = false compiles the per-particle digest bookkeeping out of the loop.
+template <bool DIG = true>
+__device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& C, Pending& P,
+                                          const DigestSlot& DS) {
+    if (!L.have_nr) L.nr = load_rec(a.rec, L.e);  // not prefetched: first step after a hop
+    const ElemRec r = L.nr;
+    L.have_nr = false;
+    Tet T;
+    load_tet(a, r, T);
+    // the previous step's score and seg_total update, while this step's
+    // vertex loads are in flight (warp-aggregated mode scores at loop level)
+    if (P.has) {  // not taken by an aggregated flush at loop level
+        atomicAdd(a.tally + P.bin, P.val);
+        P.has = false;
+    }
+    if (P.seg_pending) {
+        L.seg() = __dadd_rn(L.seg(), P.seg);
+        P.seg_pending = false;
+    }
+    double ox = L.px, oy = L.py, oz = L.pz;
+    if (__builtin_expect(L.st == 1, 0)) {  // search.py:190-196
+        const double sx = __dsub_rn(L.dx(), L.px), sy = __dsub_rn(L.dy(), L.py),
+                     sz = __dsub_rn(L.dz(), L.pz);
+        const double ln = __dsqrt_rn(
+            __dadd_rn(__dadd_rn(__dmul_rn(sx, sx), __dmul_rn(sy, sy)), __dmul_rn(sz, sz)));
+        if (ln > 0.0) {
+            ox = __dadd_rn(ox, __ddiv_rn(__dmul_rn(NUDGE, sx), ln));
+            oy = __dadd_rn(oy, __ddiv_rn(__dmul_rn(NUDGE, sy), ln));
+            oz = __dadd_rn(oz, __ddiv_rn(__dmul_rn(NUDGE, sz), ln));
+        }
+    }
+    int face;
+    double t;
+    bool exact_used, need_t;
+    int kind = exit_search_fast(T, ox, oy, oz, L.dx(), L.dy(), L.dz(), L.entry, &face, &t, &exact_used,
+                                true, &need_t);
+    // (neighbour << 2) | its face across the exit face, -1 on the boundary
+    const int nbp = (face & 2) ? ((face & 1) ? r.nb[3] : r.nb[2]) : ((face & 1) ? r.nb[1] : r.nb[0]);
+    if (kind == 1) {
+        // issue the next element's record load now: it lands while the exact
+        // t division and the commit below run
+        if (nbp >= 0) {
+            L.nr = load_rec(a.rec, nbp >> 2);
+            L.have_nr = true;
+        }
+        if (need_t)
+            t = exact_t(T, face, ox, oy, oz, rn_sub(L.dx(), ox), rn_sub(L.dy(), oy), rn_sub(L.dz(), oz));
+    }
+    bool done = false;
+    bool event = true;
+    if (kind == 2) {  // stuck ladder, search.py:199-235
+        if (contains(T, L.dx(), L.dy(), L.dz(), STUCK_TOL)) {
+            kind = 0;
+            atomicAdd(C.sh + SC_RECOV, 1u);
+        } else if (L.st == 0) {
+            L.st = 1;
+            atomicAdd(C.sh + SC_RECOV, 1u);
+            event = false;
+        } else if (L.st == 1) {
+            int hop = -1;
+#pragma unroll 1
+            for (int f = 0; f < 4; ++f) {  // rare path: reload, no local arrays
+                const int nbp = __ldg(&a.rec[L.e].nb[f]);
+                if (hop < 0 && nbp >= 0) {
+                    const int nb = nbp >> 2;
+                    const ElemRec rn = load_rec(a.rec, nb);
+                    Tet Tn;
+                    load_tet(a, rn, Tn);
+                    if (contains(Tn, ox, oy, oz, EPS_BARY)) hop = nb;
+                }
+            }
+            event = false;
+            if (hop >= 0) {
+                L.e = hop;
+                L.entry = -1;
+                L.st = 2;
+                atomicAdd(C.sh + SC_RECOV, 1u);
+            } else {
+                L.outcome() = OUT_STUCK_KILLED;
+                L.alive() = 0;
+                atomicAdd(C.sh + SC_KILLED, 1u);
+                done = true;
+            }
+        } else {
+            L.outcome() = OUT_STUCK_KILLED;
+            L.alive() = 0;
+            atomicAdd(C.sh + SC_KILLED, 1u);
+            event = false;
+            done = true;
+        }
+    }
+    if (event) {  // search.py:236-274
+        ++C.events;
+        L.st = 0;
+        if (DIG && a.digest) {
+            *DS.d = (*DS.d ^ (uint64_t)((int64_t)L.e * 8 + face + 1)) * DIGEST_PRIME;
+            ++*DS.c;
+        }
+        double qx, qy, qz;
+        if (kind == 0) {
+            qx = L.dx();
+            qy = L.dy();
+            qz = L.dz();
+        } else {
+            qx = __dadd_rn(ox, __dmul_rn(t, __dsub_rn(L.dx(), ox)));
+            qy = __dadd_rn(oy, __dmul_rn(t, __dsub_rn(L.dy(), oy)));
+            qz = __dadd_rn(oz, __dmul_rn(t, __dsub_rn(L.dz(), oz)));
+        }
+        const double ax = __dsub_rn(qx, L.px), ay = __dsub_rn(qy, L.py), az = __dsub_rn(qz, L.pz);
+        const double seg = __dsqrt_rn(
+            __dadd_rn(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)), __dmul_rn(az, az)));
+        P.has = a.score != 0;
+        P.bin = (int64_t)L.e * a.ngroups + L.g();
+        P.val = __dmul_rn(L.w(), seg);
+        P.seg = seg;
+        P.seg_pending = true;
+        L.px = qx;
+        L.py = qy;
+        L.pz = qz;
+        if (kind == 0) {
+            L.entry = -1;
+            L.outcome() = OUT_REACHED;
+            atomicAdd(C.sh + SC_REACHED, 1u);
+            done = true;
+            // the particle stays in this element: a following flight (transport)
+            // starts without the dependent record load
+            L.nr = r;
+            L.have_nr = true;
+        } else {
+            if (nbp < 0) {
+                L.outcome() = OUT_LEAKED;
+                L.alive() = 0;
+                atomicAdd(C.sh + SC_BOUNDARY, 1u);
+                done = true;
+            } else {
+                L.e = nbp >> 2;
+                L.entry = nbp & 3;
+            }
+        }
+    }
+    ++L.iters;
+    if (L.iters > a.max_sweeps32 && !done) {  // sweep guard, search.py:513-516
+        atomicOr(C.sh + SC_ERR, 1u);
+        done = true;
+    }
+    if (done && P.seg_pending) {  // the final seg_total is written now
+        L.seg() = __dadd_rn(L.seg(), P.seg);
+        P.seg_pending = false;
+    }
+    return done;
+}
+
+template <bool DIG = true>
+__device__ __forceinline__ void finish(const WalkArgs& a, Lane& L, Counters& C,
+                                       const DigestSlot& DS) {
+    const int64_t i = L.idx();
+    a.pos[3 * i] = L.px;
+    a.pos[3 * i + 1] = L.py;
+    a.pos[3 * i + 2] = L.pz;
+    a.element[i] = L.e;
+    a.entry[i] = (int8_t)L.entry;
+    a.stuck[i] = (int8_t)L.st;
+    a.outcome[i] = (int8_t)L.outcome();
+    a.alive[i] = (int8_t)L.alive();
+    a.seg_total[i] = L.seg();
+    if (DIG && a.digest) {
+        a.digest[i] = *DS.d;
+        a.dcount[i] = *DS.c;
+    }
+    C.maxit = max(C.maxit, (unsigned)L.iters);
+    L.busy = false;
+}
+
+template <bool DIG = true>
+__device__ __forceinline__ void begin(Lane& L, const WalkArgs& a, const DigestSlot& DS) {
+    L.have_nr = false;
+    L.iters = 0;
+    if (DIG && a.digest) {
+        *DS.d = DIGEST_INIT;
+        *DS.c = 0;
+    }
+    L.alive() = 1;          // overwritten by the fetch with alive | flying (load_step)
+    L.outcome() = OUT_NONE;
+}
+
+// all lanes: one atomic per distinct bin of the warp's pending scores
+__device__ __forceinline__ void score_aggregated(const WalkArgs& a, bool has_score, int64_t bin,
+                                                 double val) {
+    constexpr unsigned FULL = 0xffffffffu;
+    {
+        const int lane = threadIdx.x & 31;
+        const unsigned m = __ballot_sync(FULL, has_score);
+        if (has_score) {
+            const unsigned peers = __match_any_sync(m, (unsigned long long)bin);
+            const int leader = __ffs(peers) - 1;
+            double sum = val;
+            if (peers != (1u << lane)) {
+                sum = 0.0;
+                unsigned rest = peers;
+                while (rest) {
+                    const int src = __ffs(rest) - 1;
+                    rest &= rest - 1;
+                    sum = __dadd_rn(sum, __shfl_sync(peers, val, src));
+                }
+            }
+            if (lane == leader) atomicAdd(a.tally + bin, sum);
+        }
+    }
+}
+
+// Loop level, all lanes converged.  Pending scores are normally left for the
+// lane's next step to issue (after its loads, off the critical path).  They are
+// aggregated here instead when the warp's lanes are scoring the same bins:
+// always (WAGG_ALWAYS), or -- adaptive -- when a cheap probe (each lane's
+// pending bin against the next lane's) finds a duplicate, which is what a point
+// source with short flights produces (6x fewer contended atomics, measured in
+// profiles/r01_options.jsonl).  Idle lanes flush their pending score.
+__device__ __forceinline__ void flush_pending(const WalkArgs& a, Pending& P, bool idle) {
+    constexpr unsigned FULL = 0xffffffffu;
+    bool agg = a.wagg == WAGG_ALWAYS;
+    if (a.wagg == WAGG_ADAPTIVE) {
+        // probe every 4th iteration; the decision holds in between (warp-uniform)
+        if (--P.probe <= 0) {
+            const int lane = threadIdx.x & 31;
+            const unsigned hm = __ballot_sync(FULL, P.has);
+            const int nxt = __shfl_down_sync(FULL, (int)P.bin, 1);
+            // low 32 bits: a false match only aggregates, which stays exact
+            const bool dup = P.has && lane < 31 && ((hm >> (lane + 1)) & 1u) && nxt == (int)P.bin;
+            P.agg = __any_sync(FULL, dup);
+            P.probe = 4;
+        }
+        agg = P.agg;
+    }
+    if (agg) {
+        score_aggregated(a, P.has, P.bin, P.val);
+        P.has = false;
+    } else if (idle && P.has) {
+        atomicAdd(a.tally + P.bin, P.val);
+        P.has = false;
+    }
+}
+
+__device__ __forceinline__ void counters_init(unsigned* sh) {
+    if (threadIdx.x < SC_N) sh[threadIdx.x] = 0;
+    __syncthreads();
+}
+
+// all threads of the CTA: warp-reduce events, then one atomic per counter per CTA
+__device__ __forceinline__ void flush_counters(const WalkArgs& a, Counters& C) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const unsigned ev = __reduce_add_sync(FULL, C.events);
+    if ((threadIdx.x & 31) == 0 && ev) atomicAdd(a.counters + C_EVENTS, (unsigned long long)ev);
+    const unsigned mx = __reduce_max_sync(FULL, C.maxit);
+    if ((threadIdx.x & 31) == 0 && mx) atomicMax(C.sh + SC_MAXIT, mx);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned* sh = C.sh;
+        if (sh[SC_REACHED]) atomicAdd(a.counters + C_REACHED, (unsigned long long)sh[SC_REACHED]);
+        if (sh[SC_BOUNDARY]) atomicAdd(a.counters + C_BOUNDARY, (unsigned long long)sh[SC_BOUNDARY]);
+        if (sh[SC_RECOV]) atomicAdd(a.counters + C_RECOV, (unsigned long long)sh[SC_RECOV]);
+        if (sh[SC_KILLED]) atomicAdd(a.counters + C_KILLED, (unsigned long long)sh[SC_KILLED]);
+        if (sh[SC_MAXIT]) atomicMax(a.counters + C_SWEEPS, (unsigned long long)sh[SC_MAXIT]);
+        if (sh[SC_ERR]) atomicOr(a.counters + C_ERR, 1ull);
+    }
+}
+
+// v1: idle lanes refill straight from the particle arrays (one atomicAdd per
+// warp per refill); the fetch's global loads sit on the step's critical path.
+template <int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) walk_kernel(const WalkArgs a) {
+    static_assert(THREADS <= MAX_CTA_THREADS, "one shared lane slot per thread");
+    constexpr unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    __shared__ unsigned shc[SC_N];
+    __shared__ uint64_t sdig[THREADS];
+    __shared__ int scnt[THREADS];
+    counters_init(shc);
+    const DigestSlot DS{sdig + threadIdx.x, scnt + threadIdx.x};
+    Lane L;
+    L.busy = false;
+    Counters C;
+    C.sh = shc;
+    Pending P;
+    bool drained = false;
+    while (true) {
+        if (!drained) {
+            const unsigned idle = __ballot_sync(FULL, !L.busy);
+            if (idle) {
+                const unsigned nidle = __popc(idle);
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(a.queue, (unsigned long long)nidle);
+                base = __shfl_sync(FULL, base, 0);
+                if (base + nidle >= (unsigned long long)a.count) drained = true;
+                if (!L.busy) {
+                    const unsigned long long q = base + __popc(idle & lanemask_lt());
+                    if (q < (unsigned long long)a.count) {
+                        const int64_t i = a.order ? (int64_t)a.order[q] : (int64_t)q;
+                        if (a.digest && a.fly_in[i] == 0) {  // not moving: empty sequence
+                            a.digest[i] = DIGEST_INIT;
+                            a.dcount[i] = 0;
+                        }
+                        const bool unloc = a.fly_in[i] != 0 && a.element[i] < 0;
+                        if (unloc) atomicAdd(a.counters + C_UNLOC, 1ull);
+                        if (a.fly_in[i] != 0 && !unloc) {
+                            L.set_idx(i);
+                            L.e = a.element[i];
+                            L.px = a.pos[3 * i];
+                            L.py = a.pos[3 * i + 1];
+                            L.pz = a.pos[3 * i + 2];
+                            L.dx() = a.dest[3 * i];
+                            L.dy() = a.dest[3 * i + 1];
+                            L.dz() = a.dest[3 * i + 2];
+                            L.entry = a.entry[i];
+                            L.st = a.stuck[i];
+                            L.seg() = a.seg_total[i];
+                            L.w() = a.score ? a.weight[i] : 0.0;
+                            L.g() = a.score ? a.group[i] : 0;
+                            begin(L, a, DS);
+                            L.alive() = (int8_t)(a.alive[i] | a.fly_in[i]);
+                        }
+                    }
+                }
+            }
+        }
+        if (!__any_sync(FULL, L.busy)) {
+            flush_pending(a, P, true);
+            if (drained) break;
+            continue;
+        }
+        if (L.busy) {
+            if (walk_step(a, L, C, P, DS)) finish(a, L, C, DS);
+        }
+        flush_pending(a, P, !L.busy);
+    }
+    flush_counters(a, C);
+}
+
+// ---------------------------------------------------------------------------
+// v2: staged walk.  A stage kernel compacts the flying particles into SoA
+// work arrays (coalesced); each warp then claims chunks of 32 work items and
+// prefetches the NEXT chunk into shared memory with cp.async while its lanes
+// keep walking, so refilling an idle lane is a shared-memory read instead of
+// a dependent DRAM gather on the step's critical path.
+
+struct WorkSoA {
+    double *px, *py, *pz, *dx, *dy, *dz, *w, *seg;
+    int *idx, *e, *g, *fl;  // fl = entry (low byte, signed) | stuck << 8
+    int4 *r0, *r1;          // the starting element's record (vertex ids | adjacency)
+};
+
+// work items per stage chunk (one per lane at most).  Smaller chunks leave
+// more of the SM's 256 KB to the L1 that caches the mesh gathers, but 8 and 16
+// measured no faster than 32 on C2 (tools/build_variant.sh -DBT_STAGE_N=...)
+#ifndef BT_STAGE_N
+#define BT_STAGE_N 32
+#endif
+constexpr int STAGE_N = BT_STAGE_N;
+static_assert(STAGE_N >= 1 && STAGE_N <= 32, "a stage chunk refills at most one warp");
+
+struct __align__(16) WarpStage {
+    double px[STAGE_N], py[STAGE_N], pz[STAGE_N], dx[STAGE_N], dy[STAGE_N], dz[STAGE_N],
+        w[STAGE_N], seg[STAGE_N];
+    int4 r0[STAGE_N], r1[STAGE_N];
+    int idx[STAGE_N], e[STAGE_N], g[STAGE_N], fl[STAGE_N];
+};
+
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+// claim the next chunk of 32 work items and start copying it into `st`;
+// returns the number of valid items (warp-uniform)
+__device__ __forceinline__ int claim_chunk(const WalkArgs& a, const WorkSoA& W, WarpStage& st,
+                                           int64_t nwork) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(a.queue, (unsigned long long)STAGE_N);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    const int64_t left = nwork - (int64_t)base;
+    const int n = left <= 0 ? 0 : (left >= STAGE_N ? STAGE_N : (int)left);
+    if (lane < n) {
+        const int64_t k = (int64_t)base + lane;
+        cp_async8(&st.px[lane], W.px + k);
+        cp_async8(&st.py[lane], W.py + k);
+        cp_async8(&st.pz[lane], W.pz + k);
+        cp_async8(&st.dx[lane], W.dx + k);
+        cp_async8(&st.dy[lane], W.dy + k);
+        cp_async8(&st.dz[lane], W.dz + k);
+        cp_async8(&st.w[lane], W.w + k);
+        cp_async8(&st.seg[lane], W.seg + k);
+        cp_async4(&st.idx[lane], W.idx + k);
+        cp_async4(&st.e[lane], W.e + k);
+        cp_async4(&st.g[lane], W.g + k);
+        cp_async4(&st.fl[lane], W.fl + k);
+        cp_async16(&st.r0[lane], W.r0 + k);
+        cp_async16(&st.r1[lane], W.r1 + k);
+    }
+    cp_async_commit();
+    return n;
+}
+
+template <int THREADS, int MINB, bool DIG>
+__global__ void __launch_bounds__(THREADS, MINB)
+    walk_staged_kernel(const WalkArgs a, const WorkSoA W, const int64_t* __restrict__ nwork_p) {
+    static_assert(THREADS <= MAX_CTA_THREADS, "one shared lane slot per thread");
+    constexpr unsigned FULL = 0xffffffffu;
+    // the warps' double-buffered stages: dynamic shared memory (with the lane
+    // slots the CTA exceeds the 48 KB static limit)
+    extern __shared__ __align__(16) unsigned char dyn_smem[];
+    WarpStage(*stages)[2] = reinterpret_cast<WarpStage(*)[2]>(dyn_smem);
+    __shared__ unsigned shc[SC_N];
+    __shared__ uint64_t sdig[THREADS];
+    __shared__ int scnt[THREADS];
+    counters_init(shc);
+    const DigestSlot DS{sdig + threadIdx.x, scnt + threadIdx.x};
+    const int wid = threadIdx.x >> 5;
+    const int64_t nwork = *nwork_p;
+    Lane L;
+    L.busy = false;
+    Counters C;
+    C.sh = shc;
+    Pending P;
+    int cur = 0;
+    int head = 0;
+    int ncur = claim_chunk(a, W, stages[wid][0], nwork);
+    int nnext = ncur == STAGE_N ? claim_chunk(a, W, stages[wid][1], nwork) : 0;
+    // only the first group must have landed; wait_group 1 would do, but the
+    // second claim may be empty -- a full wait costs one DRAM latency once
+    cp_async_wait_all();
+    __syncwarp();
+    while (true) {
+        unsigned idle = __ballot_sync(FULL, !L.busy);
+        while (idle) {
+            if (head == ncur) {  // current stage used up: switch to the prefetched one
+                if (nnext == 0) break;
+                cp_async_wait_all();
+                __syncwarp();
+                cur ^= 1;
+                head = 0;
+                ncur = nnext;
+                // the stage just emptied is free: prefetch the chunk after next
+                nnext = (ncur == STAGE_N) ? claim_chunk(a, W, stages[wid][cur ^ 1], nwork) : 0;
+            }
+            const int take = min((int)__popc(idle), ncur - head);
+            if (!L.busy) {
+                const int rk = __popc(idle & lanemask_lt());
+                if (rk < take) {
+                    const WarpStage& s = stages[wid][cur];
+                    const int j = head + rk;
+                    L.set_idx(s.idx[j]);
+                    L.px = s.px[j];
+                    L.py = s.py[j];
+                    L.pz = s.pz[j];
+                    L.dx() = s.dx[j];
+                    L.dy() = s.dy[j];
+                    L.dz() = s.dz[j];
+                    L.w() = s.w[j];
+                    L.seg() = s.seg[j];
+                    L.e = s.e[j];
+                    L.g() = s.g[j];
+                    const int fl = s.fl[j];
+                    L.entry = (int)(signed char)(fl & 0xff);
+                    L.st = (fl >> 8) & 0xff;
+                    begin<DIG>(L, a, DS);
+                    L.alive() = (int)(signed char)((fl >> 16) & 0xff);
+                    // the first step's record came with the stage: no dependent load
+                    const int4 q0 = s.r0[j], q1 = s.r1[j];
+                    L.nr.v[0] = q0.x; L.nr.v[1] = q0.y; L.nr.v[2] = q0.z; L.nr.v[3] = q0.w;
+                    L.nr.nb[0] = q1.x; L.nr.nb[1] = q1.y; L.nr.nb[2] = q1.z; L.nr.nb[3] = q1.w;
+                    L.have_nr = true;
+                }
+            }
+            head += take;
+            idle = __ballot_sync(FULL, !L.busy);
+        }
+        if (!__any_sync(FULL, L.busy)) {  // no work left anywhere for this warp
+            flush_pending(a, P, true);
+            break;
+        }
+        if (L.busy) {
+            if (walk_step<DIG>(a, L, C, P, DS)) finish<DIG>(a, L, C, DS);
+        }
+        flush_pending(a, P, !L.busy);
+    }
+    cp_async_wait_all();
+    flush_counters(a, C);
+}
+
+// Compact this move's flying particles into the work arrays (order of
+// indices within a warp preserved; warps in arbitrary order).  Non-flying
+// particles get an empty digest.
+// Particles [lo, lo + a.count) of this move; work items go to W (already
+// offset by the caller).  A flying particle with element < 0 is not staged
+// and counted (the move then reports it); wsum (nullable) accumulates the
+// flying particles' weights (device-resident inputs).
+__global__ void stage_kernel(const WalkArgs a, const WorkSoA W, int64_t* __restrict__ nwork,
+                             int64_t lo, double* __restrict__ wsum) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    bool fly = false;
+    int64_t i = 0;
+    double wv = 0.0;
+    if (t < a.count) {
+        i = a.order ? (int64_t)a.order[t] : lo + t;
+        fly = a.fly_in[i] != 0;
+        if (a.digest && !fly) {
+            a.digest[i] = DIGEST_INIT;
+            a.dcount[i] = 0;
+        }
+        if (fly && wsum) wv = a.weight[i];
+        if (fly && a.element[i] < 0) {
+            atomicAdd(a.counters + C_UNLOC, 1ull);
+            fly = false;
+        }
+    }
+    if (wsum) {
+        for (int o = 16; o > 0; o >>= 1) wv += __shfl_xor_sync(0xffffffffu, wv, o);
+        if (lane == 0 && wv != 0.0) atomicAdd(wsum, wv);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, fly);
+    if (!m) return;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd((unsigned long long*)nwork, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (!fly) return;
+    const int64_t k = (int64_t)base + __popc(m & lanemask_lt());
+    W.idx[k] = (int)i;
+    W.px[k] = a.pos[3 * i];
+    W.py[k] = a.pos[3 * i + 1];
+    W.pz[k] = a.pos[3 * i + 2];
+    W.dx[k] = a.dest[3 * i];
+    W.dy[k] = a.dest[3 * i + 1];
+    W.dz[k] = a.dest[3 * i + 2];
+    W.w[k] = a.score ? a.weight[i] : 0.0;
+    W.seg[k] = a.seg_total[i];
+    W.e[k] = a.element[i];
+    W.g[k] = a.score ? a.group[i] : 0;
+    W.fl[k] = ((int)(unsigned char)a.entry[i]) | ((int)(unsigned char)a.stuck[i] << 8) |
+              ((int)(unsigned char)(a.alive[i] | a.fly_in[i]) << 16);  // load_step: alive |= flying
+    const int4* rp = reinterpret_cast<const int4*>(a.rec + a.element[i]);
+    W.r0[k] = __ldg(rp);
+    W.r1[k] = __ldg(rp + 1);
+}
