@@ -53,12 +53,38 @@ struct WalkArgs {
     int32_t wagg;    // tally atomics: WAGG_ADAPTIVE / WAGG_ALWAYS / WAGG_NEVER
 };
 
+#ifndef BT_NO_L2_HINT
+// Mesh gathers carry an L2 evict_last policy, so the streamed particle state
+// and work list are evicted first (3% on the C2 walk, 0.7% when the mesh
+// exceeds L2: tools/sweep.py --which c4 with -DBT_NO_L2_HINT as the control).
+__device__ __forceinline__ unsigned long long mesh_policy() {
+    unsigned long long pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ double2 ldg_mesh(const double2* p) {
+    double2 v;
+    asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+        : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(mesh_policy()));
+    return v;
+}
+__device__ __forceinline__ int4 ldg_mesh(const int4* p) {
+    int4 v;
+    asm("ld.global.nc.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(mesh_policy()));
+    return v;
+}
+#else
+__device__ __forceinline__ double2 ldg_mesh(const double2* p) { return __ldg(p); }
+__device__ __forceinline__ int4 ldg_mesh(const int4* p) { return __ldg(p); }
+#endif
+
 __device__ __forceinline__ void load_tet(const WalkArgs& a, const ElemRec& r, Tet& T) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         const double2* p = reinterpret_cast<const double2*>(a.vtx + r.v[j]);
-        const double2 xy = __ldg(p);
-        const double2 zw = __ldg(p + 1);
+        const double2 xy = ldg_mesh(p);
+        const double2 zw = ldg_mesh(p + 1);
         T.x[j] = xy.x;
         T.y[j] = xy.y;
         T.z[j] = zw.x;
@@ -67,8 +93,8 @@ __device__ __forceinline__ void load_tet(const WalkArgs& a, const ElemRec& r, Te
 
 __device__ __forceinline__ ElemRec load_rec(const ElemRec* __restrict__ rec, int e) {
     const int4* p = reinterpret_cast<const int4*>(rec + e);
-    const int4 a = __ldg(p);
-    const int4 b = __ldg(p + 1);
+    const int4 a = ldg_mesh(p);
+    const int4 b = ldg_mesh(p + 1);
     ElemRec r;
     r.v[0] = a.x; r.v[1] = a.y; r.v[2] = a.z; r.v[3] = a.w;
     r.nb[0] = b.x; r.nb[1] = b.y; r.nb[2] = b.z; r.nb[3] = b.w;
