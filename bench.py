@@ -98,7 +98,7 @@ def config(args, world, ne):
 # clocks sampling during the timed region
 
 class Clocks:
-    """SM clock and clock-event reasons sampled every 10 ms by NVML (a
+    """SM clock and clock-event reasons sampled every 5 ms by NVML (a
     background thread) for the duration of the timed region; nvidia-smi in
     loop mode if NVML is unavailable."""
 
@@ -116,13 +116,13 @@ class Clocks:
         self._p = None
 
     def _nvml_loop(self, nv, h):
-        while not self._stop.is_set():
+        while not self._stop.is_set():  # every 5 ms
             try:
                 self.samples.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
                                      int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))))
             except Exception:
                 pass
-            self._stop.wait(0.01)
+            self._stop.wait(0.005)
 
     def __enter__(self):
         try:
@@ -134,6 +134,10 @@ class Clocks:
             self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
             self._t = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
             self._t.start()
+            t0 = time.time()
+            while not self.samples and time.time() - t0 < 2.0:  # sampler running first
+                time.sleep(0.002)
+            self.samples.clear()  # keep only samples taken inside the region
             return self
         except Exception:
             pass
