@@ -1,21 +1,26 @@
 // b200tally.cu -- B200-native (sm_100a) tet-mesh walk with track-length
-// tallies behind the C ABI declared in include/b200tally.h.
+// tallies behind the C ABI declared in include/b200tally.h: the handle, the
+// host-side move / localization pipelines and every exported entry point.
+// The device code lives in the csrc/*.cuh headers of this translation unit.
 //
 // Replaces the reference's numba hot path:
-//   _sweep_fused + trace_and_score  search.py:169-275, 492-517 -> walk_kernel
-//   initialize_locations            search.py:557-601          -> locate_grid_kernel
-//                                                                 (or walk_kernel + tiebreak_kernel)
+//   _sweep_fused + trace_and_score  search.py:169-275, 492-517 -> walk_staged_kernel (walk.cuh)
+//   _compact_flying + load_step     search.py:160-166,
+//                                   particles.py:57-89          -> stage_kernel (walk.cuh)
+//   initialize_locations            search.py:557-601          -> locate_grid_kernel (locate.cuh)
+//                                                                 (or walk + tiebreak_kernel)
 //   _tie_break_faces                search.py:520-551          -> tiebreak_kernel
-//   _finalize                       tally.py:83-95              -> finalize_kernel
-//   load_step                       particles.py:57-89          -> fused into walk_kernel's fetch
+//   _finalize                       tally.py:83-95              -> finalize_kernel (move_prep.cuh)
 //
 // Design: persistent CTAs, one particle per lane run to
-// completion; idle lanes refill from a global work counter (warp-aggregated
-// atomicAdd) so lanes stay busy despite the exponential crossings-per-move
-// tail; the mesh is one 32-byte record per element (vertex ids + packed
-// neighbour/face) plus 32-byte padded fp64 vertices, L2-resident up to ~3M
-// tets; tallies are fp64 atomics into a private per-GPU grid, optionally
-// aggregated per warp with __match_any_sync.
+// completion; warps refill idle lanes from cp.async-prefetched stages of a
+// compacted work list, so lanes stay busy despite the exponential
+// crossings-per-move tail; the exit search is decided by an fp32 filter with
+// proven margins (fp64 reference arithmetic otherwise); the mesh is one
+// 32-byte record per element (vertex ids + packed neighbour/face) plus 32-byte
+// padded fp64 vertices, L2-resident up to ~3M tets; tallies are fp64 atomics
+// into a private per-GPU grid, warp-aggregated with __match_any_sync where
+// lanes score the same bins.
 #include <cuda_runtime.h>
 
 #include <algorithm>
