@@ -5,7 +5,7 @@
 // ---------------------------------------------------------------------------
 // walk kernels: the fused sweep (search.py:169-275) run to completion per lane
 
-constexpr int DEFAULT_VARIANT = 6;  // see run_walk's variant table
+constexpr int DEFAULT_VARIANT = 6;  // 192 x 2 CTAs/SM: see the launch variant table (b200tally.cu)
 
 // Cold per-lane state (read at events and at the end of a walk) lives in
 // shared memory, one slot per thread: fewer live registers in the hot loop.
@@ -69,10 +69,10 @@ struct Pending {
 };
 
 // One step of search.py:183-274 for a flying lane.  Returns true when the
-// particle stops (reached, leaked, stuck-killed or sweep guard).  When DEFER
-// the segment is left in P (scored by the next step or the loop); otherwise
-// has_score/bin/val are set for an immediate score.
-// DIG = false compiles the per-particle digest bookkeeping out of the loop.
+// particle stops (reached, leaked, stuck-killed or sweep guard).  The step's
+// segment is left in P: scored at the start of the lane's next step (after its
+// loads) or by the loop-level flush.  DIG = false compiles the per-particle
+// digest bookkeeping out of the loop.
 template <bool DIG = true>
 __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& C, Pending& P,
                                           const DigestSlot& DS) {
