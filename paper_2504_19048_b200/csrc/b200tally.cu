@@ -353,6 +353,29 @@ static double pairwise_sum_par(const double* a, int64_t n, int depth) {
     return left + right;
 }
 
+// index of the first group id outside [0, ngroups), or -1; blocks on threads
+static int64_t first_bad_group(const int32_t* g, int64_t n, int32_t ngroups) {
+    const int nt = (int)std::max<int64_t>(
+        1, std::min<int64_t>(std::min(8u, std::max(1u, std::thread::hardware_concurrency())),
+                             n >> 16));
+    std::vector<int64_t> first((size_t)nt, -1);
+    auto scan = [&](int b) {
+        const int64_t lo = n * b / nt, hi = n * (b + 1) / nt;
+        for (int64_t i = lo; i < hi; ++i)
+            if ((uint32_t)g[i] >= (uint32_t)ngroups) {
+                first[(size_t)b] = i;
+                return;
+            }
+    };
+    std::vector<std::thread> th;
+    for (int b = 1; b < nt; ++b) th.emplace_back(scan, b);
+    scan(0);
+    for (auto& t : th) t.join();
+    for (int64_t f : first)
+        if (f >= 0) return f;
+    return -1;
+}
+
 // weights[flying != 0] (numpy boolean-mask order) into `out`, in parallel
 // blocks; returns the selected count, or -1 (out untouched) when every
 // particle is flying and the weights can be summed in place
@@ -905,11 +928,11 @@ bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, cons
     // host-side checks and the recorded source weight (tally.py:262-269)
     bool need_w = h->source_weight == 0.0;
     if (host) {
-        if (groups) {
-            for (int64_t i = 0; i < count; ++i)
-                if (groups[i] < 0 || groups[i] >= h->ngroups)
-                    return set_err(BT_EINDEX, "group %d out of range [0, %d)", groups[i],
-                                   h->ngroups);
+        if (groups) {  // range check before any work, in parallel blocks
+            const int64_t bad = first_bad_group(groups, count, h->ngroups);
+            if (bad >= 0)
+                return set_err(BT_EINDEX, "group %d out of range [0, %d)", groups[bad],
+                               h->ngroups);
         }
     }
     CK(cudaEventRecord(h->ev2, h->stream));
