@@ -961,12 +961,13 @@ bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, cons
     if (host) {
         // pipeline: chunk c's input copies (copy stream) overlap chunk c-1's walk.
         // Chunks grow geometrically (1/2^nch, then 1/2^(nch-1-c) cumulative:
-        // 1/8, 3/8, 1/2 for three) so the first walk starts after a short copy
+        // 1/16, 3/16, 1/4, 1/2 for the default four: measured best of 2..6 chunks,
+        // tools/e2e_breakdown.py) so the first walk starts after a short copy
         // and every later copy still finishes inside the previous chunk's walk.
         WalkArgs a = walk_args(h, h->dest, h->fly, h->weight, true);
         int nch = 1;
         if (h->opt_staged && !h->opt_sort) {
-            nch = h->move_chunks > 0 ? h->move_chunks : (count >= (4 << 20) ? 3 : 1);
+            nch = h->move_chunks > 0 ? h->move_chunks : (count >= (4 << 20) ? 4 : 1);
             nch = (int)std::min<int64_t>(std::min(nch, MAX_CHUNKS), count);
         }
         auto bound = [&](int c) -> int64_t {  // end of chunk c

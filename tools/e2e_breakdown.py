@@ -20,7 +20,7 @@ h_pos = torch.from_numpy(pos).pin_memory().numpy()
 h_dest = torch.from_numpy(dest).pin_memory().numpy()
 h_fly = torch.ones(P, dtype=torch.int8).pin_memory().numpy()
 h_w = torch.ones(P, dtype=torch.float64).pin_memory().numpy()
-mt = MeshTally(m, P)
+mt = MeshTally(m, P, move_chunks=int(sys.argv[1]) if len(sys.argv) > 1 else 0)
 for it in range(4):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
