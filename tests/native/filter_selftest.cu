@@ -97,3 +97,34 @@ extern "C" int64_t bt_contains_selftest(const double* vertices, const int32_t* e
     *fallbacks = fb;
     return mism;
 }
+
+// The fp32 filter's intermediate quantities for n (tet, origin, destination)
+// cases: out[27*i ...] = stage, S, R0(unused), Nx, Dc, t1..t3, y0, Pc, P32,
+// D[4], NT[4], NU[4], NW[4] (tests/test_filter_bounds.py checks them against
+// exact rational determinants of the reference's fp64 vectors).
+extern "C" void bt_f32_probe(const double* tets /* 12 per case: x0..3, y0..3, z0..3 */,
+                             const double* od /* 6 per case */, int64_t n, float* out) {
+    for (int64_t i = 0; i < n; ++i) {
+        Tet T;
+        for (int j = 0; j < 4; ++j) {
+            T.x[j] = tets[12 * i + j];
+            T.y[j] = tets[12 * i + 4 + j];
+            T.z[j] = tets[12 * i + 8 + j];
+        }
+        F32Probe p{};
+        int f = -1;
+        unsigned q = 0;
+        exit_filter32(T, od[6 * i], od[6 * i + 1], od[6 * i + 2], od[6 * i + 3], od[6 * i + 4],
+                      od[6 * i + 5], -1, &f, &q, nullptr, &p);
+        float* o = out + 27 * i;
+        const float head[11] = {(float)p.stage, p.S, p.R0, p.Nx, p.Dc, p.t[0], p.t[1], p.t[2],
+                                p.y0, p.Pc, p.P32};
+        for (int k = 0; k < 11; ++k) o[k] = head[k];
+        for (int k = 0; k < 4; ++k) {
+            o[11 + k] = p.D[k];
+            o[15 + k] = p.NT[k];
+            o[19 + k] = p.NU[k];
+            o[23 + k] = p.NW[k];
+        }
+    }
+}
