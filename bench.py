@@ -385,11 +385,12 @@ def run_ours(args):
     alg_bytes = B_CROSSING * stats["events"] + B_MOVE * stats["moves"]
     achieved = alg_bytes / walk_s / 1e9
     peaks_p = ROOT / "MEASURED_PEAKS.json"
-    if peaks_p.exists():
+    peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    try:
         peak = float(json.loads(peaks_p.read_text())["hbm_gbs"])
-        peak_src = "measured"
-    else:
-        peak, peak_src = 6650.0, "fallback"
+        peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, ValueError, KeyError, TypeError):
+        pass
     traffic = None
     tp = ROOT / "profiles" / "walk_dram_traffic.json"
     if tp.exists():
