@@ -74,7 +74,9 @@ enum {
     BT_OPT_BLOCKS_PER_SM = 4, /* walk register budget: 1..3 resident 256-thread CTAs/SM */
     BT_OPT_STAGED = 5,        /* 1: compact flying particles + cp.async-prefetched refill */
     BT_OPT_MOVE_CHUNKS = 6,   /* host inputs: copy/walk pipeline depth (0 = auto, <= 16) */
-    BT_OPT_LOCATE_LANES = 7   /* grid localization: lanes per particle 1..32 (0 = default 2) */
+    BT_OPT_LOCATE_LANES = 7,  /* grid localization: lanes per particle 1..32 (0 = default 2) */
+    BT_OPT_EXACT_ONLY = 8     /* 1 (with BT_OPT_DIGEST): every exit search in the reference's
+                                 literal arithmetic -- validation of the filters at scale */
 };
 
 /* Mirrors meshtally.search.TraceSummary (search.py:150-157). */

@@ -169,6 +169,7 @@ struct bt_tally {
     bool opt_digest = false;
     bool opt_sort = false;
     int opt_wagg = WAGG_ADAPTIVE;
+    bool opt_exact_only = false;
     bool opt_staged = true;
     WorkSoA work{};
     void* work_mem = nullptr;
@@ -595,6 +596,7 @@ bt_status bt_set_option(bt_tally* h, int32_t key, int64_t value) {
         case BT_OPT_BLOCKS_PER_SM: h->blocks_per_sm = (int)value; break;
         case BT_OPT_STAGED: h->opt_staged = value != 0; break;
         case BT_OPT_MOVE_CHUNKS: h->move_chunks = (int)value; break;
+        case BT_OPT_EXACT_ONLY: h->opt_exact_only = value != 0; break;
         case BT_OPT_LOCATE_LANES:
             if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8 &&
                 value != 16 && value != 32)
@@ -675,6 +677,7 @@ static WalkArgs walk_args(bt_tally* h, const double* dest, const int8_t* fly, co
     a.ngroups = h->ngroups;
     a.score = score ? 1 : 0;
     a.wagg = h->opt_wagg;
+    a.exact_only = h->opt_exact_only ? 1 : 0;
     return a;
 }
 

@@ -51,6 +51,7 @@ struct WalkArgs {
     int32_t ngroups;
     int32_t score;
     int32_t wagg;    // tally atomics: WAGG_ADAPTIVE / WAGG_ALWAYS / WAGG_NEVER
+    int32_t exact_only;  // digest kernels only: literal exit search (filter validation)
 };
 
 #ifndef BT_NO_L2_HINT

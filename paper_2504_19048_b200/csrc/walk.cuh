@@ -106,8 +106,14 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
     int face;
     double t;
     bool exact_used, need_t;
-    int kind = exit_search_fast(T, ox, oy, oz, L.dx(), L.dy(), L.dz(), L.entry, &face, &t, &exact_used,
-                                true, &need_t);
+    int kind;
+    if (DIG && a.exact_only) {  // validation: the reference's literal arithmetic only
+        kind = exit_search(T, ox, oy, oz, L.dx(), L.dy(), L.dz(), L.entry, &face, &t);
+        need_t = false;
+    } else {
+        kind = exit_search_fast(T, ox, oy, oz, L.dx(), L.dy(), L.dz(), L.entry, &face, &t,
+                                &exact_used, true, &need_t);
+    }
     // (neighbour << 2) | its face across the exit face, -1 on the boundary
     const int nbp = (face & 2) ? ((face & 1) ? r.nb[3] : r.nb[2]) : ((face & 1) ? r.nb[1] : r.nb[0]);
     if (kind == 1) {

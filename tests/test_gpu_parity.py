@@ -434,3 +434,43 @@ def test_torus_chained_moves_sampled_parity():
         assert np.array_equal(d[idx], ref.digest) and np.array_equal(c[idx], ref.count), move
         cur = st.position
     mt.close()
+
+
+@pytest.mark.parametrize("mesh_kind", ["cube", "torus"])
+def test_filters_equal_literal_arithmetic_at_scale(mesh_kind):
+    """The walk with its fp32/fp64 filters against the same walk with every exit
+    search in the reference's literal arithmetic (BT_OPT_EXACT_ONLY), on the
+    device, for every particle of a bench-size move: ~5.7e8 (cube) exit searches
+    must take identical decisions -- digests, positions and flags bit-exact."""
+    torch = pytest.importorskip("torch")
+    if mesh_kind == "cube":
+        m = build_cube_mesh(55)
+        gen = synth.rng(synth.SEED + 91)
+        n = 10_000_000
+        pos = synth.uniform_box(gen, n)
+        dest = synth.flight_destinations(gen, pos, 2.0)
+    else:
+        from paper_2504_19048_b200 import build_torus_shell_mesh
+        m = build_torus_shell_mesh(8, 64, 102)
+        gen = synth.rng(synth.SEED + 92)
+        n = 2_000_000
+        el = gen.integers(0, m.num_elements, n)
+        pos = synth.points_in_elements(gen, m.vertices, m.elements, el)
+        dest = synth.flight_destinations(gen, pos, 1.0 / 30.0)
+    res = []
+    for exact in (0, 1):
+        mt = MeshTally(m, n, digest=True)
+        mt.set_option(_lib.BT_OPT_EXACT_ONLY, exact)
+        mt.initialize_particle_location(torch.from_numpy(pos).cuda())
+        s = mt.move_to_next_location(torch.from_numpy(dest).cuda(),
+                                     torch.ones(n, dtype=torch.int8, device="cuda"),
+                                     torch.ones(n, dtype=torch.float64, device="cuda"))
+        res.append((s, mt.read_particles(), mt.read_digest(), mt.batch_totals()))
+        mt.close()
+    (s0, st0, (d0, c0), t0), (s1, st1, (d1, c1), t1) = res
+    assert s0 == s1
+    assert s0.events > 10 * n
+    for k in ("position", "element", "alive", "entry_face", "stuck", "outcome", "seg_total"):
+        assert np.array_equal(getattr(st0, k), getattr(st1, k)), k
+    assert np.array_equal(d0, d1) and np.array_equal(c0, c1)
+    assert rel_close(t0.reshape(-1), t1.reshape(-1), TALLY_RTOL)[0]
