@@ -75,8 +75,9 @@ enum {
     BT_OPT_STAGED = 5,        /* 1: compact flying particles + cp.async-prefetched refill */
     BT_OPT_MOVE_CHUNKS = 6,   /* host inputs: copy/walk pipeline depth (0 = auto, <= 16) */
     BT_OPT_LOCATE_LANES = 7,  /* grid localization: lanes per particle 1..32 (0 = default 2) */
-    BT_OPT_EXACT_ONLY = 8     /* 1 (with BT_OPT_DIGEST): every exit search in the reference's
-                                 literal arithmetic -- validation of the filters at scale */
+    BT_OPT_EXACT_ONLY = 8     /* 1: no fp32 pre-filters -- grid localization tests every
+                                 candidate exactly, and (with BT_OPT_DIGEST) every exit search
+                                 runs the reference's literal arithmetic; for validation */
 };
 
 /* Mirrors meshtally.search.TraceSummary (search.py:150-157). */

@@ -833,6 +833,7 @@ static LocateArgs locate_args(bt_tally* h, const double* target, int64_t count) 
     memcpy(a.c0, h->c0, sizeof a.c0);
     a.count = count;
     a.lo = 0;
+    a.exact_only = h->opt_exact_only ? 1 : 0;
     return a;
 }
 

@@ -163,6 +163,7 @@ struct LocateArgs {
     double c0[3];
     int64_t count;
     int64_t lo;  // locate_grid_kernel: first particle of this launch
+    int32_t exact_only;  // BT_OPT_EXACT_ONLY: every candidate takes the exact test
 };
 
 // elem_contains(p, EPS_BARY) (geometry.py:149-154) decided from the element's
@@ -255,7 +256,7 @@ __global__ void __launch_bounds__(LOCATE_THREADS) locate_grid_kernel(const Locat
         const int k = k0 + gl;
         if (act && k < s1) {
             c = __ldg(a.G.cand + k);
-            const int pre = lambda_prefilter(a.lam + c, q0, q1, q2);
+            const int pre = a.exact_only ? 0 : lambda_prefilter(a.lam + c, q0, q1, q2);
             hit = pre > 0;
             if (pre == 0) {
                 const ElemRec r = load_rec(a.rec, c);

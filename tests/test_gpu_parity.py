@@ -474,3 +474,30 @@ def test_filters_equal_literal_arithmetic_at_scale(mesh_kind):
         assert np.array_equal(getattr(st0, k), getattr(st1, k)), k
     assert np.array_equal(d0, d1) and np.array_equal(c0, c1)
     assert rel_close(t0.reshape(-1), t1.reshape(-1), TALLY_RTOL)[0]
+
+
+def test_localization_prefilter_equals_exact_at_scale():
+    """Grid localization with the fp32 barycentric pre-filter against the same
+    search with every candidate tested exactly (BT_OPT_EXACT_ONLY): identical
+    elements for 1e7 points on C2, a third of them on grid planes, edges and
+    vertices or within 1e-12 of them."""
+    torch = pytest.importorskip("torch")
+    m = build_cube_mesh(55)
+    gen = synth.rng(synth.SEED + 93)
+    n = 10_000_000
+    pts = gen.uniform(0.0, 1.0, (n, 3))
+    grid = np.arange(56) / 55.0
+    for ax in range(3):
+        sel = gen.random(n) < 0.2
+        pts[sel, ax] = grid[gen.integers(0, 56, sel.sum())]
+    near = gen.random(n) < 0.1
+    pts[near] += gen.normal(size=(near.sum(), 3)) * 1e-12
+    out = []
+    for exact in (0, 1):
+        mt = MeshTally(m, n)
+        mt.set_option(_lib.BT_OPT_EXACT_ONLY, exact)
+        mt.initialize_particle_location(torch.from_numpy(pts).cuda())
+        out.append(mt.read_particles().element)
+        mt.close()
+    assert np.array_equal(out[0], out[1])
+    assert (out[0] >= 0).mean() > 0.9
