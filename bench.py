@@ -58,7 +58,8 @@ def parse():
     p.add_argument("--warp-agg", type=int, default=-1,
                    help="tally atomics: -1 adaptive aggregation (default), 0 never, 1 always")
     p.add_argument("--blocks-per-sm", type=int, default=0)
-    p.add_argument("--staged", type=int, default=1)
+    p.add_argument("--staged", type=int, default=-1,
+                   help="refill: -1 library default, 0 v1, 1 stage kernel, 2 direct")
     return p.parse_args()
 
 
@@ -90,7 +91,8 @@ def config(args, world, ne):
               "mesh 38 MB stays L2-resident by design",
         "options": {"sort": bool(args.sort),
                     "warp_agg": ("adaptive" if args.warp_agg < 0 else bool(args.warp_agg)),
-                    "staged": bool(args.staged), "blocks_per_sm": args.blocks_per_sm or "default"},
+                    "staged": "default" if args.staged < 0 else args.staged,
+                    "blocks_per_sm": args.blocks_per_sm or "default"},
     }
 
 
@@ -309,7 +311,7 @@ def run_ours(args):
 
     mt = MeshTally(mesh, P, device=local, sort=bool(args.sort),
                    warp_aggregate=None if args.warp_agg < 0 else bool(args.warp_agg),
-                   staged=bool(args.staged))
+                   staged=True if args.staged < 0 else args.staged)
     if args.blocks_per_sm:
         mt.set_option(_lib.BT_OPT_BLOCKS_PER_SM, args.blocks_per_sm)
     d_pos = torch.from_numpy(pos).to(dev)

@@ -72,7 +72,9 @@ enum {
                                 0 adaptive (default: when a warp's lanes score the same
                                 bins), 1 always, 2 never */
     BT_OPT_BLOCKS_PER_SM = 4, /* walk register budget: 1..3 resident 256-thread CTAs/SM */
-    BT_OPT_STAGED = 5,        /* 1: compact flying particles + cp.async-prefetched refill */
+    BT_OPT_STAGED = 5,        /* refill: 0 v1 (per-lane loads), 1 stage kernel + cp.async work
+                                 list, 2 direct (warp-claimed chunks read from the particle
+                                 arrays, no stage kernel) */
     BT_OPT_MOVE_CHUNKS = 6,   /* host inputs: copy/walk pipeline depth (0 = auto, <= 16) */
     BT_OPT_LOCATE_LANES = 7,  /* grid localization: lanes per particle 1..32 (0 = default 2) */
     BT_OPT_EXACT_ONLY = 8     /* 1: no fp32 pre-filters -- grid localization tests every

@@ -170,7 +170,7 @@ struct bt_tally {
     bool opt_sort = false;
     int opt_wagg = WAGG_ADAPTIVE;
     bool opt_exact_only = false;
-    bool opt_staged = true;
+    int opt_staged = 2;  // 0: v1 refill, 1: stage kernel + work list, 2: direct refill
     WorkSoA work{};
     void* work_mem = nullptr;
     int blocks_per_sm = 0;
@@ -594,7 +594,11 @@ bt_status bt_set_option(bt_tally* h, int32_t key, int64_t value) {
             h->opt_wagg = (int)value;
             break;
         case BT_OPT_BLOCKS_PER_SM: h->blocks_per_sm = (int)value; break;
-        case BT_OPT_STAGED: h->opt_staged = value != 0; break;
+        case BT_OPT_STAGED:
+            if (value < 0 || value > 2)
+                return set_err(BT_EINVAL, "staged must be 0 (v1), 1 (stage kernel) or 2 (direct)");
+            h->opt_staged = (int)value;
+            break;
         case BT_OPT_MOVE_CHUNKS: h->move_chunks = (int)value; break;
         case BT_OPT_EXACT_ONLY: h->opt_exact_only = value != 0; break;
         case BT_OPT_LOCATE_LANES:
@@ -635,17 +639,29 @@ struct HostOverlap {
 static const struct Variant {
     int threads;
     void (*plain)(const WalkArgs);
-    void (*staged)(const WalkArgs, const WorkSoA, const int64_t*);      // digests off
-    void (*staged_dig)(const WalkArgs, const WorkSoA, const int64_t*);  // digests on
+    // [direct][digest]: direct refill or the stage kernel's work list; digests on/off
+    void (*staged[2][2])(const WalkArgs, const WorkSoA, const int64_t*, const DirectArgs);
 } kVariants[] = {
     // launch variant (CTA size, resident CTAs per SM = register budget);
     // BT_OPT_BLOCKS_PER_SM selects it, 0 = the tuned default
-    {256, walk_kernel<256, 1>, walk_staged_kernel<256, 1, false>, walk_staged_kernel<256, 1, true>},  // 1: <=255 regs
-    {256, walk_kernel<256, 2>, walk_staged_kernel<256, 2, false>, walk_staged_kernel<256, 2, true>},  // 2: <=128 regs
-    {256, walk_kernel<256, 3>, walk_staged_kernel<256, 3, false>, walk_staged_kernel<256, 3, true>},  // 3: <=80 regs
-    {128, walk_kernel<128, 3>, walk_staged_kernel<128, 3, false>, walk_staged_kernel<128, 3, true>},  // 4: <=168 regs
-    {128, walk_kernel<128, 4>, walk_staged_kernel<128, 4, false>, walk_staged_kernel<128, 4, true>},  // 5: <=128 regs
-    {192, walk_kernel<192, 2>, walk_staged_kernel<192, 2, false>, walk_staged_kernel<192, 2, true>},  // 6: <=168 regs
+    {256, walk_kernel<256, 1>,
+     {{walk_staged_kernel<256, 1, false, false>, walk_staged_kernel<256, 1, true, false>},
+      {walk_staged_kernel<256, 1, false, true>, walk_staged_kernel<256, 1, true, true>}}},  // 1: <=255 regs
+    {256, walk_kernel<256, 2>,
+     {{walk_staged_kernel<256, 2, false, false>, walk_staged_kernel<256, 2, true, false>},
+      {walk_staged_kernel<256, 2, false, true>, walk_staged_kernel<256, 2, true, true>}}},  // 2: <=128 regs
+    {256, walk_kernel<256, 3>,
+     {{walk_staged_kernel<256, 3, false, false>, walk_staged_kernel<256, 3, true, false>},
+      {walk_staged_kernel<256, 3, false, true>, walk_staged_kernel<256, 3, true, true>}}},  // 3: <=80 regs
+    {128, walk_kernel<128, 3>,
+     {{walk_staged_kernel<128, 3, false, false>, walk_staged_kernel<128, 3, true, false>},
+      {walk_staged_kernel<128, 3, false, true>, walk_staged_kernel<128, 3, true, true>}}},  // 4: <=168 regs
+    {128, walk_kernel<128, 4>,
+     {{walk_staged_kernel<128, 4, false, false>, walk_staged_kernel<128, 4, true, false>},
+      {walk_staged_kernel<128, 4, false, true>, walk_staged_kernel<128, 4, true, true>}}},  // 5: <=128 regs
+    {192, walk_kernel<192, 2>,
+     {{walk_staged_kernel<192, 2, false, false>, walk_staged_kernel<192, 2, true, false>},
+      {walk_staged_kernel<192, 2, false, true>, walk_staged_kernel<192, 2, true, true>}}},  // 6: <=168 regs
 };
 
 static WalkArgs walk_args(bt_tally* h, const double* dest, const int8_t* fly, const double* w,
@@ -696,7 +712,8 @@ static bt_status walk_enqueue(bt_tally* h, WalkArgs a, int64_t lo, int64_t hi, i
     const int64_t count = hi - lo;
     a.count = count;
     a.queue = h->dcounters + 16 + chunk;
-    const bool staged = h->opt_staged;
+    const bool staged = h->opt_staged != 0;
+    const bool direct = h->opt_staged == 2;  // refill straight from the particle arrays
     if (h->opt_sort && a.score) {  // whole move only (lo == 0)
         iota_keys_kernel<<<grid_for(count, 256), 256, 0, st>>>(
             h->element, count, h->sort_keys_in, h->sort_vals_in);
@@ -712,7 +729,7 @@ static bt_status walk_enqueue(bt_tally* h, WalkArgs a, int64_t lo, int64_t hi, i
     const int vi = (h->blocks_per_sm >= 1 && h->blocks_per_sm <= NVAR ? h->blocks_per_sm
                                                                        : DEFAULT_VARIANT) - 1;
     const Variant& V = kVariants[vi];
-    auto* staged_k = a.digest ? V.staged_dig : V.staged;
+    auto* staged_k = V.staged[direct ? 1 : 0][a.digest ? 1 : 0];
     const void* kptr = staged ? (const void*)staged_k : (const void*)V.plain;
     const size_t dyn = staged ? sizeof(WarpStage) * 2 * (V.threads / 32) : 0;
     if (staged) CK(cudaFuncSetAttribute(kptr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
@@ -724,7 +741,10 @@ static bt_status walk_enqueue(bt_tally* h, WalkArgs a, int64_t lo, int64_t hi, i
         (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)bps * h->num_sms));
     int64_t* nwork = reinterpret_cast<int64_t*>(h->dcounters + 32 + chunk);
     WorkSoA W = h->work;
-    if (staged) {
+    DirectArgs D{lo, hi, wsum};
+    if (direct && !a.order) D = DirectArgs{lo, hi, wsum};
+    if (direct && a.order) D = DirectArgs{0, count, wsum};  // sorted: slots index h->order
+    if (staged && !direct) {
         TRY(ensure_work(h));
         W = h->work;
         W.px += lo; W.py += lo; W.pz += lo; W.dx += lo; W.dy += lo; W.dz += lo;
@@ -747,7 +767,7 @@ static bt_status walk_enqueue(bt_tally* h, WalkArgs a, int64_t lo, int64_t hi, i
         h->walk_first = false;
     }
     if (staged)
-        staged_k<<<blocks, V.threads, dyn, st>>>(a, W, nwork);
+        staged_k<<<blocks, V.threads, dyn, st>>>(a, W, nwork, D);
     else
         V.plain<<<blocks, V.threads, 0, st>>>(a);
     CK(cudaGetLastError());

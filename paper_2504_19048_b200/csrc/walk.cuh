@@ -491,9 +491,69 @@ __device__ __forceinline__ int claim_chunk(const WalkArgs& a, const WorkSoA& W, 
     return n;
 }
 
-template <int THREADS, int MINB, bool DIG>
+// Direct refill (no stage kernel, no work list): a warp claims 32 consecutive
+// slots of the move and reads its particles straight from the particle
+// arrays into a stage (plain loads: one latency per 32 particles; measured
+// faster than splitting them into cp.async groups), including the starting
+// element's record.  Flags: bit 24 = walkable (flying and localized), bit 25
+// = flying.  The flying particles' weights are summed per chunk into `wsum`
+// (the recorded source weight of device-input moves).
+struct DirectArgs {
+    int64_t lo, hi;  // particles [lo, hi) of this launch (slots through a.order if set)
+    double* wsum;    // nullable
+};
+
+__device__ __forceinline__ int claim_direct(const WalkArgs& a, const DirectArgs& d, WarpStage& st) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(a.queue, (unsigned long long)STAGE_N);
+    base = __shfl_sync(FULL, base, 0);
+    const int64_t left = (d.hi - d.lo) - (int64_t)base;
+    const int n = left <= 0 ? 0 : (left >= STAGE_N ? STAGE_N : (int)left);
+    double wv = 0.0;
+    if (lane < n) {
+        const int64_t t = (int64_t)base + lane;
+        const int64_t i = a.order ? (int64_t)a.order[t] : d.lo + t;
+        const int fly = a.fly_in[i] != 0;
+        const int el = a.element[i];
+        const bool walk = fly && el >= 0;
+        st.idx[lane] = (int)i;
+        st.px[lane] = a.pos[3 * i];
+        st.py[lane] = a.pos[3 * i + 1];
+        st.pz[lane] = a.pos[3 * i + 2];
+        st.dx[lane] = a.dest[3 * i];
+        st.dy[lane] = a.dest[3 * i + 1];
+        st.dz[lane] = a.dest[3 * i + 2];
+        const double w = a.score ? a.weight[i] : 0.0;
+        st.w[lane] = w;
+        if (fly) wv = w;
+        st.seg[lane] = a.seg_total[i];
+        st.e[lane] = el;
+        st.g[lane] = a.score ? a.group[i] : 0;
+        st.fl[lane] = ((int)(unsigned char)a.entry[i]) | ((int)(unsigned char)a.stuck[i] << 8) |
+                      ((int)(unsigned char)(a.alive[i] | a.fly_in[i]) << 16) |  // load_step
+                      (walk ? 1 << 24 : 0) | (fly ? 1 << 25 : 0);
+        if (walk) {
+            const int4* rp = reinterpret_cast<const int4*>(a.rec + el);
+            st.r0[lane] = ldg_mesh(rp);
+            st.r1[lane] = ldg_mesh(rp + 1);
+        }
+    }
+    if (d.wsum) {
+        for (int o = 16; o > 0; o >>= 1) wv += __shfl_xor_sync(FULL, wv, o);
+        if (lane == 0 && wv != 0.0) atomicAdd(d.wsum, wv);
+    }
+    __syncwarp();
+    return n;
+}
+
+// DIRECT: stages filled by claim_direct from the particle arrays; otherwise
+// from the stage kernel's work list with cp.async (claim_chunk).
+template <int THREADS, int MINB, bool DIG, bool DIRECT>
 __global__ void __launch_bounds__(THREADS, MINB)
-    walk_staged_kernel(const WalkArgs a, const WorkSoA W, const int64_t* __restrict__ nwork_p) {
+    walk_staged_kernel(const WalkArgs a, const WorkSoA W, const int64_t* __restrict__ nwork_p,
+                       const DirectArgs D) {
     static_assert(THREADS <= MAX_CTA_THREADS, "one shared lane slot per thread");
     constexpr unsigned FULL = 0xffffffffu;
     // the warps' double-buffered stages: dynamic shared memory (with the lane
@@ -506,7 +566,10 @@ __global__ void __launch_bounds__(THREADS, MINB)
     counters_init(shc);
     const DigestSlot DS{sdig + threadIdx.x, scnt + threadIdx.x};
     const int wid = threadIdx.x >> 5;
-    const int64_t nwork = *nwork_p;
+    const int64_t nwork = DIRECT ? 0 : *nwork_p;
+    auto claim = [&](WarpStage& st) -> int {
+        return DIRECT ? claim_direct(a, D, st) : claim_chunk(a, W, st, nwork);
+    };
     Lane L;
     L.busy = false;
     Counters C;
@@ -514,8 +577,8 @@ __global__ void __launch_bounds__(THREADS, MINB)
     Pending P;
     int cur = 0;
     int head = 0;
-    int ncur = claim_chunk(a, W, stages[wid][0], nwork);
-    int nnext = ncur == STAGE_N ? claim_chunk(a, W, stages[wid][1], nwork) : 0;
+    int ncur = claim(stages[wid][0]);
+    int nnext = ncur == STAGE_N ? claim(stages[wid][1]) : 0;
     // only the first group must have landed; wait_group 1 would do, but the
     // second claim may be empty -- a full wait costs one DRAM latency once
     cp_async_wait_all();
@@ -531,14 +594,24 @@ __global__ void __launch_bounds__(THREADS, MINB)
                 head = 0;
                 ncur = nnext;
                 // the stage just emptied is free: prefetch the chunk after next
-                nnext = (ncur == STAGE_N) ? claim_chunk(a, W, stages[wid][cur ^ 1], nwork) : 0;
+                nnext = (ncur == STAGE_N) ? claim(stages[wid][cur ^ 1]) : 0;
             }
             const int take = min((int)__popc(idle), ncur - head);
             if (!L.busy) {
                 const int rk = __popc(idle & lanemask_lt());
-                if (rk < take) {
-                    const WarpStage& s = stages[wid][cur];
-                    const int j = head + rk;
+                const WarpStage& s = stages[wid][cur];
+                const int j = head + rk;
+                const int fl0 = rk < take ? s.fl[j] : 0;
+                if (DIRECT && rk < take && !(fl0 & (1 << 24))) {
+                    // not walked: a non-flying particle (empty digest) or a flying
+                    // one that was never localized (counted, reported by the move)
+                    if (fl0 & (1 << 25)) {
+                        atomicAdd(a.counters + C_UNLOC, 1ull);
+                    } else if (DIG && a.digest) {
+                        a.digest[s.idx[j]] = DIGEST_INIT;
+                        a.dcount[s.idx[j]] = 0;
+                    }
+                } else if (rk < take) {
                     L.set_idx(s.idx[j]);
                     L.px = s.px[j];
                     L.py = s.py[j];

@@ -219,7 +219,7 @@ class MeshTally:
 
     def __init__(self, mesh, num_particles: int, num_groups: int = 1, threads: int = 1, *,
                  device: int = 0, localize: str = "grid", digest: bool = False,
-                 sort: bool = False, warp_aggregate: bool | None = None, staged: bool = True,
+                 sort: bool = False, warp_aggregate: bool | None = None, staged: bool | int = True,
                  move_chunks: int = 0):
         if isinstance(mesh, (str, Path)):
             mesh = read_tetmesh(mesh)
@@ -259,7 +259,10 @@ class MeshTally:
         # None: adaptive (aggregate while a warp's lanes score the same bins)
         self.set_option(_lib.BT_OPT_WARP_AGG,
                         0 if warp_aggregate is None else (1 if warp_aggregate else 2))
-        self.set_option(_lib.BT_OPT_STAGED, int(staged))
+        # staged: True -> the library's default refill, False -> v1, 1 / 2 -> stage
+        # kernel / direct refill explicitly
+        if staged is not True:
+            self.set_option(_lib.BT_OPT_STAGED, int(staged))
         self.set_option(_lib.BT_OPT_MOVE_CHUNKS, int(move_chunks))
         self._grid = TallyGrid(self)
 

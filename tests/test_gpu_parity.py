@@ -93,7 +93,8 @@ def test_walk_matches_reference_grid_localize(name):
                                   dict(staged=False), dict(staged=False, sort=True,
                                                            warp_aggregate=True),
                                   dict(move_chunks=3), dict(move_chunks=16, warp_aggregate=True),
-                                  dict(warp_aggregate=False)])
+                                  dict(warp_aggregate=False), dict(staged=1), dict(staged=2),
+                                  dict(staged=2, sort=True), dict(staged=2, move_chunks=5)])
 def test_walk_options_keep_parity(opts):
     _check_case(load_walk_case("c1_point_s2"), "grid", **opts)
     _check_case(load_walk_case("n6_uniform_g3"), "grid", **opts)
@@ -218,7 +219,8 @@ def test_full_size_c2_against_oracle(sigma_t):
 
 
 @pytest.mark.parametrize("opts", [{}, dict(sort=True), dict(staged=False),
-                                  dict(warp_aggregate=True), dict(warp_aggregate=False)])
+                                  dict(warp_aggregate=True), dict(warp_aggregate=False),
+                                  dict(staged=1), dict(staged=2), dict(staged=2, sort=True)])
 def test_device_pointer_path_equals_host_path(opts):
     torch = pytest.importorskip("torch")
     case = load_walk_case("n6_uniform_g3")

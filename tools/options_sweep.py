@@ -33,7 +33,8 @@ point = torch.tensor([[0.5123456789, 0.4876543211, 0.5031415926]], dtype=torch.f
                      device=dev).expand(n, 3).contiguous()
 OPTS = [("default", {}), ("sort", {"sort": True}),
         ("warp_aggregate_always", {"warp_aggregate": True}),
-        ("warp_aggregate_never", {"warp_aggregate": False}), ("unstaged", {"staged": False})]
+        ("warp_aggregate_never", {"warp_aggregate": False}), ("unstaged", {"staged": False}),
+        ("stage_kernel", {"staged": 1}), ("direct", {"staged": 2})]
 res = []
 for src_name, src in (("uniform", uniform), ("point", point)):
     for sigma in (2.0, 100.0):
