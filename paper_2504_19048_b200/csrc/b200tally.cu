@@ -707,13 +707,28 @@ static bt_status walk_begin(bt_tally* h) {
 // enqueue stage + walk of particles [lo, hi) as chunk `chunk` (staged path),
 // or the whole range with the v1 kernel / element-sorted hand-out
 static bt_status walk_enqueue(bt_tally* h, WalkArgs a, int64_t lo, int64_t hi, int chunk,
-                              double* wsum, cudaStream_t st = nullptr) {
+                              double* wsum, cudaStream_t st = nullptr, bool pick_refill = false) {
     if (!st) st = h->stream;
     const int64_t count = hi - lo;
     a.count = count;
     a.queue = h->dcounters + 16 + chunk;
     const bool staged = h->opt_staged != 0;
-    const bool direct = h->opt_staged == 2;  // refill straight from the particle arrays
+    // direct refill straight from the particle arrays, except: element-sorted
+    // hand-out (its gathers would be random), and -- when the caller lets us
+    // look (single-launch moves) -- moves where fewer than half the slots walk
+    // (chained moves after most particles leaked), where compacting first wins
+    bool direct = h->opt_staged == 2 && !(h->opt_sort && a.score);
+    if (direct && pick_refill && count >= (1 << 16)) {
+        CK(cudaMemsetAsync(h->dcounters + 14, 0, sizeof(unsigned long long), st));
+        count_walkable_kernel<<<std::min<int64_t>(grid_for(count, 256), 1184), 256, 0, st>>>(
+            a.fly_in + lo, h->element + lo, count, h->dcounters + 14);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(h->hcounters + 14, h->dcounters + 14, sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        h->kernels += 1;
+        direct = 2 * (int64_t)h->hcounters[14] >= count;
+    }
     if (h->opt_sort && a.score) {  // whole move only (lo == 0)
         iota_keys_kernel<<<grid_for(count, 256), 256, 0, st>>>(
             h->element, count, h->sort_keys_in, h->sort_vals_in);
@@ -1044,7 +1059,7 @@ bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, cons
         WalkArgs a = walk_args(h, destinations, flying, weights, true);
         if (need_w) CK(cudaMemsetAsync(h->dwsum, 0, sizeof(double), h->stream));
         TRY(walk_begin(h));
-        TRY(walk_enqueue(h, a, 0, count, 0, need_w ? h->dwsum : nullptr));
+        TRY(walk_enqueue(h, a, 0, count, 0, need_w ? h->dwsum : nullptr, nullptr, true));
         s = walk_end(h, a.max_sweeps, summary);
         if (need_w) {
             double dw = 0.0;

@@ -17,7 +17,8 @@ struct __align__(32) Vtx {
 static_assert(sizeof(Vtx) == 32, "one 32-byte sector per vertex");
 
 enum { C_EVENTS = 0, C_REACHED, C_BOUNDARY, C_RECOV, C_KILLED, C_SWEEPS, C_ERR, C_UNLOC, C_NCOUNTERS };
-// dcounters layout (unsigned long long): [1..8] counters, [15] flags,
+// dcounters layout (unsigned long long): [1..8] counters, [14] walkable count
+// (refill choice), [15] flags,
 // [16 + c] queue of chunk c, [32 + c] work count of chunk c, c < MAX_CHUNKS
 constexpr int MAX_CHUNKS = 16;
 constexpr int NDCOUNTERS = 48;

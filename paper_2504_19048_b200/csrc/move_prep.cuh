@@ -45,3 +45,15 @@ __global__ void iota_keys_kernel(const int32_t* __restrict__ element, int64_t co
     keys[i] = (unsigned)(element[i] + 1);
     vals[i] = (int32_t)i;
 }
+
+// walkable particles of a move (flying and localized): picks the refill mode
+__global__ void count_walkable_kernel(const int8_t* __restrict__ fly,
+                                      const int32_t* __restrict__ element, int64_t n,
+                                      unsigned long long* __restrict__ out) {
+    unsigned c = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        c += fly[i] != 0 && element[i] >= 0;
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
+}
