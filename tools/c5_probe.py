@@ -27,7 +27,11 @@ for st in [int(a) for a in (sys.argv[1:] or ["1", "2"])]:
     gen.manual_seed(20261017)
     w = torch.ones(n, dtype=torch.float64, device=dev)
     for rep in range(2):
+        torch.cuda.synchronize()
+        tb0 = time.perf_counter()
         mt.initialize_particle_location(pts)
+        torch.cuda.synchronize()
+        tinit = time.perf_counter() - tb0
         pos_t, _, alive_t = mt.particle_tensors()
         rows = []
         for mv in range(10):
@@ -42,6 +46,9 @@ for st in [int(a) for a in (sys.argv[1:] or ["1", "2"])]:
             wk, call, kern = mt.last_timing()
             rows.append((nf, round(wk, 3), round(call, 3), round(1e3 * (t1 - t0), 3), kern))
         mt.finalize_batch()
+        torch.cuda.synchronize()
+        tbatch = time.perf_counter() - tb0
         if rep == 1:
-            print(f"staged={st}", rows, flush=True)
+            print(f"staged={st} init {1e3 * tinit:.2f} ms batch {1e3 * tbatch:.2f} ms moves "
+                  f"{sum(r[3] for r in rows):.2f} ms", rows, flush=True)
     mt.close()
