@@ -7,7 +7,8 @@ required to stay inside the bound the margins are built on.
 
 Claims checked (u = 2^-24, P32 = Nx^2 (S + Nx), Pc = Nx^2 (S + 2 Nx)):
   face D, NT, NU, NW:           |err| <= 14.1 u P32
-  containment y0 = |Dc|-t1-t2-t3: |err| <= 37 u Pc  (t_k, Dc inside the same)
+  containment t_k = b.n_k (= D_k - NT_k) and y0 = |Dc|-t1-t2-t3 (= sign(Dc) (NT0 - D0)):
+                                |err| <= 29.3 u P32 <= 37 u Pc  (the margin is 48 u Pc)
 """
 import ctypes as C
 from fractions import Fraction as Fr
@@ -51,7 +52,7 @@ def check(L, V, o, d):
     od = np.ascontiguousarray(np.concatenate([o, d], axis=1))
     out = np.zeros((k, 27), np.float32)
     L.bt_f32_probe(tets.ctypes.data, od.ctypes.data, k, out.ctypes.data)
-    worst = {"face": 0.0, "y0": 0.0}
+    worst = {"face": 0.0, "y0": 0.0, "cont32": 0.0}
     for i in range(k):
         p = out[i]
         if p[0] < 1:
@@ -63,12 +64,13 @@ def check(L, V, o, d):
         N = [det(b, a[1], a[2]), det(a[0], b, a[2]), det(a[0], a[1], b)]
         sg = 1 if Dc >= 0 else -1
         y0 = sg * (Dc - N[0] - N[1] - N[2])
-        Pc = float(p[9])
+        Pc, P32 = float(p[9]), float(p[10])
         worst["y0"] = max(worst["y0"], abs(float(Fr(float(p[8])) - y0)) / (U * Pc))
+        for got, e in zip((p[5], p[6], p[7], p[8]), (sg * N[0], sg * N[1], sg * N[2], y0)):
+            worst["cont32"] = max(worst["cont32"], abs(float(Fr(float(got)) - e)) / (U * P32))
         if p[0] < 2:
             continue
         s = sub(d[i], o[i])
-        P32 = float(p[10])
         for f, (ia, ib, ic) in enumerate(FV):
             e1, e2, r = sub(v[ia], v[ib]), sub(v[ia], v[ic]), sub(v[ia], o[i])
             exact = (det(s, e1, e2), det(r, e1, e2), det(s, r, e2), det(s, e1, r))
@@ -97,3 +99,4 @@ def test_fp32_filter_error_bounds(_lib_fixture, name):
     w = check(L, V, o, d)
     assert w["face"] <= 14.1, w
     assert w["y0"] <= 37.0, w
+    assert w["cont32"] <= 29.3, w
