@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(THREADS, MINB) transport_kernel(const Transpor
                         rb = t.rng_block[i];
                         L.entry = -1;
                         L.st = 0;
-                        L.have_nr = false;  // a new history: load its element's record
+                        L.nr = load_rec(a.rec, L.e);  // a new history: its element's record
                         rounds = 0;
                         need_flight = true;
                     }

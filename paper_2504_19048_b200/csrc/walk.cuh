@@ -20,8 +20,7 @@ __shared__ int8_t s_lane_alive[MAX_CTA_THREADS];
 
 // one particle's walk state while it flies
 struct Lane {
-    ElemRec nr;   // prefetched record of the element entered next
-    bool have_nr;
+    ElemRec nr;   // record of element e (loaded one step ahead, or at the refill)
     bool busy;    // false: lane idle
     double px, py, pz;
     int e, entry, st, iters;
@@ -76,9 +75,7 @@ struct Pending {
 template <bool DIG = true>
 __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& C, Pending& P,
                                           const DigestSlot& DS) {
-    if (!L.have_nr) L.nr = load_rec(a.rec, L.e);  // not prefetched: first step after a hop
     const ElemRec r = L.nr;
-    L.have_nr = false;
     Tet T;
     load_tet(a, r, T);
     // the previous step's score and seg_total update, while this step's
@@ -116,13 +113,12 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
     }
     // (neighbour << 2) | its face across the exit face, -1 on the boundary
     const int nbp = (face & 2) ? ((face & 1) ? r.nb[3] : r.nb[2]) : ((face & 1) ? r.nb[1] : r.nb[0]);
+    // the next step's record, issued now so it lands while the exact t
+    // division and the commit below run; on the paths where the particle
+    // stays (reached, stuck) it is the current element's again, so the
+    // loop-carried record has a single definition (no register copies)
+    L.nr = load_rec(a.rec, (kind == 1 && nbp >= 0) ? (nbp >> 2) : L.e);
     if (kind == 1) {
-        // issue the next element's record load now: it lands while the exact
-        // t division and the commit below run
-        if (nbp >= 0) {
-            L.nr = load_rec(a.rec, nbp >> 2);
-            L.have_nr = true;
-        }
         if (need_t)
             t = exact_t(T, face, ox, oy, oz, rn_sub(L.dx(), ox), rn_sub(L.dy(), oy), rn_sub(L.dz(), oz));
     }
@@ -152,6 +148,7 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
             event = false;
             if (hop >= 0) {
                 L.e = hop;
+                L.nr = load_rec(a.rec, hop);
                 L.entry = -1;
                 L.st = 2;
                 atomicAdd(C.sh + SC_RECOV, 1u);
@@ -203,9 +200,7 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
             atomicAdd(C.sh + SC_REACHED, 1u);
             done = true;
             // the particle stays in this element: a following flight (transport)
-            // starts without the dependent record load
-            L.nr = r;
-            L.have_nr = true;
+            // starts with its record already loaded (above)
         } else {
             if (nbp < 0) {
                 L.outcome() = OUT_LEAKED;
@@ -253,7 +248,6 @@ __device__ __forceinline__ void finish(const WalkArgs& a, Lane& L, Counters& C,
 
 template <bool DIG = true>
 __device__ __forceinline__ void begin(Lane& L, const WalkArgs& a, const DigestSlot& DS) {
-    L.have_nr = false;
     L.iters = 0;
     if (DIG && a.digest) {
         *DS.d = DIGEST_INIT;
@@ -396,6 +390,7 @@ __global__ void __launch_bounds__(THREADS, MINB) walk_kernel(const WalkArgs a) {
                             L.w() = a.score ? a.weight[i] : 0.0;
                             L.g() = a.score ? a.group[i] : 0;
                             begin(L, a, DS);
+                            L.nr = load_rec(a.rec, L.e);
                             L.alive() = (int8_t)(a.alive[i] | a.fly_in[i]);
                         }
                     }
@@ -632,7 +627,6 @@ __global__ void __launch_bounds__(THREADS, MINB)
                     const int4 q0 = s.r0[j], q1 = s.r1[j];
                     L.nr.v[0] = q0.x; L.nr.v[1] = q0.y; L.nr.v[2] = q0.z; L.nr.v[3] = q0.w;
                     L.nr.nb[0] = q1.x; L.nr.nb[1] = q1.y; L.nr.nb[2] = q1.z; L.nr.nb[3] = q1.w;
-                    L.have_nr = true;
                 }
             }
             head += take;
