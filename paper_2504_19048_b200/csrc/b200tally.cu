@@ -662,6 +662,11 @@ static const struct Variant {
     {192, walk_kernel<192, 2>,
      {{walk_staged_kernel<192, 2, false, false>, walk_staged_kernel<192, 2, true, false>},
       {walk_staged_kernel<192, 2, false, true>, walk_staged_kernel<192, 2, true, true>}}},  // 6: <=168 regs
+#ifdef BT_EXTRA_VARIANT  // experiments: -DBT_EXTRA_VARIANT -DBT_XV_T=224 -DBT_XV_B=2 -> variant 7
+    {BT_XV_T, walk_kernel<BT_XV_T, BT_XV_B>,
+     {{walk_staged_kernel<BT_XV_T, BT_XV_B, false, false>, walk_staged_kernel<BT_XV_T, BT_XV_B, true, false>},
+      {walk_staged_kernel<BT_XV_T, BT_XV_B, false, true>, walk_staged_kernel<BT_XV_T, BT_XV_B, true, true>}}},
+#endif
 };
 
 static WalkArgs walk_args(bt_tally* h, const double* dest, const int8_t* fly, const double* w,

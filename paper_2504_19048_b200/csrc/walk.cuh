@@ -9,7 +9,10 @@ constexpr int DEFAULT_VARIANT = 6;  // 192 x 2 CTAs/SM: see the launch variant t
 
 // Cold per-lane state (read at events and at the end of a walk) lives in
 // shared memory, one slot per thread: fewer live registers in the hot loop.
-constexpr int MAX_CTA_THREADS = 256;
+#ifndef BT_MAX_CTA_THREADS
+#define BT_MAX_CTA_THREADS 256
+#endif
+constexpr int MAX_CTA_THREADS = BT_MAX_CTA_THREADS;
 __shared__ double s_lane_w[MAX_CTA_THREADS];
 __shared__ double s_lane_seg[MAX_CTA_THREADS];
 __shared__ int64_t s_lane_idx[MAX_CTA_THREADS];
