@@ -635,7 +635,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
             head += take;
             idle = __ballot_sync(FULL, !L.busy);
         }
-        if (!__any_sync(FULL, L.busy)) {  // no work left anywhere for this warp
+        if (idle == FULL) {  // no work left anywhere for this warp (idle is current here)
             flush_pending(a, P, true);
             break;
         }
