@@ -95,6 +95,8 @@ struct bt_tally {
     // mesh
     ElemRec* rec = nullptr;
     Vtx* vtx = nullptr;
+    XRec* xrec = nullptr;  // crossing records (walk)
+    uint2* xsel = nullptr;
     // grid
     GridDev grid{};
     int* cell_start = nullptr;
@@ -193,7 +195,7 @@ static bt_status ensure_device(bt_tally* h) {
     } while (0)
 
 static bt_status free_all(bt_tally* h) {
-    void* ptrs[] = {h->rec, h->vtx, h->cell_start, h->cand, h->lam, h->pos, h->element, h->alive,
+    void* ptrs[] = {h->rec, h->vtx, h->xrec, h->xsel, h->cell_start, h->cand, h->lam, h->pos, h->element, h->alive,
                     h->entry, h->stuck, h->outcome, h->seg_total, h->group, h->dest, h->fly,
                     h->weight, h->digest, h->dcount, h->order, h->sort_keys_in,
                     h->sort_keys_out, h->sort_vals_in, h->sort_tmp, h->tally, h->sum,
@@ -510,6 +512,16 @@ bt_status bt_create(const double* vertices, int64_t num_vertices, const int32_t*
         TRYF(dalloc(&h->vtx, num_vertices));
         CKF(cudaMemcpy(h->rec, hr.data(), sizeof(ElemRec) * hr.size(), cudaMemcpyHostToDevice));
         CKF(cudaMemcpy(h->vtx, hv.data(), sizeof(Vtx) * hv.size(), cudaMemcpyHostToDevice));
+        TRYF(dalloc(&h->xrec, num_elements));
+        TRYF(dalloc(&h->xsel, num_elements));
+        unsigned long long* dbad = nullptr;
+        TRYF(dalloc(&dbad, 1));
+        CKF(cudaMemset(dbad, 0, sizeof(unsigned long long)));
+        xrec_kernel<<<grid_for(num_elements, 256), 256>>>(h->rec, num_elements, h->xrec, h->xsel, dbad);
+        unsigned long long bad = 0;
+        CKF(cudaMemcpy(&bad, dbad, sizeof(bad), cudaMemcpyDeviceToHost));
+        cudaFree(dbad);
+        if (bad) return fail(set_err(BT_EINVAL, "adjacency: a neighbour does not share the face's vertices"));
     }
     // ---- particles / staging / tallies
     const int64_t n = num_particles;
@@ -616,15 +628,15 @@ static bt_status ensure_work(bt_tally* h) {
     if (h->work_mem) return BT_OK;
     const size_t n = (size_t)h->cap;
     char* p = nullptr;
-    CK(cudaMalloc((void**)&p, n * (8 * sizeof(double) + 2 * sizeof(int4) + 4 * sizeof(int)) + 256));
+    CK(cudaMalloc((void**)&p, n * (8 * sizeof(double) + sizeof(int4) + 4 * sizeof(int)) + 256));
     h->work_mem = p;
     WorkSoA& W = h->work;
     double* d = reinterpret_cast<double*>(p);
     W.px = d; W.py = d + n; W.pz = d + 2 * n; W.dx = d + 3 * n; W.dy = d + 4 * n;
     W.dz = d + 5 * n; W.w = d + 6 * n; W.seg = d + 7 * n;
     int4* r = reinterpret_cast<int4*>(d + 8 * n);
-    W.r0 = r; W.r1 = r + n;
-    int* q = reinterpret_cast<int*>(r + 2 * n);
+    W.r0 = r;
+    int* q = reinterpret_cast<int*>(r + n);
     W.idx = q; W.e = q + n; W.g = q + 2 * n; W.fl = q + 3 * n;
     return BT_OK;
 }
@@ -674,6 +686,8 @@ static WalkArgs walk_args(bt_tally* h, const double* dest, const int8_t* fly, co
     WalkArgs a;
     a.rec = h->rec;
     a.vtx = h->vtx;
+    a.xrec = h->xrec;
+    a.xsel = h->xsel;
     a.pos = h->pos;
     a.dest = dest;
     a.fly_in = fly;
@@ -768,7 +782,7 @@ static bt_status walk_enqueue(bt_tally* h, WalkArgs a, int64_t lo, int64_t hi, i
         TRY(ensure_work(h));
         W = h->work;
         W.px += lo; W.py += lo; W.pz += lo; W.dx += lo; W.dy += lo; W.dz += lo;
-        W.r0 += lo; W.r1 += lo;
+        W.r0 += lo;
         W.w += lo; W.seg += lo; W.idx += lo; W.e += lo; W.g += lo; W.fl += lo;
         stage_kernel<<<grid_for(count, 256), 256, 0, st>>>(a, W, nwork, lo, wsum);
         CK(cudaGetLastError());

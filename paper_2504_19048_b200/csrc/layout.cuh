@@ -16,6 +16,20 @@ struct __align__(32) Vtx {
 };
 static_assert(sizeof(Vtx) == 32, "one 32-byte sector per vertex");
 
+// Crossing record: per face f of an element, the neighbour
+// across f ((nb << 2) | nf, -1 on the boundary) and the one vertex of the
+// neighbour that is not on f (its local vertex nf).  The other three are
+// the element's own, so a crossing fetches ONE vertex, at the same time as
+// the neighbour's record, instead of record -> four vertices.  sel[f] maps
+// the neighbour's local vertex order onto the element's: nibble k = the
+// element's local index of the neighbour's vertex k (f itself for k = nf,
+// whose slot receives the new vertex) -- a __byte_perm selector.
+struct __align__(16) XRec {
+    int nbp[4];
+    int nv[4];
+};
+static_assert(sizeof(XRec) == 32, "one 32-byte sector per element");
+
 enum { C_EVENTS = 0, C_REACHED, C_BOUNDARY, C_RECOV, C_KILLED, C_SWEEPS, C_ERR, C_UNLOC, C_NCOUNTERS };
 // dcounters layout (unsigned long long): [1..8] counters, [14] walkable count
 // (refill choice), [15] flags,
@@ -29,6 +43,8 @@ enum { WAGG_ADAPTIVE = 0, WAGG_ALWAYS = 1, WAGG_NEVER = 2 };
 struct WalkArgs {
     const ElemRec* __restrict__ rec;
     const Vtx* __restrict__ vtx;
+    const XRec* __restrict__ xrec;       // (E) crossing records
+    const uint2* __restrict__ xsel;      // (E) their sel[4], 4 x 16 bits
     double* __restrict__ pos;            // (N,3) persistent
     const double* __restrict__ dest;     // (count,3) this move's destinations
     const int8_t* __restrict__ fly_in;   // (count) this move's flying flags

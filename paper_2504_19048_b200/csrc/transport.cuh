@@ -120,10 +120,12 @@ __global__ void __launch_bounds__(THREADS, MINB) transport_kernel(const Transpor
     const WalkArgs& a = t.w;
     const int lane = threadIdx.x & 31;
     __shared__ unsigned shc[SC_N];
+    VSLOTS_DECL(THREADS)
     counters_init(shc);
     const DigestSlot DS{nullptr, nullptr};
     Lane L;
     L.busy = false;
+    VSLOTS_INIT(L);
     Counters C;
     C.sh = shc;
     Pending P;
@@ -161,7 +163,7 @@ __global__ void __launch_bounds__(THREADS, MINB) transport_kernel(const Transpor
                         rb = t.rng_block[i];
                         L.entry = -1;
                         L.st = 0;
-                        L.nr = load_rec(a.rec, L.e);  // a new history: its element's record
+                        vslots_fill(a, L, L.e, elem_vids(a, L.e));  // a new history
                         rounds = 0;
                         need_flight = true;
                     }

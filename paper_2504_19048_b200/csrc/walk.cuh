@@ -17,10 +17,36 @@ __shared__ int64_t s_lane_idx[MAX_CTA_THREADS];
 __shared__ int8_t s_lane_outcome[MAX_CTA_THREADS];
 __shared__ int8_t s_lane_alive[MAX_CTA_THREADS];
 
+// crossing record of one element, as held by a lane
+struct XR {
+    int nbp[4], nv[4];
+    uint2 sel;
+};
+__device__ __forceinline__ XR load_xr(const WalkArgs& a, int e) {
+    const int4* p = reinterpret_cast<const int4*>(a.xrec + e);
+    const int4 u = ldg_mesh(p), v = ldg_mesh(p + 1);
+    XR r;
+    r.nbp[0] = u.x; r.nbp[1] = u.y; r.nbp[2] = u.z; r.nbp[3] = u.w;
+    r.nv[0] = v.x; r.nv[1] = v.y; r.nv[2] = v.z; r.nv[3] = v.w;
+    r.sel = __ldg(a.xsel + e);
+    return r;
+}
+__device__ __forceinline__ void cpa8(unsigned dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src));
+}
+__device__ __forceinline__ double lds64(unsigned ad) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(ad));
+    return v;
+}
+
 // one particle's walk state while it flies
 struct Lane {
-    ElemRec nr;   // record of element e (loaded one step ahead, or at the refill)
-    bool busy;    // false: lane idle
+    XR nr;          // crossing record of element e (loaded one step ahead)
+    unsigned pm;    // byte k = the shared-memory slot holding local vertex k
+    unsigned vsb;   // this lane's vertex slots: x of slot 0 (shared address)
+    unsigned vss;   // slot stride in bytes (coordinate stride = 4 * vss)
+    bool busy;      // false: lane idle
     double px, py, pz;
     int e, entry, st, iters;
     // weight, group, seg_total and destination in registers: the peak
@@ -42,6 +68,36 @@ struct Lane {
         busy = true;
     }
 };
+
+// start copying element e's four vertices into the lane's slots (identity
+// order) and load its crossing record; the next walk_step waits for them
+__device__ __forceinline__ void vslots_fill(const WalkArgs& a, Lane& L, int e, const int4 v) {
+    const int vid[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double* g = &a.vtx[vid[k]].x;
+        const unsigned ad = L.vsb + k * L.vss;
+        cpa8(ad, g);
+        cpa8(ad + 4 * L.vss, g + 1);
+        cpa8(ad + 8 * L.vss, g + 2);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    L.pm = 0x03020100u;
+    L.nr = load_xr(a, e);
+}
+__device__ __forceinline__ int4 elem_vids(const WalkArgs& a, int e) {
+    return ldg_mesh(reinterpret_cast<const int4*>(a.rec + e));
+}
+// shared-memory vertex slots of a kernel with THREADS threads
+#define VSLOTS_DECL(THREADS)                                                   \
+    __shared__ double s_vslots[3 * 4 * (THREADS)];                                \
+    const unsigned vsb0 = (unsigned)__cvta_generic_to_shared(s_vslots + threadIdx.x); \
+    constexpr unsigned VSS = 8u * (THREADS);
+#define VSLOTS_INIT(L) \
+    do {                  \
+        (L).vsb = vsb0;   \
+        (L).vss = VSS;    \
+    } while (0)
 
 // this thread's digest slot in shared memory (digest mode only; keeps the
 // sequence hash out of the hot loop's registers)
@@ -77,11 +133,20 @@ struct Pending {
 template <bool DIG = true>
 __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& C, Pending& P,
                                           const DigestSlot& DS) {
-    const ElemRec r = L.nr;
+    const XR r = L.nr;
     Tet T;
-    load_tet(a, r, T);
-    // the previous step's score and seg_total update, while this step's
-    // vertex loads are in flight (warp-aggregated mode scores at loop level)
+    // this element's vertices: three stayed in the lane's slots from the
+    // previous element, the fourth was copied in (cp.async) when the previous
+    // step chose its exit face -- one gather per crossing, issued a step ahead
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const unsigned ad = L.vsb + ((L.pm >> (8 * k)) & 0xffu) * L.vss;
+        T.x[k] = lds64(ad);
+        T.y[k] = lds64(ad + 4 * L.vss);
+        T.z[k] = lds64(ad + 8 * L.vss);
+    }
+    // the previous step's score (warp-aggregated mode scores at loop level)
     if (P.has) {  // not taken by an aggregated flush at loop level
         atomicAdd(a.tally + P.bin, P.val);
         P.has = false;
@@ -110,12 +175,25 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
                                 &exact_used, true, &need_t);
     }
     // (neighbour << 2) | its face across the exit face, -1 on the boundary
-    const int nbp = (face & 2) ? ((face & 1) ? r.nb[3] : r.nb[2]) : ((face & 1) ? r.nb[1] : r.nb[0]);
-    // the next step's record, issued now so it lands while the exact t
-    // division and the commit below run; on the paths where the particle
-    // stays (reached, stuck) it is the current element's again, so the
-    // loop-carried record has a single definition (no register copies)
-    L.nr = load_rec(a.rec, (kind == 1 && nbp >= 0) ? (nbp >> 2) : L.e);
+    const int nbp = (face & 2) ? ((face & 1) ? r.nbp[3] : r.nbp[2]) : ((face & 1) ? r.nbp[1] : r.nbp[0]);
+    if (kind == 1 && nbp >= 0) {
+        // crossing: the neighbour's one new vertex replaces local vertex
+        // `face` in its slot, and the slot map follows the neighbour's order
+        const int nv = (face & 2) ? ((face & 1) ? r.nv[3] : r.nv[2]) : ((face & 1) ? r.nv[1] : r.nv[0]);
+        const unsigned sw = (face & 2) ? r.sel.y : r.sel.x;
+        const unsigned sel = (face & 1) ? (sw >> 16) : (sw & 0xffffu);
+        const unsigned ad = L.vsb + ((L.pm >> (8 * face)) & 0xffu) * L.vss;
+        const double* g = &a.vtx[nv].x;
+        cpa8(ad, g);
+        cpa8(ad + 4 * L.vss, g + 1);
+        cpa8(ad + 8 * L.vss, g + 2);
+        asm volatile("cp.async.commit_group;\n" ::);
+        L.pm = __byte_perm(L.pm, 0u, sel);
+    }
+    // the next step's crossing record: needed only after the next step's
+    // exit filter, so its latency is hidden; the current element's again on
+    // the paths where the particle stays (one definition, no register copies)
+    L.nr = load_xr(a, (kind == 1 && nbp >= 0) ? (nbp >> 2) : L.e);
     if (kind == 1) {
         if (need_t)
             t = exact_t(T, face, ox, oy, oz, rn_sub(L.dx(), ox), rn_sub(L.dy(), oy), rn_sub(L.dz(), oz));
@@ -146,7 +224,7 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
             event = false;
             if (hop >= 0) {
                 L.e = hop;
-                L.nr = load_rec(a.rec, hop);
+                vslots_fill(a, L, hop, elem_vids(a, hop));
                 L.entry = -1;
                 L.st = 2;
                 atomicAdd(C.sh + SC_RECOV, 1u);
@@ -341,10 +419,12 @@ __global__ void __launch_bounds__(THREADS, MINB) walk_kernel(const WalkArgs a) {
     __shared__ unsigned shc[SC_N];
     __shared__ uint64_t sdig[THREADS];
     __shared__ int scnt[THREADS];
+    VSLOTS_DECL(THREADS)
     counters_init(shc);
     const DigestSlot DS{sdig + threadIdx.x, scnt + threadIdx.x};
     Lane L;
     L.busy = false;
+    VSLOTS_INIT(L);
     Counters C;
     C.sh = shc;
     Pending P;
@@ -383,7 +463,7 @@ __global__ void __launch_bounds__(THREADS, MINB) walk_kernel(const WalkArgs a) {
                             L.w() = a.score ? a.weight[i] : 0.0;
                             L.g() = a.score ? a.group[i] : 0;
                             begin(L, a, DS);
-                            L.nr = load_rec(a.rec, L.e);
+                            vslots_fill(a, L, L.e, elem_vids(a, L.e));
                             L.alive() = (int8_t)(a.alive[i] | a.fly_in[i]);
                         }
                     }
@@ -413,7 +493,7 @@ __global__ void __launch_bounds__(THREADS, MINB) walk_kernel(const WalkArgs a) {
 struct WorkSoA {
     double *px, *py, *pz, *dx, *dy, *dz, *w, *seg;
     int *idx, *e, *g, *fl;  // fl = entry (low byte, signed) | stuck << 8
-    int4 *r0, *r1;          // the starting element's record (vertex ids | adjacency)
+    int4* r0;               // the starting element's vertex ids
 };
 
 // work items per stage chunk (one per lane at most).  Smaller chunks leave
@@ -428,7 +508,7 @@ static_assert(STAGE_N >= 1 && STAGE_N <= 32, "a stage chunk refills at most one 
 struct __align__(16) WarpStage {
     double px[STAGE_N], py[STAGE_N], pz[STAGE_N], dx[STAGE_N], dy[STAGE_N], dz[STAGE_N],
         w[STAGE_N], seg[STAGE_N];
-    int4 r0[STAGE_N], r1[STAGE_N];
+    int4 r0[STAGE_N];
     int idx[STAGE_N], e[STAGE_N], g[STAGE_N], fl[STAGE_N];
 };
 
@@ -473,7 +553,6 @@ __device__ __forceinline__ int claim_chunk(const WalkArgs& a, const WorkSoA& W, 
         cp_async4(&st.g[lane], W.g + k);
         cp_async4(&st.fl[lane], W.fl + k);
         cp_async16(&st.r0[lane], W.r0 + k);
-        cp_async16(&st.r1[lane], W.r1 + k);
     }
     cp_async_commit();
     return n;
@@ -525,7 +604,6 @@ __device__ __forceinline__ int claim_direct(const WalkArgs& a, const DirectArgs&
         if (walk) {
             const int4* rp = reinterpret_cast<const int4*>(a.rec + el);
             st.r0[lane] = ldg_mesh(rp);
-            st.r1[lane] = ldg_mesh(rp + 1);
         }
     }
     if (d.wsum) {
@@ -551,6 +629,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     __shared__ unsigned shc[SC_N];
     __shared__ uint64_t sdig[THREADS];
     __shared__ int scnt[THREADS];
+    VSLOTS_DECL(THREADS)
     counters_init(shc);
     const DigestSlot DS{sdig + threadIdx.x, scnt + threadIdx.x};
     const int wid = threadIdx.x >> 5;
@@ -560,6 +639,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     };
     Lane L;
     L.busy = false;
+    VSLOTS_INIT(L);
     Counters C;
     C.sh = shc;
     Pending P;
@@ -616,10 +696,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
                     L.st = (fl >> 8) & 0xff;
                     begin<DIG>(L, a, DS);
                     L.alive() = (int)(signed char)((fl >> 16) & 0xff);
-                    // the first step's record came with the stage: no dependent load
-                    const int4 q0 = s.r0[j], q1 = s.r1[j];
-                    L.nr.v[0] = q0.x; L.nr.v[1] = q0.y; L.nr.v[2] = q0.z; L.nr.v[3] = q0.w;
-                    L.nr.nb[0] = q1.x; L.nr.nb[1] = q1.y; L.nr.nb[2] = q1.z; L.nr.nb[3] = q1.w;
+                    vslots_fill(a, L, L.e, s.r0[j]);
                 }
             }
             head += take;
@@ -691,5 +768,4 @@ __global__ void stage_kernel(const WalkArgs a, const WorkSoA W, int64_t* __restr
               ((int)(unsigned char)(a.alive[i] | a.fly_in[i]) << 16);  // load_step: alive |= flying
     const int4* rp = reinterpret_cast<const int4*>(a.rec + a.element[i]);
     W.r0[k] = __ldg(rp);
-    W.r1[k] = __ldg(rp + 1);
 }
