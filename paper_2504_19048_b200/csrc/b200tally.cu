@@ -96,7 +96,7 @@ struct bt_tally {
     ElemRec* rec = nullptr;
     Vtx* vtx = nullptr;
     XRec* xrec = nullptr;  // crossing records (walk)
-    uint2* xsel = nullptr;
+    unsigned* xsel = nullptr;  // meshes of >= 2^24 vertices only
     // grid
     GridDev grid{};
     int* cell_start = nullptr;
@@ -513,7 +513,11 @@ bt_status bt_create(const double* vertices, int64_t num_vertices, const int32_t*
         CKF(cudaMemcpy(h->rec, hr.data(), sizeof(ElemRec) * hr.size(), cudaMemcpyHostToDevice));
         CKF(cudaMemcpy(h->vtx, hv.data(), sizeof(Vtx) * hv.size(), cudaMemcpyHostToDevice));
         TRYF(dalloc(&h->xrec, num_elements));
-        TRYF(dalloc(&h->xsel, num_elements));
+        // packed records need vertex ids < 2^24; B200TALLY_WIDE_XREC=1 forces the
+        // wide layout on any mesh (tests)
+        const char* wide_env = getenv("B200TALLY_WIDE_XREC");
+        if (num_vertices >= (1 << 24) || (wide_env && atoi(wide_env) != 0))
+            TRYF(dalloc(&h->xsel, num_elements));
         unsigned long long* dbad = nullptr;
         TRYF(dalloc(&dbad, 1));
         CKF(cudaMemset(dbad, 0, sizeof(unsigned long long)));

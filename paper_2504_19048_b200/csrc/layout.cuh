@@ -21,12 +21,14 @@ static_assert(sizeof(Vtx) == 32, "one 32-byte sector per vertex");
 // neighbour that is not on f (its local vertex nf).  The other three are
 // the element's own, so a crossing fetches ONE vertex, at the same time as
 // the neighbour's record, instead of record -> four vertices.  sel[f] maps
-// the neighbour's local vertex order onto the element's: nibble k = the
-// element's local index of the neighbour's vertex k (f itself for k = nf,
-// whose slot receives the new vertex) -- a __byte_perm selector.
+// the neighbour's local vertex order onto the element's: bits 2k..2k+1 =
+// the element's local index of the neighbour's vertex k (f itself for
+// k = nf, whose slot receives the new vertex).  nvs[f] = nv | sel << 24 in
+// one 32-byte sector; meshes of 2^24 vertices or more keep nv whole and the
+// four sel bytes in a separate array (WalkArgs::xsel, one more sector).
 struct __align__(16) XRec {
     int nbp[4];
-    int nv[4];
+    unsigned nvs[4];
 };
 static_assert(sizeof(XRec) == 32, "one 32-byte sector per element");
 
@@ -44,7 +46,7 @@ struct WalkArgs {
     const ElemRec* __restrict__ rec;
     const Vtx* __restrict__ vtx;
     const XRec* __restrict__ xrec;       // (E) crossing records
-    const uint2* __restrict__ xsel;      // (E) their sel[4], 4 x 16 bits
+    const unsigned* __restrict__ xsel;   // (E) sel[4] as 4 bytes; null: packed in nvs
     double* __restrict__ pos;            // (N,3) persistent
     const double* __restrict__ dest;     // (count,3) this move's destinations
     const int8_t* __restrict__ fly_in;   // (count) this move's flying flags

@@ -62,7 +62,8 @@ __global__ void count_walkable_kernel(const int8_t* __restrict__ fly,
 // vertex-order selector of every face's neighbour; *bad counts faces whose
 // neighbour does not share the face's three vertices (non-conforming mesh)
 __global__ void xrec_kernel(const ElemRec* __restrict__ rec, int64_t ne, XRec* __restrict__ xrec,
-                            uint2* __restrict__ xsel, unsigned long long* bad) {
+                            unsigned* __restrict__ xsel /* null: pack into nvs */,
+                            unsigned long long* bad) {
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= ne) return;
     const ElemRec r = rec[e];
@@ -70,12 +71,12 @@ __global__ void xrec_kernel(const ElemRec* __restrict__ rec, int64_t ne, XRec* _
     unsigned sel[4];
     for (int f = 0; f < 4; ++f) {
         x.nbp[f] = r.nb[f];
-        x.nv[f] = 0;
+        x.nvs[f] = 0;
         sel[f] = 0;
         if (r.nb[f] < 0) continue;
         const ElemRec q = rec[r.nb[f] >> 2];
         const int nf = r.nb[f] & 3;
-        x.nv[f] = q.v[nf];
+        x.nvs[f] = (unsigned)q.v[nf];
         for (int k = 0; k < 4; ++k) {
             int j = f;  // slot of the leaving vertex receives the new one
             if (k != nf) {
@@ -87,9 +88,10 @@ __global__ void xrec_kernel(const ElemRec* __restrict__ rec, int64_t ne, XRec* _
                     j = 0;
                 }
             }
-            sel[f] |= (unsigned)j << (4 * k);
+            sel[f] |= (unsigned)j << (2 * k);
         }
+        if (!xsel) x.nvs[f] |= sel[f] << 24;
     }
     xrec[e] = x;
-    xsel[e] = make_uint2(sel[0] | (sel[1] << 16), sel[2] | (sel[3] << 16));
+    if (xsel) xsel[e] = sel[0] | (sel[1] << 8) | (sel[2] << 16) | (sel[3] << 24);
 }

@@ -19,16 +19,17 @@ __shared__ int8_t s_lane_alive[MAX_CTA_THREADS];
 
 // crossing record of one element, as held by a lane
 struct XR {
-    int nbp[4], nv[4];
-    uint2 sel;
+    int nbp[4];
+    unsigned nvs[4];
+    unsigned selw;  // wide meshes only: the four sel bytes
 };
 __device__ __forceinline__ XR load_xr(const WalkArgs& a, int e) {
     const int4* p = reinterpret_cast<const int4*>(a.xrec + e);
     const int4 u = ldg_mesh(p), v = ldg_mesh(p + 1);
     XR r;
     r.nbp[0] = u.x; r.nbp[1] = u.y; r.nbp[2] = u.z; r.nbp[3] = u.w;
-    r.nv[0] = v.x; r.nv[1] = v.y; r.nv[2] = v.z; r.nv[3] = v.w;
-    r.sel = __ldg(a.xsel + e);
+    r.nvs[0] = v.x; r.nvs[1] = v.y; r.nvs[2] = v.z; r.nvs[3] = v.w;
+    r.selw = a.xsel ? __ldg(a.xsel + e) : 0u;
     return r;
 }
 __device__ __forceinline__ void cpa8(unsigned dst, const void* src) {
@@ -179,9 +180,14 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
     if (kind == 1 && nbp >= 0) {
         // crossing: the neighbour's one new vertex replaces local vertex
         // `face` in its slot, and the slot map follows the neighbour's order
-        const int nv = (face & 2) ? ((face & 1) ? r.nv[3] : r.nv[2]) : ((face & 1) ? r.nv[1] : r.nv[0]);
-        const unsigned sw = (face & 2) ? r.sel.y : r.sel.x;
-        const unsigned sel = (face & 1) ? (sw >> 16) : (sw & 0xffffu);
+        const unsigned nvs =
+            (face & 2) ? ((face & 1) ? r.nvs[3] : r.nvs[2]) : ((face & 1) ? r.nvs[1] : r.nvs[0]);
+        const bool wide = a.xsel != nullptr;
+        const int nv = wide ? (int)nvs : (int)(nvs & 0xffffffu);
+        const unsigned s8 = wide ? (r.selw >> (8 * face)) & 0xffu : nvs >> 24;
+        // 2-bit fields -> the nibbles of a __byte_perm selector
+        const unsigned t4 = (s8 | (s8 << 4)) & 0x0f0fu;
+        const unsigned sel = (t4 | (t4 << 2)) & 0x3333u;
         const unsigned ad = L.vsb + ((L.pm >> (8 * face)) & 0xffu) * L.vss;
         const double* g = &a.vtx[nv].x;
         cpa8(ad, g);

@@ -89,6 +89,14 @@ def test_walk_matches_reference_grid_localize(name):
     _check_case(load_walk_case(name), "grid")
 
 
+@pytest.mark.parametrize("name", ["c1_point_s2", "torus_small"])
+def test_wide_crossing_records_keep_parity(name, monkeypatch):
+    # meshes of >= 2^24 vertices keep the crossing records' vertex-order
+    # selectors in a separate array (layout.cuh XRec); force that layout
+    monkeypatch.setenv("B200TALLY_WIDE_XREC", "1")
+    _check_case(load_walk_case(name), "walk")
+
+
 @pytest.mark.parametrize("opts", [dict(sort=True), dict(warp_aggregate=True),
                                   dict(staged=False), dict(staged=False, sort=True,
                                                            warp_aggregate=True),
