@@ -129,11 +129,22 @@ __global__ void __launch_bounds__(THREADS, MINB) transport_kernel(const Transpor
     Counters C;
     C.sh = shc;
     Pending P;
-    double ux = 0, uy = 0, uz = 0;  // direction
+    // direction and the per-lane totals, touched once per flight: shared
+    // slots keep them out of the walk step's registers
+    __shared__ double s_tr[6][THREADS];
+    __shared__ unsigned s_col[THREADS];
+    double& ux = s_tr[0][threadIdx.x];
+    double& uy = s_tr[1][threadIdx.x];
+    double& uz = s_tr[2][threadIdx.x];
+    double& leaked = s_tr[3][threadIdx.x];
+    double& absorbed = s_tr[4][threadIdx.x];
+    double& stuck_w = s_tr[5][threadIdx.x];
+    unsigned& collisions = s_col[threadIdx.x];
+    ux = uy = uz = 0.0;
+    leaked = absorbed = stuck_w = 0.0;
+    collisions = 0;
     uint32_t rb = 0;
     int rounds = 0;
-    unsigned collisions = 0;
-    double leaked = 0, absorbed = 0, stuck_w = 0;
     bool drained = false;
     bool need_flight = false;
     while (true) {
@@ -249,17 +260,18 @@ __global__ void __launch_bounds__(THREADS, MINB) transport_kernel(const Transpor
         flush_pending(a, P, !L.busy);
     }
     // reduce the per-lane totals (tally sums are order-free up to rounding)
+    double lk = leaked, ab = absorbed, sw = stuck_w;
     for (int o = 16; o > 0; o >>= 1) {
-        leaked += __shfl_xor_sync(FULL, leaked, o);
-        absorbed += __shfl_xor_sync(FULL, absorbed, o);
-        stuck_w += __shfl_xor_sync(FULL, stuck_w, o);
+        lk += __shfl_xor_sync(FULL, lk, o);
+        ab += __shfl_xor_sync(FULL, ab, o);
+        sw += __shfl_xor_sync(FULL, sw, o);
     }
-    collisions = __reduce_add_sync(FULL, collisions);
+    const unsigned cl = __reduce_add_sync(FULL, collisions);
     if (lane == 0) {
-        if (leaked != 0.0) atomicAdd(t.wsum + 0, leaked);
-        if (absorbed != 0.0) atomicAdd(t.wsum + 1, absorbed);
-        if (stuck_w != 0.0) atomicAdd(t.wsum + 2, stuck_w);
-        if (collisions) atomicAdd(t.tcount + 0, (unsigned long long)collisions);
+        if (lk != 0.0) atomicAdd(t.wsum + 0, lk);
+        if (ab != 0.0) atomicAdd(t.wsum + 1, ab);
+        if (sw != 0.0) atomicAdd(t.wsum + 2, sw);
+        if (cl) atomicAdd(t.tcount + 0, (unsigned long long)cl);
     }
     flush_counters(a, C);
 }
