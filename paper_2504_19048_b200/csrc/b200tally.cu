@@ -769,7 +769,7 @@ static bt_status walk_enqueue(bt_tally* h, WalkArgs a, int64_t lo, int64_t hi, i
     const Variant& V = kVariants[vi];
     auto* staged_k = V.staged[direct ? 1 : 0][a.digest ? 1 : 0];
     const void* kptr = staged ? (const void*)staged_k : (const void*)V.plain;
-    const size_t dyn = staged ? sizeof(WarpStage) * 2 * (V.threads / 32) : 0;
+    const size_t dyn = staged ? sizeof(WarpStage) * (direct ? 1 : 2) * (V.threads / 32) : 0;
     if (staged) CK(cudaFuncSetAttribute(kptr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     int bps = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kptr, V.threads, dyn));

@@ -628,8 +628,8 @@ __global__ void __launch_bounds__(THREADS, MINB)
                        const DirectArgs D) {
     static_assert(THREADS <= MAX_CTA_THREADS, "one shared lane slot per thread");
     constexpr unsigned FULL = 0xffffffffu;
-    // the warps' double-buffered stages: dynamic shared memory (with the lane
-    // slots the CTA exceeds the 48 KB static limit)
+    // the warps' stages in dynamic shared memory: double-buffered for the
+    // stage kernel's cp.async prefetch, one per warp for the direct refill
     extern __shared__ __align__(16) unsigned char dyn_smem[];
     WarpStage(*stages)[2] = reinterpret_cast<WarpStage(*)[2]>(dyn_smem);
     __shared__ unsigned shc[SC_N];
@@ -651,8 +651,12 @@ __global__ void __launch_bounds__(THREADS, MINB)
     Pending P;
     int cur = 0;
     int head = 0;
-    int ncur = claim(stages[wid][0]);
-    int nnext = ncur == STAGE_N ? claim(stages[wid][1]) : 0;
+    // direct refill: claim_direct's loads block anyway, so one stage per warp
+    // (claimed when the previous one is used up) -- the second buffer's
+    // shared memory goes to L1
+    WarpStage* const st1 = reinterpret_cast<WarpStage*>(dyn_smem) + wid;
+    int ncur = DIRECT ? claim(*st1) : claim(stages[wid][0]);
+    int nnext = (!DIRECT && ncur == STAGE_N) ? claim(stages[wid][1]) : 0;
     // only the first group must have landed; wait_group 1 would do, but the
     // second claim may be empty -- a full wait costs one DRAM latency once
     cp_async_wait_all();
@@ -661,19 +665,27 @@ __global__ void __launch_bounds__(THREADS, MINB)
         unsigned idle = __ballot_sync(FULL, !L.busy);
         while (idle) {
             if (head == ncur) {  // current stage used up: switch to the prefetched one
-                if (nnext == 0) break;
-                cp_async_wait_all();
-                __syncwarp();
-                cur ^= 1;
-                head = 0;
-                ncur = nnext;
-                // the stage just emptied is free: prefetch the chunk after next
-                nnext = (ncur == STAGE_N) ? claim(stages[wid][cur ^ 1]) : 0;
+                if (DIRECT) {
+                    if (ncur < STAGE_N) break;  // the last chunk was partial: no more work
+                    __syncwarp();               // every lane is done reading the stage
+                    ncur = claim(*st1);
+                    head = 0;
+                    if (ncur == 0) break;
+                } else {
+                    if (nnext == 0) break;
+                    cp_async_wait_all();
+                    __syncwarp();
+                    cur ^= 1;
+                    head = 0;
+                    ncur = nnext;
+                    // the stage just emptied is free: prefetch the chunk after next
+                    nnext = (ncur == STAGE_N) ? claim(stages[wid][cur ^ 1]) : 0;
+                }
             }
             const int take = min((int)__popc(idle), ncur - head);
             if (!L.busy) {
                 const int rk = __popc(idle & lanemask_lt());
-                const WarpStage& s = stages[wid][cur];
+                const WarpStage& s = DIRECT ? *st1 : stages[wid][cur];
                 const int j = head + rk;
                 const int fl0 = rk < take ? s.fl[j] : 0;
                 if (DIRECT && rk < take && !(fl0 & (1 << 24))) {
