@@ -511,3 +511,38 @@ def test_localization_prefilter_equals_exact_at_scale():
         mt.close()
     assert np.array_equal(out[0], out[1])
     assert (out[0] >= 0).mean() > 0.9
+
+
+def test_permuted_vertex_orders_sampled_parity():
+    """The walk keeps a lane's element vertices in shared-memory slots and
+    re-maps them through each crossing record's vertex-order selector
+    (csrc/layout.cuh XRec).  A mesh whose elements list their vertices in
+    random local orders (orientation fixed by from_arrays) exercises every
+    selector: the walk must still match the oracle bit for bit."""
+    torch = pytest.importorskip("torch")
+    from paper_2504_19048_b200 import TetMesh
+    base = build_cube_mesh(20)
+    gen = np.random.default_rng(4242)
+    perm = np.argsort(gen.random((base.num_elements, 4)), axis=1)
+    m = TetMesh.from_arrays(base.vertices, np.take_along_axis(base.elements, perm, axis=1))
+    n = 400_000
+    pos = synth.uniform_box(gen, n)
+    dest = synth.flight_destinations(gen, pos, 2.0)
+    w = 0.5 + gen.random(n)
+    mt = MeshTally(m, n, digest=True)
+    mt.initialize_particle_location(torch.from_numpy(pos).cuda())
+    s = mt.move_to_next_location(torch.from_numpy(dest).cuda(),
+                                 torch.ones(n, dtype=torch.int8, device="cuda"),
+                                 torch.from_numpy(w).cuda())
+    st = mt.read_particles()
+    d, c = mt.read_digest()
+    assert s.events == int(c.sum())
+    idx = np.sort(gen.choice(n, 20_000, replace=False))
+    ref = orc.OracleTally(m, idx.size, threads=orc.max_threads())
+    ref.initialize_particle_location(pos[idx])
+    ref.seg_total[:] = 0.0
+    ref.move_to_next_location(dest[idx], np.ones(idx.size, np.int8), w[idx])
+    for k in ("position", "element", "alive", "entry_face", "stuck", "outcome", "seg_total"):
+        assert np.array_equal(getattr(st, k)[idx], getattr(ref, k)[:idx.size]), k
+    assert np.array_equal(d[idx], ref.digest) and np.array_equal(c[idx], ref.count)
+    mt.close()
