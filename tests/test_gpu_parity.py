@@ -546,3 +546,59 @@ def test_permuted_vertex_orders_sampled_parity():
         assert np.array_equal(getattr(st, k)[idx], getattr(ref, k)[:idx.size]), k
     assert np.array_equal(d[idx], ref.digest) and np.array_equal(c[idx], ref.count)
     mt.close()
+
+
+@pytest.mark.parametrize("localize", ["grid", "walk"])
+def test_ragged_moves_and_edge_inputs(localize):
+    """Edge inputs the reference's facade accepts, each move checked against
+    the oracle bit for bit: initialization below capacity with points outside
+    the mesh (lost, element -1), a move over fewer particles than were
+    initialized (ragged count: the rest stay put), mixed flying flags (only
+    localized particles fly), an empty move (None), a move where almost
+    nothing flies, and a zero-weight particle."""
+    m = build_cube_mesh(8)
+    gen = np.random.default_rng(99)
+    cap, n0 = 1000, 700
+    pos = synth.uniform_box(gen, n0)
+    pos[650:] = [1.5, 0.5, 0.5] + 0.1 * gen.random((50, 3))  # outside the bbox: lost
+    mt = MeshTally(m, cap, digest=True, localize=localize)
+    ref = orc.OracleTally(m, cap)
+    mt.initialize_particle_location(pos)
+    ref.initialize_particle_location(pos)
+    st = mt.read_particles(n0)
+    assert np.array_equal(st.element, ref.element[:n0])
+    assert (st.element[650:] == -1).all()
+    ref.seg_total[:] = 0.0
+
+    def check(count, fly, w):
+        dest = synth.flight_destinations(gen, ref.position[:count].copy(), 2.0)
+        s = mt.move_to_next_location(dest, fly, w)
+        e = ref.move_to_next_location(dest, fly, w)
+        if count == 0:
+            assert s is None and e is None
+            return
+        assert (s.sweeps, s.events, s.reached, s.boundary_exits, s.stuck_recoveries,
+                s.stuck_terminations) == tuple(e)
+        got = mt.read_particles(n0)
+        for k in ("position", "element", "alive", "entry_face", "stuck", "outcome"):
+            assert np.array_equal(getattr(got, k), getattr(ref, k)[:n0]), k
+        d, c = mt.read_digest(n0)
+        assert np.array_equal(d[:count], ref.digest[:count])
+        assert np.array_equal(c[:count], ref.count[:count])
+        ok, worst = rel_close(mt.batch_totals().reshape(-1), ref.batch_totals(), TALLY_RTOL)
+        assert ok, worst
+
+    loc = ref.element[:n0] >= 0
+    fly = ((gen.random(500) < 0.7) & loc[:500]).astype(np.int8)
+    w = 0.5 + gen.random(500)
+    w[3] = 0.0
+    check(500, fly, w)
+    check(0, np.zeros(0, np.int8), np.zeros(0))
+    fly = np.zeros(n0, np.int8)
+    fly[[5, 17, 400]] = 1
+    fly &= loc.astype(np.int8)
+    check(n0, fly, np.ones(n0))
+    mt.finalize_batch()
+    ref.finalize_batch()
+    assert rel_close(mt.grid.sum, ref.sum, TALLY_RTOL)[0]
+    mt.close()
