@@ -62,7 +62,7 @@ def run_point(mesh, positions, sigma_t, moves, label, warm=1, chain=False, **mt_
             dest = pos_t + flights_torch(torch, n, gen, dev, sigma_t)[:, None] * \
                 iso_dirs_torch(torch, n, gen, dev)
             f = alive_t.clone() if chain else fly
-            nf = int(f.sum().item()) if record else 0
+            nf = int(f.sum().item())  # also in the warm-up batch (first-use kernel loads)
             s = mt.move_to_next_location(dest.contiguous(), f, w)
             ev += s.events
             mv += nf
