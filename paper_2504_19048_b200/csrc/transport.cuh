@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(THREADS, MINB) transport_kernel(const Transpor
     Counters C;
     C.sh = shc;
     Pending P;
+    P.init(a);
     // direction and the per-lane totals, touched once per flight: shared
     // slots keep them out of the walk step's registers
     __shared__ double s_tr[6][THREADS];

@@ -124,6 +124,11 @@ struct Pending {
     double val = 0.0;
     int probe = 0;      // loop iterations to the next contention probe
     bool agg = false;   // warp-uniform: aggregate the pending scores
+    bool adaptive = false;  // probe for contention (WAGG_ADAPTIVE)
+    __device__ __forceinline__ void init(const WalkArgs& a) {
+        adaptive = a.wagg == WAGG_ADAPTIVE;
+        agg = a.wagg == WAGG_ALWAYS;
+    }
 };
 
 // One step of search.py:183-274 for a flying lane.  Returns true when the
@@ -368,20 +373,18 @@ __device__ __forceinline__ void score_aggregated(const WalkArgs& a, bool has_sco
 // profiles/r01_options.jsonl).  Idle lanes flush their pending score.
 __device__ __forceinline__ void flush_pending(const WalkArgs& a, Pending& P, bool idle) {
     constexpr unsigned FULL = 0xffffffffu;
-    bool agg = a.wagg == WAGG_ALWAYS;
-    if (a.wagg == WAGG_ADAPTIVE) {
-        // probe every 4th iteration; the decision holds in between (warp-uniform)
-        if (--P.probe <= 0) {
-            const int lane = threadIdx.x & 31;
-            const unsigned hm = __ballot_sync(FULL, P.has);
-            const int nxt = __shfl_down_sync(FULL, (int)P.bin, 1);
-            // low 32 bits: a false match only aggregates, which stays exact
-            const bool dup = P.has && lane < 31 && ((hm >> (lane + 1)) & 1u) && nxt == (int)P.bin;
-            P.agg = __any_sync(FULL, dup);
-            P.probe = 4;
-        }
-        agg = P.agg;
+    // mode flags resolved once per kernel (Pending::init); P.agg is the
+    // current decision in every mode
+    if (P.adaptive && --P.probe <= 0) {  // probe every 4th iteration (warp-uniform)
+        const int lane = threadIdx.x & 31;
+        const unsigned hm = __ballot_sync(FULL, P.has);
+        const int nxt = __shfl_down_sync(FULL, (int)P.bin, 1);
+        // low 32 bits: a false match only aggregates, which stays exact
+        const bool dup = P.has && lane < 31 && ((hm >> (lane + 1)) & 1u) && nxt == (int)P.bin;
+        P.agg = __any_sync(FULL, dup);
+        P.probe = 4;
     }
+    const bool agg = P.agg;
     if (agg) {
         score_aggregated(a, P.has, P.bin, P.val);
         P.has = false;
@@ -434,6 +437,7 @@ __global__ void __launch_bounds__(THREADS, MINB) walk_kernel(const WalkArgs a) {
     Counters C;
     C.sh = shc;
     Pending P;
+    P.init(a);
     bool drained = false;
     while (true) {
         if (!drained) {
@@ -649,6 +653,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     Counters C;
     C.sh = shc;
     Pending P;
+    P.init(a);
     int cur = 0;
     int head = 0;
     // direct refill: claim_direct's loads block anyway, so one stage per warp
