@@ -141,17 +141,6 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
                                           const DigestSlot& DS) {
     const XR r = L.nr;
     Tet T;
-    // this element's vertices: three stayed in the lane's slots from the
-    // previous element, the fourth was copied in (cp.async) when the previous
-    // step chose its exit face -- one gather per crossing, issued a step ahead
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const unsigned ad = L.vsb + ((L.pm >> (8 * k)) & 0xffu) * L.vss;
-        T.x[k] = lds64(ad);
-        T.y[k] = lds64(ad + 4 * L.vss);
-        T.z[k] = lds64(ad + 8 * L.vss);
-    }
     // the previous step's score (warp-aggregated mode scores at loop level)
     if (P.has) {  // not taken by an aggregated flush at loop level
         atomicAdd(a.tally + P.bin, P.val);
@@ -168,6 +157,19 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
             oy = __dadd_rn(oy, __ddiv_rn(__dmul_rn(NUDGE, sy), ln));
             oz = __dadd_rn(oz, __ddiv_rn(__dmul_rn(NUDGE, sz), ln));
         }
+    }
+    // this element's vertices: three stayed in the lane's slots from the
+    // previous element, the fourth was copied in (cp.async) when the previous
+    // step chose its exit face -- one gather per crossing, issued a step
+    // ahead.  Waited for only here, so the score atomic and the nudge check
+    // above issue while the copy lands (in-order issue: -0.9%).
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const unsigned ad = L.vsb + ((L.pm >> (8 * k)) & 0xffu) * L.vss;
+        T.x[k] = lds64(ad);
+        T.y[k] = lds64(ad + 4 * L.vss);
+        T.z[k] = lds64(ad + 8 * L.vss);
     }
     int face;
     double t;
