@@ -209,7 +209,9 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
     L.nr = load_xr(a, (kind == 1 && nbp >= 0) ? (nbp >> 2) : L.e);
     if (kind == 1) {
         if (need_t)
-            t = exact_t(T, face, ox, oy, oz, rn_sub(L.dx(), ox), rn_sub(L.dy(), oy), rn_sub(L.dz(), oz));
+            // a face the fp32 filter decided: t in (1e-12, 1], division in range
+            t = exact_t<true>(T, face, ox, oy, oz, rn_sub(L.dx(), ox), rn_sub(L.dy(), oy),
+                              rn_sub(L.dz(), oz));
     }
     bool done = false;
     bool event = true;
