@@ -13,14 +13,16 @@
 //   _finalize                       tally.py:83-95              -> finalize_kernel (move_prep.cuh)
 //
 // Design: persistent CTAs, one particle per lane run to
-// completion; warps refill idle lanes from cp.async-prefetched stages of a
-// compacted work list, so lanes stay busy despite the exponential
-// crossings-per-move tail; the exit search is decided by an fp32 filter with
-// proven margins (fp64 reference arithmetic otherwise); the mesh is one
-// 32-byte record per element (vertex ids + packed neighbour/face) plus 32-byte
-// padded fp64 vertices, L2-resident up to ~3M tets; tallies are fp64 atomics
-// into a private per-GPU grid, warp-aggregated with __match_any_sync where
-// lanes score the same bins.
+// completion; warps refill idle lanes from per-warp stages claimed straight
+// from the particle arrays (or from the stage kernel's compacted work list),
+// so lanes stay busy despite the exponential crossings-per-move tail; the
+// exit search is decided by an fp32 filter with proven margins (fp64
+// reference arithmetic otherwise); each lane keeps its element's four fp64
+// vertices in shared-memory slots, and a crossing fetches only the
+// neighbour's one new vertex, named (with the neighbour's vertex order) by a
+// 32-byte crossing record per element; tallies are fp64 atomics into a
+// private per-GPU grid, warp-aggregated with __match_any_sync where lanes
+// score the same bins.
 #include <cuda_runtime.h>
 
 #include <algorithm>
