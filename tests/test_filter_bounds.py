@@ -51,7 +51,10 @@ def check(L, V, o, d):
     tets = np.ascontiguousarray(np.concatenate([V[:, :, 0], V[:, :, 1], V[:, :, 2]], axis=1))
     od = np.ascontiguousarray(np.concatenate([o, d], axis=1))
     out = np.zeros((k, 27), np.float32)
-    L.bt_f32_probe(tets.ctypes.data, od.ctypes.data, k, out.ctypes.data)
+    pm = np.zeros(1, np.int64)
+    L.bt_f32_probe(tets.ctypes.data, od.ctypes.data, k, out.ctypes.data, pm.ctypes.data)
+    # the packed (FFMA2) filter's intermediates equal the scalar formulation's
+    assert pm[0] == 0, pm
     worst = {"face": 0.0, "y0": 0.0, "cont32": 0.0}
     for i in range(k):
         p = out[i]
@@ -83,7 +86,7 @@ def check(L, V, o, d):
 @pytest.mark.parametrize("name", ["cube", "torus", "sliver", "scaled"])
 def test_fp32_filter_error_bounds(_lib_fixture, name):
     L = _lib_fixture
-    L.bt_f32_probe.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+    L.bt_f32_probe.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
     gen = np.random.default_rng(123)
     if name == "cube":
         m, scale = build_cube_mesh(20), 0.05
