@@ -36,6 +36,7 @@
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
 
 #include "../../include/b200tally.h"
 #include "geometry.cuh"
@@ -135,7 +136,12 @@ struct bt_tally {
     double source_weight = 0.0;
     // counters
     unsigned long long* dcounters = nullptr;  // queue + counters + flags
-    double* dwsum = nullptr;
+    double* wsel = nullptr;                   // device source weight: selected weights
+    double* wsel_vals = nullptr;              // pairwise tree nodes
+    unsigned* wsel_ticks = nullptr;
+    void* wsel_tmp = nullptr;
+    size_t wsel_tmp_bytes = 0;
+    int wsel_depth = 0;
     unsigned long long* hcounters = nullptr;  // pinned
     int move_chunks = 0;                      // host-input pipeline depth (0 = auto)
     int locate_lanes = 0;                     // grid search lanes per particle (0 = default)
@@ -201,7 +207,7 @@ static bt_status free_all(bt_tally* h) {
                     h->entry, h->stuck, h->outcome, h->seg_total, h->group, h->dest, h->fly,
                     h->weight, h->digest, h->dcount, h->order, h->sort_keys_in,
                     h->sort_keys_out, h->sort_vals_in, h->sort_tmp, h->tally, h->sum,
-                    h->sum_sq, h->dcounters, h->dwsum, h->snap_pos, h->snap_element,
+                    h->sum_sq, h->dcounters, h->wsel, h->wsel_vals, h->wsel_ticks, h->wsel_tmp, h->snap_pos, h->snap_element,
                     h->snap_flags, h->snap_seg, h->work_mem, h->init_stage,
                     h->col_tally, h->col_sum, h->col_sum_sq, h->tr_dir, h->tr_weight,
                     h->tr_rng, h->tr_round_max, h->tr_count, h->tr_wsum, h->tr_xs,
@@ -547,7 +553,6 @@ bt_status bt_create(const double* vertices, int64_t num_vertices, const int32_t*
     TRYF(dalloc(&h->sum, nbins));
     TRYF(dalloc(&h->sum_sq, nbins));
     TRYF(dalloc(&h->dcounters, NDCOUNTERS));
-    TRYF(dalloc(&h->dwsum, 1));
     CKF(cudaMallocHost((void**)&h->hcounters, NDCOUNTERS * sizeof(unsigned long long)));
     CKF(cudaMemset(h->pos, 0, sizeof(double) * 3 * n));
     CKF(cudaMemset(h->element, 0xff, sizeof(int32_t) * n));  // -1: unlocalized
@@ -719,6 +724,8 @@ static WalkArgs walk_args(bt_tally* h, const double* dest, const int8_t* fly, co
     a.score = score ? 1 : 0;
     a.wagg = h->opt_wagg;
     a.exact_only = h->opt_exact_only ? 1 : 0;
+    a.gate = nullptr;
+    a.gate_pick = 0;
     return a;
 }
 
@@ -729,31 +736,10 @@ static bt_status walk_begin(bt_tally* h) {
     return BT_OK;
 }
 
-// enqueue stage + walk of particles [lo, hi) as chunk `chunk` (staged path),
-// or the whole range with the v1 kernel / element-sorted hand-out
-static bt_status walk_enqueue(bt_tally* h, WalkArgs a, int64_t lo, int64_t hi, int chunk,
-                              double* wsum, cudaStream_t st = nullptr, bool pick_refill = false) {
-    if (!st) st = h->stream;
-    const int64_t count = hi - lo;
-    a.count = count;
-    a.queue = h->dcounters + 16 + chunk;
+// one walk launch (+ its stage kernel / sort) of particles [lo, lo + count)
+static bt_status launch_walk(bt_tally* h, WalkArgs a, int64_t lo, int64_t count, int chunk,
+                             cudaStream_t st, bool direct) {
     const bool staged = h->opt_staged != 0;
-    // direct refill straight from the particle arrays, except: element-sorted
-    // hand-out (its gathers would be random), and -- when the caller lets us
-    // look (single-launch moves) -- moves where fewer than half the slots walk
-    // (chained moves after most particles leaked), where compacting first wins
-    bool direct = h->opt_staged == 2 && !(h->opt_sort && a.score);
-    if (direct && pick_refill && count >= (1 << 16)) {
-        CK(cudaMemsetAsync(h->dcounters + 14, 0, sizeof(unsigned long long), st));
-        count_walkable_kernel<<<std::min<int64_t>(grid_for(count, 256), 1184), 256, 0, st>>>(
-            a.fly_in + lo, h->element + lo, count, h->dcounters + 14);
-        CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(h->hcounters + 14, h->dcounters + 14, sizeof(unsigned long long),
-                           cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        h->kernels += 1;
-        direct = 2 * (int64_t)h->hcounters[14] >= count;
-    }
     if (h->opt_sort && a.score) {  // whole move only (lo == 0)
         iota_keys_kernel<<<grid_for(count, 256), 256, 0, st>>>(
             h->element, count, h->sort_keys_in, h->sort_vals_in);
@@ -781,24 +767,15 @@ static bt_status walk_enqueue(bt_tally* h, WalkArgs a, int64_t lo, int64_t hi, i
         (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)bps * h->num_sms));
     int64_t* nwork = reinterpret_cast<int64_t*>(h->dcounters + 32 + chunk);
     WorkSoA W = h->work;
-    DirectArgs D{lo, hi, wsum};
-    if (direct && !a.order) D = DirectArgs{lo, hi, wsum};
-    if (direct && a.order) D = DirectArgs{0, count, wsum};  // sorted: slots index h->order
+    DirectArgs D{lo, lo + count};
+    if (direct && a.order) D = DirectArgs{0, count};  // sorted: slots index h->order
     if (staged && !direct) {
         TRY(ensure_work(h));
         W = h->work;
         W.px += lo; W.py += lo; W.pz += lo; W.dx += lo; W.dy += lo; W.dz += lo;
         W.r0 += lo;
         W.w += lo; W.seg += lo; W.idx += lo; W.e += lo; W.g += lo; W.fl += lo;
-        stage_kernel<<<grid_for(count, 256), 256, 0, st>>>(a, W, nwork, lo, wsum);
-        CK(cudaGetLastError());
-        h->kernels += 1;
-    }
-    if (!staged && wsum) {  // the unstaged kernel has no stage pass to sum the weights in
-        CK(cudaMemsetAsync(h->dcounters + 15, 0, sizeof(unsigned long long), st));
-        prepare_kernel<<<grid_for(count, 256), 256, 0, st>>>(
-            a.fly_in + lo, h->element + lo, nullptr, h->ngroups, a.weight + lo, count,
-            h->dcounters + 15, wsum);
+        stage_kernel<<<grid_for(count, 256), 256, 0, st>>>(a, W, nwork, lo);
         CK(cudaGetLastError());
         h->kernels += 1;
     }
@@ -813,6 +790,35 @@ static bt_status walk_enqueue(bt_tally* h, WalkArgs a, int64_t lo, int64_t hi, i
     CK(cudaGetLastError());
     h->kernels += 1;
     return BT_OK;
+}
+
+
+// enqueue stage + walk of particles [lo, hi) as chunk `chunk` (staged path),
+// or the whole range with the v1 kernel / element-sorted hand-out.
+// pick_refill (single-launch moves): direct refill straight from the particle
+// arrays, unless fewer than half the slots walk (chained moves after most
+// particles leaked), where compacting first (stage kernel) wins -- decided on
+// the device (WalkArgs::gate): both are enqueued, the other returns at once.
+static bt_status walk_enqueue(bt_tally* h, WalkArgs a, int64_t lo, int64_t hi, int chunk,
+                              cudaStream_t st = nullptr, bool pick_refill = false) {
+    if (!st) st = h->stream;
+    const int64_t count = hi - lo;
+    a.count = count;
+    a.queue = h->dcounters + 16 + chunk;
+    // element-sorted hand-out: the stage kernel (direct gathers would be random)
+    bool direct = h->opt_staged == 2 && !(h->opt_sort && a.score);
+    if (direct && pick_refill && count >= (1 << 16)) {
+        count_walkable_kernel<<<std::min<int64_t>(grid_for(count, 256), 1184), 256, 0, st>>>(
+            a.fly_in + lo, h->element + lo, count, h->dcounters + 14);
+        CK(cudaGetLastError());
+        h->kernels += 1;
+        a.gate = h->dcounters + 14;
+        a.gate_pick = 1;
+        TRY(launch_walk(h, a, lo, count, chunk, st, false));
+        TRY(launch_walk(h, a, lo, count, chunk, st, true));
+        return BT_OK;
+    }
+    return launch_walk(h, a, lo, count, chunk, st, direct);
 }
 
 // read the counters (running `overlap` on the host meanwhile) and fill the summary
@@ -973,6 +979,40 @@ bt_status bt_initialize_particle_location(bt_tally* h, const double* positions, 
     return BT_OK;
 }
 
+// The recorded source weight of a device-input move, on the device: the
+// flying particles' weights compacted in index order, then numpy's pairwise
+// summation tree (move_prep.cuh) into dcounters[DC_SOURCE_WEIGHT] -- the
+// same bits as the host-input path and the reference (tally.py:267-269).
+static bt_status device_source_weight(bt_tally* h, const int8_t* flying, const double* weights,
+                                      int64_t count) {
+    if (!h->wsel) {
+        int depth = 0;
+        while ((h->cap >> depth) > 64) ++depth;
+        h->wsel_depth = depth;
+        TRY(dalloc(&h->wsel, h->cap));
+        TRY(dalloc(&h->wsel_vals, (int64_t)2 << depth));
+        TRY(dalloc(&h->wsel_ticks, (int64_t)2 << depth));
+        CK(cudaMemset(h->wsel_ticks, 0, sizeof(unsigned) * ((size_t)2 << depth)));
+        size_t b = 0;
+        CK(cub::DeviceSelect::Flagged(nullptr, b, weights, flying, h->wsel,
+                                      reinterpret_cast<long long*>(h->dcounters + DC_SELECTED),
+                                      (int)h->cap));
+        CK(cudaMalloc(&h->wsel_tmp, b));
+        h->wsel_tmp_bytes = b;
+    }
+    size_t b = h->wsel_tmp_bytes;
+    long long* m = reinterpret_cast<long long*>(h->dcounters + DC_SELECTED);
+    CK(cub::DeviceSelect::Flagged(h->wsel_tmp, b, weights, flying, h->wsel, m, (int)count,
+                                  h->stream));
+    const int64_t nthreads = (int64_t)1 << h->wsel_depth;
+    pairwise_sum_kernel<<<grid_for(nthreads, 256), 256, 0, h->stream>>>(
+        h->wsel, m, h->wsel_depth, h->wsel_vals, h->wsel_ticks,
+        reinterpret_cast<double*>(h->dcounters + DC_SOURCE_WEIGHT));
+    CK(cudaGetLastError());
+    h->kernels += 3;
+    return BT_OK;
+}
+
 bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, const int8_t* flying,
                                    const double* weights, const int32_t* groups, int64_t size,
                                    int32_t mem_kind, bt_summary* summary) {
@@ -1066,29 +1106,28 @@ bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, cons
         s = walk_end(h, a.max_sweeps, summary, ov);
         if (need_w) h->source_weight = job.out;
     } else {
-        if (groups) {  // device groups: range check before any work
+        // Device inputs: one host synchronisation per move.  The group range
+        // check, the refill choice and the recorded source weight are all
+        // decided on the device, and come back with the counters in one copy.
+        WalkArgs a = walk_args(h, destinations, flying, weights, true);
+        TRY(walk_begin(h));
+        a.gate = h->dcounters + 14;  // [14] walkable, [15] prepare_kernel's flags
+        if (groups) {
             CK(cudaMemcpyAsync(h->group, groups, sizeof(int32_t) * count,
                                cudaMemcpyDeviceToDevice, h->stream));
-            CK(cudaMemsetAsync(h->dcounters + 15, 0, sizeof(unsigned long long), h->stream));
             prepare_kernel<<<grid_for(count, 256), 256, 0, h->stream>>>(
-                flying, h->element, h->group, h->ngroups, weights, count, h->dcounters + 15,
-                nullptr);
+                flying, h->element, h->group, h->ngroups, count, h->dcounters + 15);
             CK(cudaGetLastError());
             h->kernels += 1;
-            unsigned long long flags = 0;
-            CK(cudaMemcpyAsync(&flags, h->dcounters + 15, sizeof flags, cudaMemcpyDeviceToHost,
-                               h->stream));
-            CK(cudaStreamSynchronize(h->stream));
-            if (flags & 2ull) return set_err(BT_EINDEX, "group out of range [0, %d)", h->ngroups);
         }
-        WalkArgs a = walk_args(h, destinations, flying, weights, true);
-        if (need_w) CK(cudaMemsetAsync(h->dwsum, 0, sizeof(double), h->stream));
-        TRY(walk_begin(h));
-        TRY(walk_enqueue(h, a, 0, count, 0, need_w ? h->dwsum : nullptr, nullptr, true));
+        if (need_w) TRY(device_source_weight(h, flying, weights, count));
+        TRY(walk_enqueue(h, a, 0, count, 0, nullptr, true));
         s = walk_end(h, a.max_sweeps, summary);
-        if (need_w) {
-            double dw = 0.0;
-            CK(cudaMemcpy(&dw, h->dwsum, sizeof dw, cudaMemcpyDeviceToHost));
+        if (h->hcounters[15] & 2ull)
+            return set_err(BT_EINDEX, "group out of range [0, %d)", h->ngroups);
+        if (need_w && s == BT_OK) {
+            double dw;
+            memcpy(&dw, h->hcounters + DC_SOURCE_WEIGHT, sizeof dw);
             h->source_weight = dw;
         }
     }
@@ -1141,6 +1180,9 @@ bt_status bt_tally_device_ptr(bt_tally* h, int32_t which, void** ptr) {
     if (!h || !ptr) return set_err(BT_EINVAL, "NULL argument");
     double* p = tally_ptr(h, which);
     if (!p) return set_err(BT_EINVAL, "unknown tally array %d", which);
+    // a consumer on another stream must see every kernel enqueued so far
+    TRY(ensure_device(h));
+    CK(cudaStreamSynchronize(h->stream));
     *ptr = p;
     return BT_OK;
 }
@@ -1216,6 +1258,10 @@ bt_status bt_last_timing(bt_tally* h, float* walk_ms, float* call_ms, int64_t* k
 bt_status bt_particle_device_ptrs(bt_tally* h, double** position, int32_t** element,
                                   int8_t** alive) {
     if (!h) return set_err(BT_EINVAL, "NULL handle");
+    // the localization of host positions completes asynchronously: a consumer
+    // on another stream (e.g. torch's) must see its element / pos / alive
+    TRY(ensure_device(h));
+    CK(cudaStreamSynchronize(h->stream));
     if (position) *position = h->pos;
     if (element) *element = h->element;
     if (alive) *alive = h->alive;

@@ -33,10 +33,12 @@ struct __align__(16) XRec {
 static_assert(sizeof(XRec) == 32, "one 32-byte sector per element");
 
 enum { C_EVENTS = 0, C_REACHED, C_BOUNDARY, C_RECOV, C_KILLED, C_SWEEPS, C_ERR, C_UNLOC, C_NCOUNTERS };
-// dcounters layout (unsigned long long): [1..8] counters, [14] walkable count
-// (refill choice), [15] flags,
+// dcounters layout (unsigned long long): [1..8] counters, [9] the recorded
+// source weight of a device-input move (double bits), [10] its selected
+// count, [14] walkable count (refill choice), [15] flags,
 // [16 + c] queue of chunk c, [32 + c] work count of chunk c, c < MAX_CHUNKS
 constexpr int MAX_CHUNKS = 16;
+constexpr int DC_SOURCE_WEIGHT = 9, DC_SELECTED = 10;
 constexpr int NDCOUNTERS = 48;
 
 // __match_any_sync aggregation of the tally atomics (BT_OPT_WARP_AGG)
@@ -71,7 +73,24 @@ struct WalkArgs {
     int32_t score;
     int32_t wagg;    // tally atomics: WAGG_ADAPTIVE / WAGG_ALWAYS / WAGG_NEVER
     int32_t exact_only;  // digest kernels only: literal exit search (filter validation)
+    // Device-side decision of a move (nullable): gate[0] = walkable particles
+    // of the move, gate[1] = prepare_kernel's flags.  Every walk launch of the
+    // move returns at once when flags bit 2 is set (a group out of range: the
+    // move fails before any work); with gate_pick, the direct-refill walk runs
+    // iff 2 * walkable >= count and the stage-kernel pair otherwise (both are
+    // enqueued; the other returns at once), so the host never waits for the
+    // choice.
+    const unsigned long long* gate;
+    int32_t gate_pick;
 };
+
+// the launch runs (see WalkArgs::gate); DIRECT: the direct-refill walk
+__device__ __forceinline__ bool gate_open(const WalkArgs& a, bool direct) {
+    if (!a.gate) return true;
+    const unsigned long long walkable = a.gate[0], flags = a.gate[1];
+    if (flags & 2ull) return false;
+    return !a.gate_pick || ((2 * (long long)walkable >= a.count) == direct);
+}
 
 #ifndef BT_NO_L2_HINT
 // Mesh gathers carry an L2 evict_last policy, so the streamed particle state

@@ -3,29 +3,97 @@
 #pragma once
 
 // ---------------------------------------------------------------------------
-// move preparation: localization check (+ group range + source weight for
-// device-resident inputs)
+// move preparation (device-resident inputs): group range check; flags bit 1
+// = a flying particle is not localized, bit 2 = a group id outside
+// [0, ngroups) (the move's walk kernels then do nothing: MoveGate)
 
 __global__ void prepare_kernel(const int8_t* __restrict__ fly, const int32_t* __restrict__ element,
-                               const int32_t* __restrict__ groups, int32_t ngroups,
-                               const double* __restrict__ weight, int64_t count,
-                               unsigned long long* __restrict__ flags,
-                               double* __restrict__ wsum) {
+                               const int32_t* __restrict__ groups, int32_t ngroups, int64_t count,
+                               unsigned long long* __restrict__ flags) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     bool unloc = false, badg = false;
-    double wv = 0.0;
     if (i < count) {
         const bool f = fly[i] != 0;
         unloc = f && element[i] < 0;
         if (groups) badg = groups[i] < 0 || groups[i] >= ngroups;
-        if (wsum && f) wv = weight[i];
     }
     if (__any_sync(0xffffffffu, unloc) && (threadIdx.x & 31) == 0) atomicOr(flags, 1ull);
     if (__any_sync(0xffffffffu, badg) && (threadIdx.x & 31) == 0) atomicOr(flags, 2ull);
-    if (wsum) {
-        for (int o = 16; o > 0; o >>= 1) wv += __shfl_xor_sync(0xffffffffu, wv, o);
-        if ((threadIdx.x & 31) == 0 && wv != 0.0) atomicAdd(wsum, wv);
+}
+
+// ---------------------------------------------------------------------------
+// Recorded source weight of a device-input move: numpy's pairwise summation
+// (numpy/_core/src/umath/loops_utils.h.src, pairwise_sum_DOUBLE) of the
+// flying particles' weights in index order -- the reference's
+// `weight[:count][fly.astype(bool)].sum()` (tally.py:267-269) bit for bit,
+// and the same value the host-input path computes (b200tally.cu
+// pairwise_sum).  The selection is compacted first (CUB DeviceSelect); the
+// summation tree is then evaluated with one thread per leaf (<= 128 values,
+// eight accumulators as numpy) and the inner nodes by the second of the two
+// children to finish (ticket per node, reset on use), so the association is
+// numpy's whatever the scheduling.
+
+__device__ __forceinline__ double pairwise_leaf(const double* __restrict__ a, int64_t n) {
+    if (n < 8) {
+        double res = -0.0;
+        for (int64_t i = 0; i < n; ++i) res = __dadd_rn(res, a[i]);
+        return res;
     }
+    double r[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] = a[k];
+    int64_t i;
+    for (i = 8; i < n - (n % 8); i += 8)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) r[k] = __dadd_rn(r[k], a[i + k]);
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+    return res;
+}
+
+// Thread t follows the bits of t (most significant first) from the root of
+// the tree over [0, *m); the first node of <= 128 values on its path is a
+// leaf, summed by the thread whose remaining bits are zero.  `depth` is
+// chosen by the host so that every node at that depth is a leaf
+// (capacity / 2^depth <= 64 gives nodes of <= 80 values).  vals/ticks are
+// heap-indexed (root 1) with 2^(depth+1) entries; ticks start (and end) 0.
+__global__ void pairwise_sum_kernel(const double* __restrict__ a,
+                                    const long long* __restrict__ m_p, int depth,
+                                    double* __restrict__ vals, unsigned* __restrict__ ticks,
+                                    double* __restrict__ out) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t(1) << depth)) return;
+    int64_t lo = 0, n = *m_p;
+    int64_t node = 1;
+    int d = 0;
+    while (n > 128) {
+        int64_t n2 = n / 2;
+        n2 -= n2 % 8;
+        const int bit = (int)((t >> (depth - 1 - d)) & 1);
+        if (bit) {
+            lo += n2;
+            n -= n2;
+        } else {
+            n = n2;
+        }
+        node = 2 * node + bit;
+        ++d;
+    }
+    if (d < depth && (t & ((int64_t(1) << (depth - d)) - 1)) != 0) return;  // not the representative
+    double v = pairwise_leaf(a + lo, n);
+    while (node > 1) {
+        vals[node] = v;
+        __threadfence();
+        const int64_t p = node >> 1;
+        if (atomicAdd(ticks + p, 1u) == 0) return;  // the sibling finishes the parent
+        ticks[p] = 0;
+        __threadfence();
+        const double other = *(volatile double*)(vals + (node ^ 1));
+        v = (node & 1) ? __dadd_rn(other, v) : __dadd_rn(v, other);
+        node = p;
+    }
+    *out = v;
 }
 
 __global__ void finalize_kernel(double* __restrict__ acc, double* __restrict__ sum,

@@ -304,7 +304,10 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
         }
     }
     ++L.iters;
-    if (L.iters > a.max_sweeps32 && !done) {  // sweep guard, search.py:513-516
+    // sweep guard (search.py:513-516): the reference raises once its sweep
+    // count exceeds the limit, even when the last particle finished in that
+    // very sweep -- so a lane finishing on step limit + 1 raises too
+    if (L.iters > a.max_sweeps32) {
         atomicOr(C.sh + SC_ERR, 1u);
         done = true;
     }
@@ -428,6 +431,7 @@ template <int THREADS, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB) walk_kernel(const WalkArgs a) {
     static_assert(THREADS <= MAX_CTA_THREADS, "one shared lane slot per thread");
     constexpr unsigned FULL = 0xffffffffu;
+    if (!gate_open(a, false)) return;  // v1 launches never set gate_pick
     const int lane = threadIdx.x & 31;
     __shared__ unsigned shc[SC_N];
     __shared__ uint64_t sdig[THREADS];
@@ -581,11 +585,9 @@ __device__ __forceinline__ int claim_chunk(const WalkArgs& a, const WorkSoA& W, 
 // arrays into a stage (plain loads: one latency per 32 particles; measured
 // faster than splitting them into cp.async groups), including the starting
 // element's record.  Flags: bit 24 = walkable (flying and localized), bit 25
-// = flying.  The flying particles' weights are summed per chunk into `wsum`
-// (the recorded source weight of device-input moves).
+// = flying.
 struct DirectArgs {
     int64_t lo, hi;  // particles [lo, hi) of this launch (slots through a.order if set)
-    double* wsum;    // nullable
 };
 
 __device__ __forceinline__ int claim_direct(const WalkArgs& a, const DirectArgs& d, WarpStage& st) {
@@ -596,7 +598,6 @@ __device__ __forceinline__ int claim_direct(const WalkArgs& a, const DirectArgs&
     base = __shfl_sync(FULL, base, 0);
     const int64_t left = (d.hi - d.lo) - (int64_t)base;
     const int n = left <= 0 ? 0 : (left >= STAGE_N ? STAGE_N : (int)left);
-    double wv = 0.0;
     if (lane < n) {
         const int64_t t = (int64_t)base + lane;
         const int64_t i = a.order ? (int64_t)a.order[t] : d.lo + t;
@@ -612,7 +613,6 @@ __device__ __forceinline__ int claim_direct(const WalkArgs& a, const DirectArgs&
         st.dz[lane] = a.dest[3 * i + 2];
         const double w = a.score ? a.weight[i] : 0.0;
         st.w[lane] = w;
-        if (fly) wv = w;
         st.seg[lane] = a.seg_total[i];
         st.e[lane] = el;
         st.g[lane] = a.score ? a.group[i] : 0;
@@ -623,10 +623,6 @@ __device__ __forceinline__ int claim_direct(const WalkArgs& a, const DirectArgs&
             const int4* rp = reinterpret_cast<const int4*>(a.rec + el);
             st.r0[lane] = ldg_mesh(rp);
         }
-    }
-    if (d.wsum) {
-        for (int o = 16; o > 0; o >>= 1) wv += __shfl_xor_sync(FULL, wv, o);
-        if (lane == 0 && wv != 0.0) atomicAdd(d.wsum, wv);
     }
     __syncwarp();
     return n;
@@ -640,6 +636,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
                        const DirectArgs D) {
     static_assert(THREADS <= MAX_CTA_THREADS, "one shared lane slot per thread");
     constexpr unsigned FULL = 0xffffffffu;
+    if (!gate_open(a, DIRECT)) return;
     // the warps' stages in dynamic shared memory: double-buffered for the
     // stage kernel's cp.async prefetch, one per warp for the direct refill
     extern __shared__ __align__(16) unsigned char dyn_smem[];
@@ -757,15 +754,14 @@ __global__ void __launch_bounds__(THREADS, MINB)
 // particles get an empty digest.
 // Particles [lo, lo + a.count) of this move; work items go to W (already
 // offset by the caller).  A flying particle with element < 0 is not staged
-// and counted (the move then reports it); wsum (nullable) accumulates the
-// flying particles' weights (device-resident inputs).
+// and counted (the move then reports it).
 __global__ void stage_kernel(const WalkArgs a, const WorkSoA W, int64_t* __restrict__ nwork,
-                             int64_t lo, double* __restrict__ wsum) {
+                             int64_t lo) {
+    if (!gate_open(a, false)) return;
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     bool fly = false;
     int64_t i = 0;
-    double wv = 0.0;
     if (t < a.count) {
         i = a.order ? (int64_t)a.order[t] : lo + t;
         fly = a.fly_in[i] != 0;
@@ -773,15 +769,10 @@ __global__ void stage_kernel(const WalkArgs a, const WorkSoA W, int64_t* __restr
             a.digest[i] = DIGEST_INIT;
             a.dcount[i] = 0;
         }
-        if (fly && wsum) wv = a.weight[i];
         if (fly && a.element[i] < 0) {
             atomicAdd(a.counters + C_UNLOC, 1ull);
             fly = false;
         }
-    }
-    if (wsum) {
-        for (int o = 16; o > 0; o >>= 1) wv += __shfl_xor_sync(0xffffffffu, wv, o);
-        if (lane == 0 && wv != 0.0) atomicAdd(wsum, wv);
     }
     const unsigned m = __ballot_sync(0xffffffffu, fly);
     if (!m) return;

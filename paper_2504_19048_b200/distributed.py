@@ -45,13 +45,16 @@ def reduce_summary(s: TraceSummary | None, device=None, group=None) -> TraceSumm
     return TraceSummary(int(m.item()), *(int(x) for x in t.tolist()))
 
 
-def reduce_batch_(tally, source_weight: float, device=None, group=None) -> float:
-    """In-place sum of the per-rank batch tallies; returns the global source
-    weight (sum of the ranks' recorded weights)."""
-    import torch
+def reduce_tally_(tally, group=None) -> None:
+    """In-place sum of the per-rank batch tallies (the one collective per batch)."""
     import torch.distributed as dist
     dist.all_reduce(tally, group=group)
-    w = torch.tensor([float(source_weight)], dtype=torch.float64, device=device)
+
+
+def all_reduce_scalar(x: float, device=None, group=None) -> float:
+    import torch
+    import torch.distributed as dist
+    w = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(w, group=group)
     return float(w.item())
 
@@ -88,6 +91,7 @@ class ShardedMeshTally:
         self.num_particles = int(num_particles)
         self.lo, self.hi = shard_bounds(self.num_particles, self.rank, self.world)
         self.presharded = presharded
+        self._source_weight = 0.0
         if _tally_factory is None:
             from .tally import MeshTally
             if device is None:
@@ -119,22 +123,42 @@ class ShardedMeshTally:
         if pos.size != 3 * count:
             raise ValueError(f"positions must hold 3*count = {3 * count} floats, got {pos.size}")
         self.mt.initialize_particle_location(self._local(pos, count, 3))
+        self._source_weight = 0.0  # tally.py:245
 
     def move_to_next_location(self, destinations, flying, weights, groups=None):
         fly = np.asarray(flying).reshape(-1)
         count = fly.size
+        if count == 0:  # tally.py:258-260: nothing moved, nothing recorded
+            return None
         g = None if groups is None else self._local(groups, count, 1)
+        recording = self._source_weight == 0.0
+        if recording:
+            self.mt.source_weight = 0.0  # this rank records this move's flying weight
         s = self.mt.move_to_next_location(self._local(destinations, count, 3),
                                           self._local(fly, count, 1),
                                           self._local(weights, count, 1), g)
+        if recording:
+            # The reference records the batch's source weight on the first move
+            # whose flying weight is non-zero (tally.py:267-269) -- decided on
+            # the GLOBAL move, so a rank whose shard is empty or not flying on
+            # that move does not record a later one of its own.
+            w = all_reduce_scalar(self.mt.source_weight if s is not None else 0.0,
+                                  self.device, self.group)
+            self._source_weight = w
+            self.mt.source_weight = w if w != 0.0 else 0.0
         return reduce_summary(s, self.device, self.group)
 
+    @property
+    def source_weight(self) -> float:
+        return self._source_weight
+
     def finalize_batch(self, source_weight: float | None = None) -> None:
-        w_local = self.mt.source_weight
-        w = reduce_batch_(self._tally, w_local, self.device, self.group)
-        if source_weight is not None:
-            w = float(source_weight)
+        w = self._source_weight if source_weight is None else float(source_weight)
+        if not w or w <= 0.0:
+            raise RuntimeError("no source weight recorded for this batch; pass source_weight")
+        reduce_tally_(self._tally, self.group)
         self.mt.finalize_batch(w)
+        self._source_weight = 0.0
 
     def flux(self):
         return self.mt.flux()

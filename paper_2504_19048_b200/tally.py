@@ -405,12 +405,18 @@ class MeshTally:
                                device_events=device_events)
 
     # ------------------------------------------------------------------ extras
+    # dtypes a CUDA tensor argument must have: the library reads its bits as
+    # float64 / int8 / int32 (the reference converts host arrays with
+    # np.asarray(dtype=...); a device buffer is never converted silently)
+    _DEVICE_DTYPES = {8: ("float64",), 1: ("int8", "uint8", "bool"), 4: ("int32",)}
+
     def _check_tensor(self, t, itemsize):
         if not t.is_contiguous():
             raise ValueError("device arrays must be contiguous")
-        if t.element_size() != itemsize:
-            raise ValueError(f"device array has element size {t.element_size()}, "
-                             f"expected {itemsize}")
+        dt = str(t.dtype).replace("torch.", "")
+        if dt not in self._DEVICE_DTYPES[itemsize]:
+            raise TypeError(f"device array has dtype {dt}, expected "
+                            f"{' or '.join(self._DEVICE_DTYPES[itemsize])}")
         if t.device.index is not None and t.device.index != self.device:
             raise ValueError(f"tensor on cuda:{t.device.index}, handle on cuda:{self.device}")
 

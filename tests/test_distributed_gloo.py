@@ -40,6 +40,10 @@ class OracleShard:
     def source_weight(self):
         return self.t.source_weight
 
+    @source_weight.setter
+    def source_weight(self, w):
+        self.t.source_weight = w
+
     def initialize_particle_location(self, pos):
         self.t.initialize_particle_location(pos)
 
@@ -71,6 +75,18 @@ def _workload():
     return mesh, pos, moves
 
 
+def _fly(batch, move, n):
+    fly = np.ones(n, np.int8)
+    if batch == 1:
+        fly[::3] = 0  # some particles sit out a move
+    if batch == 2 and move == 0:
+        fly[1000:] = 0  # only rank 0's shard flies: rank 1 must not record move 2
+    return fly
+
+
+NBATCH = 3
+
+
 def _worker(rank, world, port, q):
     sys.path[:0] = [str(ROOT), str(ROOT / "oracle"), str(ROOT / "tests")]
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -81,15 +97,13 @@ def _worker(rank, world, port, q):
         n = pos.shape[0]
         sh = ShardedMeshTally(mesh, n, 2, _tally_factory=OracleShard)
         out = []
-        for batch in range(2):
+        for batch in range(NBATCH):
             sh.initialize_particle_location(pos)
             sums = []
-            for d, w, g in moves:
-                fly = np.ones(n, np.int8)
-                if batch == 1:
-                    fly[::3] = 0  # some particles sit out a move
-                s = sh.move_to_next_location(d, fly, w, g)
+            for mv, (d, w, g) in enumerate(moves):
+                s = sh.move_to_next_location(d, _fly(batch, mv, n), w, g)
                 sums.append(tuple(s.__dict__.values()))
+            sums.append(sh.source_weight)
             sh.finalize_batch()
             out.append(sums)
         mean, rel = sh.flux()
@@ -105,14 +119,12 @@ def test_sharded_equals_single_process():
     n = pos.shape[0]
     ref = orc.OracleTally(mesh, n, 2, threads=1)
     ref_out = []
-    for batch in range(2):
+    for batch in range(NBATCH):
         ref.initialize_particle_location(pos)
         sums = []
-        for d, w, g in moves:
-            fly = np.ones(n, np.int8)
-            if batch == 1:
-                fly[::3] = 0
-            sums.append(tuple(ref.move_to_next_location(d, fly, w, g)))
+        for mv, (d, w, g) in enumerate(moves):
+            sums.append(tuple(ref.move_to_next_location(d, _fly(batch, mv, n), w, g)))
+        sums.append(ref.source_weight)
         ref.finalize_batch()
         ref_out.append(sums)
     rmean, rrel = ref.flux()
@@ -132,8 +144,12 @@ def test_sharded_equals_single_process():
     bounds = [(r[4], r[5]) for r in results]
     assert bounds == [(0, 1501), (1501, 3001)]
     for rank, out, mean, rel, lo, hi in results:
-        # summaries: sums of counters, max of sweeps -> identical to one process
-        assert out == ref_out
+        # summaries: sums of counters, max of sweeps -> identical to one process;
+        # the recorded source weight is the global first move's (two partial
+        # sums: equal to the single-process pairwise sum within rounding)
+        for got, want in zip(out, ref_out):
+            assert got[:-1] == want[:-1]
+            assert got[-1] == pytest.approx(want[-1], rel=1e-14)
         den = np.maximum(np.abs(mean), np.abs(rmean))
         assert (np.abs(mean - rmean) <= 1e-12 * den).all()
         assert np.abs(rel - rrel).max() < 1e-5
