@@ -234,10 +234,105 @@ def cpu_model():
 
 # ---------------------------------------------------------------------------
 
+def _import_stock_reference():
+    """The unmodified reference package installed in baseline/_ref (numba);
+    None when it is not importable on this host."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "meshtally").is_dir():
+        return None
+    sys.path.insert(0, str(ref))
+    try:
+        import meshtally  # noqa: F401
+        import numba  # noqa: F401
+    except Exception:
+        sys.path.remove(str(ref))
+        return None
+    return meshtally
+
+
+def run_reference_stock(args, mt_mod):
+    """The reference's own CPU path (baseline/_ref, numba, unmodified) through
+    its public MeshTally API: per step, the localized start state is restored
+    and one move_to_next_location (load_step + trace_and_score,
+    search.py:492-517) + finalize_batch runs over a bounded sample of the same
+    workload, on every host core (numba.set_num_threads(T) with T tally slabs,
+    the configuration in which the reference's threads > 1 path is correct,
+    SURVEY.md §8b)."""
+    import numba
+    T = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    T = max(1, min(T, numba.config.NUMBA_NUM_THREADS))
+    numba.set_num_threads(T)
+    t_build = time.perf_counter()
+    mesh = mt_mod.build_cube_mesh(args.n)
+    t_build = time.perf_counter() - t_build
+    pos, dest = workload(args.particles, args.sigma_t, 0)
+    per_step = float(os.environ.get("BENCH_REF_STEP_S", "2.0"))
+
+    def make(k):
+        t = mt_mod.MeshTally(mesh, k, threads=T)
+        t.initialize_particle_location(pos[:k])
+        b, ws = t._batch, t._ws
+        snap = [(a, a[:k].copy()) for a in (b.position, b.element, b.alive, ws.entry_face,
+                                             ws.stuck, ws.outcome, ws.seg_total)]
+        return t, snap
+
+    fly_all = np.ones(args.particles, np.int8)
+    w_all = np.ones(args.particles)
+
+    def step(t, snap, k):
+        for a, v in snap:
+            a[:k] = v
+        s = t.move_to_next_location(dest[:k], fly_all[:k], w_all[:k])
+        t.finalize_batch()
+        return s
+
+    # JIT warm-up and sizing on a small sample, then the bounded sample
+    k = min(50_000, args.particles)
+    t, snap = make(k)
+    step(t, snap, k)
+    t0 = time.perf_counter()
+    s = step(t, snap, k)
+    dt = time.perf_counter() - t0
+    k = int(min(args.particles, max(k, k * per_step / max(dt, 1e-3))))
+    t, snap = make(k)
+    for _ in range(args.warmup):
+        step(t, snap, k)
+    ev = 0
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ev += step(t, snap, k).events
+    dt = time.perf_counter() - t0
+    val = ev / dt
+    rank, world, _ = env_rank()
+    sample = (f"first {k:,} of the {args.particles:,} particles per step (same workload); "
+              "stock reference from baseline/_ref (meshtally 0.1.0, numba "
+              f"{numba.__version__}): MeshTally(threads={T}).move_to_next_location + "
+              "finalize_batch, localized start state restored per step (untimed "
+              "localization)")
+    out = {
+        "impl": "reference",
+        "metric": "tet-crossings/s", "value": val, "unit": "crossings/s",
+        "particle_moves_per_s": k * args.steps / dt,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config(args, 1, mesh.num_elements),
+        "cpu_baseline": {"value": val, "unit": "crossings/s", "cores": T, "kind": "reference",
+                         "sample": sample, "cpu": cpu_model(),
+                         "mesh_build_s": round(t_build, 3)},
+        "e2e": {"value": val, "unit": "crossings/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
 def run_reference(args):
     rank, world, local = env_rank()
     if rank != 0:
         return
+    mt_mod = None if os.environ.get("BENCH_REF_PORT") else _import_stock_reference()
+    if mt_mod is not None:
+        return run_reference_stock(args, mt_mod)
     from paper_2504_19048_b200 import build_cube_mesh
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle as orc
@@ -289,6 +384,57 @@ def run_reference(args):
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
+
+
+def roofline(stats, steps, walk_s, alg_gbps, hbm_peak, peak_src, clk):
+    """The walk kernel against each resource it can be bound by, from the live
+    kernel time and the per-crossing demands of the committed ncu capture of
+    the same kernel (profiles/walk_sol.json, tools/ncu_walk_sol.py): warp
+    instruction issue (4 per SM per cycle at the measured SM clock), the
+    L1TEX LSU data pipe (1 wavefront per SM per cycle), L2 (the measured
+    random 32-byte-sector gather rate, profiles/r02_l2_peak.json), DRAM (the
+    measured HBM copy rate).  `bound` is the resource with the highest
+    fraction; SURVEY §8d's algorithmic-byte figure against HBM stays as
+    `alg_frac` (the walk's gathers are served by L1/L2, not HBM)."""
+    ev = stats["events"] / steps  # crossings per launch
+    t = walk_s / steps
+    sol_p, l2_p = ROOT / "profiles" / "walk_sol.json", ROOT / "profiles" / "r02_l2_peak.json"
+    out = {"kernel": "walk_staged_kernel<192,2,0,1>", "kernel_ms_per_step": 1e3 * t,
+           "alg_gbps": alg_gbps, "alg_frac": alg_gbps / hbm_peak,
+           "algorithmic_bytes": "133 B/crossing + 100 B/move (SURVEY.md §8d) vs HBM",
+           "hbm_peak_source": peak_src}
+    try:
+        sol = json.loads(sol_p.read_text())
+        l2 = json.loads(l2_p.read_text())
+    except (OSError, ValueError):
+        out.update({"bound": "hbm", "achieved": alg_gbps, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": alg_gbps / hbm_peak, "traffic": None})
+        return out
+    pc = sol["per_crossing"]
+    sms = int(l2.get("sms", 148))
+    mhz = clk.get("sm_mhz") or clk.get("sm_max_mhz") or 1965.0
+    hz = float(mhz) * 1e6
+    units = {
+        "issue": (pc["warp_instructions"] * ev / t, 4 * sms * hz, "warp-inst/s"),
+        "l1tex_lsu": (pc["lsu_wavefronts"] * ev / t, sms * hz, "wavefronts/s"),
+        "l2": (pc["l2_bytes"] * ev / t / 1e9,
+               float(l2.get("l2_gather32_v8_gbs") or l2["l2_gather32_gbs"]), "GB/s"),
+        "hbm": (pc["dram_bytes"] * ev / t / 1e9, hbm_peak, "GB/s"),
+    }
+    fr = {k: a / p for k, (a, p, _) in units.items()}
+    bound = max(fr, key=fr.get)
+    a, p, unit = units[bound]
+    out.update({"bound": bound, "achieved": a, "peak": p, "unit": unit, "frac": fr[bound],
+                "traffic": sol["per_launch"]["dram_bytes"],
+                "traffic_source": f"dram__bytes_read+write.sum of one launch, {sol['source']}",
+                "fracs": fr,
+                "units": {k: {"achieved": a, "peak": p, "unit": u}
+                          for k, (a, p, u) in units.items()},
+                "sol_source": "profiles/walk_sol.json per-crossing demands x live crossings "
+                              "/ live kernel time; peaks: 4 warp-inst and 1 LSU wavefront per "
+                              f"SM-cycle at {mhz} MHz x {sms} SMs, L2 = measured 32-B sector "
+                              "gather rate (profiles/r02_l2_peak.json), HBM = " + peak_src})
+    return out
 
 
 def run_ours(args):
@@ -385,29 +531,17 @@ def run_ours(args):
     # roofline of the walk kernel (rank-local, CUDA events on the library stream)
     walk_s = stats["walk_ms"] / 1e3
     alg_bytes = B_CROSSING * stats["events"] + B_MOVE * stats["moves"]
-    achieved = alg_bytes / walk_s / 1e9
-    peaks_p = ROOT / "MEASURED_PEAKS.json"
-    peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    alg_gbps = alg_bytes / walk_s / 1e9
+    hbm_peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
     try:
-        peak = float(json.loads(peaks_p.read_text())["hbm_gbs"])
+        hbm_peak = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
         peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
     except (OSError, ValueError, KeyError, TypeError):
         pass
-    traffic = None
-    tp = ROOT / "profiles" / "walk_dram_traffic.json"
-    if tp.exists():
-        try:
-            traffic = json.loads(tp.read_text()).get("bytes_per_launch")
-        except Exception:
-            traffic = None
 
-    # e2e through the public API with pinned host buffers
-    e2e = None
-    if not args.no_e2e:
-        h_pos = torch.from_numpy(pos).pin_memory().numpy()
-        h_dest = torch.from_numpy(dest).pin_memory().numpy()
-        h_fly = torch.ones(P, dtype=torch.int8).pin_memory().numpy()
-        h_w = torch.ones(P, dtype=torch.float64).pin_memory().numpy()
+    # e2e through the public API with host buffers: pinned (the contract's
+    # case) and ordinary pageable numpy arrays (what a drop-in user passes)
+    def e2e_run(h_pos, h_dest, h_fly, h_w):
         ev_e2e = 0
 
         def e2e_step():
@@ -435,11 +569,23 @@ def run_ours(args):
         if dist is not None:
             dist.all_reduce(ms2, op=dist.ReduceOp.MAX)
             dist.all_reduce(ev2)
-        e2e = {"value": float(ev2.item()) / (float(ms2.item()) / 1e3), "unit": "crossings/s",
-               "h2d_bytes_per_step": int(h_pos.nbytes + h_dest.nbytes + h_fly.nbytes
-                                         + h_w.nbytes) * world,
-               "d2h_bytes_per_step": 48 * world,
-               "ms_per_step": float(ms2.item()) / args.steps}
+        return {"value": float(ev2.item()) / (float(ms2.item()) / 1e3), "unit": "crossings/s",
+                "h2d_bytes_per_step": int(h_pos.nbytes + h_dest.nbytes + h_fly.nbytes
+                                          + h_w.nbytes) * world,
+                "d2h_bytes_per_step": 48 * world,
+                "ms_per_step": float(ms2.item()) / args.steps}
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_run(torch.from_numpy(pos).pin_memory().numpy(),
+                      torch.from_numpy(dest).pin_memory().numpy(),
+                      torch.ones(P, dtype=torch.int8).pin_memory().numpy(),
+                      torch.ones(P, dtype=torch.float64).pin_memory().numpy())
+        e2e["host_memory"] = "pinned"
+        pg = e2e_run(pos, dest, np.ones(P, np.int8), np.ones(P))
+        e2e["pageable"] = {"value": pg["value"], "ms_per_step": pg["ms_per_step"],
+                           "host_memory": "pageable numpy (library-staged through a pinned "
+                                          "ring by host threads)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -459,11 +605,8 @@ def run_ours(args):
             "config": config(args, world, mesh.num_elements),
             "crossings_per_move": events_all / max(moves_all, 1.0),
             "e2e": e2e,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "peak_source": peak_src,
-                         "kernel": "walk_staged_kernel", "kernel_ms_per_step": stats["walk_ms"] / args.steps,
-                         "algorithmic_bytes": "133 B/crossing + 100 B/move (SURVEY.md §8d)"},
+            "roofline": roofline(stats, args.steps, walk_s, alg_gbps, hbm_peak, peak_src,
+                                 clocks.summary()),
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
             "gpu_launches": stats["kernels"],

@@ -80,6 +80,8 @@ static bt_status set_err(bt_status s, const char* fmt, ...) {
 // ---------------------------------------------------------------------------
 // handle
 
+struct HostStager;
+
 struct bt_tally {
     int dev = 0;
     int num_sms = 148;
@@ -146,6 +148,7 @@ struct bt_tally {
     int move_chunks = 0;                      // host-input pipeline depth (0 = auto)
     int locate_lanes = 0;                     // grid search lanes per particle (0 = default)
     std::vector<double> host_sel;             // host scratch: weights of flying particles
+    HostStager* stager = nullptr;             // pageable host inputs (host_stage.cuh)
     // transport (allocated on first bt_transport_run)
     double* col_tally = nullptr;
     double* col_sum = nullptr;
@@ -202,6 +205,22 @@ static bt_status ensure_device(bt_tally* h) {
         if (s__ != BT_OK) return s__;  \
     } while (0)
 
+#include "host_stage.cuh"
+
+// host -> device copy of a caller buffer on `st`: DMA straight from pinned
+// memory, through the pinned ring + host threads from pageable memory.
+// Returns once `src` has been read.
+static bt_status h2d(bt_tally* h, void* dst, const void* src, size_t bytes, cudaStream_t st,
+                     bool pageable) {
+    if (!bytes) return BT_OK;
+    if (!pageable) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+        return BT_OK;
+    }
+    if (!h->stager) h->stager = new HostStager();
+    return h->stager->copy(dst, src, bytes, st);
+}
+
 static bt_status free_all(bt_tally* h) {
     void* ptrs[] = {h->rec, h->vtx, h->xrec, h->xsel, h->cell_start, h->cand, h->lam, h->pos, h->element, h->alive,
                     h->entry, h->stuck, h->outcome, h->seg_total, h->group, h->dest, h->fly,
@@ -215,6 +234,11 @@ static bt_status free_all(bt_tally* h) {
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->hcounters) cudaFreeHost(h->hcounters);
+    if (h->stager) {
+        h->stager->release();
+        delete h->stager;
+        h->stager = nullptr;
+    }
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
     if (h->ev2) cudaEventDestroy(h->ev2);
@@ -775,7 +799,8 @@ static bt_status launch_walk(bt_tally* h, WalkArgs a, int64_t lo, int64_t count,
         W.px += lo; W.py += lo; W.pz += lo; W.dx += lo; W.dy += lo; W.dz += lo;
         W.r0 += lo;
         W.w += lo; W.seg += lo; W.idx += lo; W.e += lo; W.g += lo; W.fl += lo;
-        stage_kernel<<<grid_for(count, 256), 256, 0, st>>>(a, W, nwork, lo);
+        stage_kernel<<<std::min<int64_t>(grid_for(count, 256), 16 * h->num_sms), 256, 0, st>>>(
+            a, W, nwork, lo);
         CK(cudaGetLastError());
         h->kernels += 1;
     }
@@ -935,12 +960,12 @@ bt_status bt_initialize_particle_location(bt_tally* h, const double* positions, 
         if (!h->init_stage) TRY(dalloc(&h->init_stage, 3 * h->cap));
         CK(cudaStreamWaitEvent(h->cstream, h->ev_loc, 0));  // previous localization done
         const int nch = (int)std::min<int64_t>(count >= (4 << 20) ? 4 : 1, count);
+        const bool pageable = is_pageable(positions);
         LocateArgs la = locate_args(h, h->init_stage, count);
         for (int c = 0; c < nch; ++c) {
             const int64_t lo = count * c / nch, hi = count * (c + 1) / nch;
-            CK(cudaMemcpyAsync(h->init_stage + 3 * lo, positions + 3 * lo,
-                               sizeof(double) * 3 * (hi - lo), cudaMemcpyHostToDevice,
-                               h->cstream));
+            TRY(h2d(h, h->init_stage + 3 * lo, positions + 3 * lo,
+                    sizeof(double) * 3 * (hi - lo), h->cstream, pageable));
             CK(cudaEventRecord(h->evchunk[c], h->cstream));
             CK(cudaStreamWaitEvent(h->stream, h->evchunk[c], 0));
             la.lo = lo;
@@ -950,13 +975,15 @@ bt_status bt_initialize_particle_location(bt_tally* h, const double* positions, 
         CK(cudaEventRecord(h->evc0, h->cstream));
         CK(cudaEventRecord(h->ev_loc, h->stream));
         CK(cudaEventRecord(h->ev3, h->stream));
-        CK(cudaEventSynchronize(h->evc0));
+        // a pinned caller buffer is read by the DMA engine: wait for it; a
+        // pageable one has already been copied into the library's ring
+        if (!pageable) CK(cudaEventSynchronize(h->evc0));
         h->call_pending = true;
         return BT_OK;
     }
     if (host) {
-        CK(cudaMemcpyAsync(h->dest, positions, sizeof(double) * 3 * count,
-                           cudaMemcpyHostToDevice, h->stream));
+        TRY(h2d(h, h->dest, positions, sizeof(double) * 3 * count, h->stream,
+                is_pageable(positions)));
         target = h->dest;
     }
     LocateArgs la = locate_args(h, target, count);
@@ -984,7 +1011,7 @@ bt_status bt_initialize_particle_location(bt_tally* h, const double* positions, 
 // summation tree (move_prep.cuh) into dcounters[DC_SOURCE_WEIGHT] -- the
 // same bits as the host-input path and the reference (tally.py:267-269).
 static bt_status device_source_weight(bt_tally* h, const int8_t* flying, const double* weights,
-                                      int64_t count) {
+                                      int64_t count, cudaStream_t st) {
     if (!h->wsel) {
         int depth = 0;
         while ((h->cap >> depth) > 64) ++depth;
@@ -1002,10 +1029,9 @@ static bt_status device_source_weight(bt_tally* h, const int8_t* flying, const d
     }
     size_t b = h->wsel_tmp_bytes;
     long long* m = reinterpret_cast<long long*>(h->dcounters + DC_SELECTED);
-    CK(cub::DeviceSelect::Flagged(h->wsel_tmp, b, weights, flying, h->wsel, m, (int)count,
-                                  h->stream));
+    CK(cub::DeviceSelect::Flagged(h->wsel_tmp, b, weights, flying, h->wsel, m, (int)count, st));
     const int64_t nthreads = (int64_t)1 << h->wsel_depth;
-    pairwise_sum_kernel<<<grid_for(nthreads, 256), 256, 0, h->stream>>>(
+    pairwise_sum_kernel<<<grid_for(nthreads, 256), 256, 0, st>>>(
         h->wsel, m, h->wsel_depth, h->wsel_vals, h->wsel_ticks,
         reinterpret_cast<double*>(h->dcounters + DC_SOURCE_WEIGHT));
     CK(cudaGetLastError());
@@ -1079,6 +1105,8 @@ bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, cons
             const int sh = c == 0 ? nch : nch - 1 - c;
             return (int64_t)((double)count / (double)(1ll << sh));
         };
+        const bool pg_dest = is_pageable(destinations), pg_fly = is_pageable(flying),
+                   pg_w = is_pageable(weights), pg_g = groups && is_pageable(groups);
         TRY(walk_begin(h));
         // odd chunks go to a second stream, so chunk c+1's CTAs take the SMs
         // that chunk c's tail frees instead of waiting for its last walk
@@ -1089,14 +1117,12 @@ bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, cons
             const int64_t n = hi - lo;
             if (n <= 0) continue;
             cudaStream_t st = (c & 1) ? h->stream2 : h->stream;
-            CK(cudaMemcpyAsync(h->dest + 3 * lo, destinations + 3 * lo, sizeof(double) * 3 * n,
-                               cudaMemcpyHostToDevice, h->cstream));
-            CK(cudaMemcpyAsync(h->fly + lo, flying + lo, n, cudaMemcpyHostToDevice, h->cstream));
-            CK(cudaMemcpyAsync(h->weight + lo, weights + lo, sizeof(double) * n,
-                               cudaMemcpyHostToDevice, h->cstream));
+            TRY(h2d(h, h->dest + 3 * lo, destinations + 3 * lo, sizeof(double) * 3 * n,
+                    h->cstream, pg_dest));
+            TRY(h2d(h, h->fly + lo, flying + lo, n, h->cstream, pg_fly));
+            TRY(h2d(h, h->weight + lo, weights + lo, sizeof(double) * n, h->cstream, pg_w));
             if (groups)
-                CK(cudaMemcpyAsync(h->group + lo, groups + lo, sizeof(int32_t) * n,
-                                   cudaMemcpyHostToDevice, h->cstream));
+                TRY(h2d(h, h->group + lo, groups + lo, sizeof(int32_t) * n, h->cstream, pg_g));
             CK(cudaEventRecord(h->evchunk[c], h->cstream));
             CK(cudaStreamWaitEvent(st, h->evchunk[c], 0));
             TRY(walk_enqueue(h, a, lo, hi, c, nullptr, st));
@@ -1120,8 +1146,14 @@ bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, cons
             CK(cudaGetLastError());
             h->kernels += 1;
         }
-        if (need_w) TRY(device_source_weight(h, flying, weights, count));
+        if (need_w) {  // on the second stream: overlaps the walk (its tail, at least)
+            CK(cudaEventRecord(h->ev_s1, h->stream));
+            CK(cudaStreamWaitEvent(h->stream2, h->ev_s1, 0));
+            TRY(device_source_weight(h, flying, weights, count, h->stream2));
+            CK(cudaEventRecord(h->ev_s2, h->stream2));
+        }
         TRY(walk_enqueue(h, a, 0, count, 0, nullptr, true));
+        if (need_w) CK(cudaStreamWaitEvent(h->stream, h->ev_s2, 0));
         s = walk_end(h, a.max_sweeps, summary);
         if (h->hcounters[15] & 2ull)
             return set_err(BT_EINDEX, "group out of range [0, %d)", h->ngroups);
@@ -1643,11 +1675,20 @@ bt_status bt_load_step(bt_tally* h, const double* destinations, const int8_t* fl
         for (int64_t i = 0; i < count; ++i)
             if (groups[i] < 0 || groups[i] >= h->ngroups)
                 return set_err(BT_EINDEX, "group %d out of range [0, %d)", groups[i], h->ngroups);
-    CK(cudaMemcpyAsync(h->dest, destinations, sizeof(double) * 3 * count, kind, h->stream));
-    CK(cudaMemcpyAsync(h->fly, flying, count, kind, h->stream));
-    CK(cudaMemcpyAsync(h->weight, weights, sizeof(double) * count, kind, h->stream));
-    if (groups)
-        CK(cudaMemcpyAsync(h->group, groups, sizeof(int32_t) * count, kind, h->stream));
+    if (mem_kind == BT_MEM_HOST) {
+        TRY(h2d(h, h->dest, destinations, sizeof(double) * 3 * count, h->stream,
+                is_pageable(destinations)));
+        TRY(h2d(h, h->fly, flying, count, h->stream, is_pageable(flying)));
+        TRY(h2d(h, h->weight, weights, sizeof(double) * count, h->stream, is_pageable(weights)));
+        if (groups)
+            TRY(h2d(h, h->group, groups, sizeof(int32_t) * count, h->stream, is_pageable(groups)));
+    } else {
+        CK(cudaMemcpyAsync(h->dest, destinations, sizeof(double) * 3 * count, kind, h->stream));
+        CK(cudaMemcpyAsync(h->fly, flying, count, kind, h->stream));
+        CK(cudaMemcpyAsync(h->weight, weights, sizeof(double) * count, kind, h->stream));
+        if (groups)
+            CK(cudaMemcpyAsync(h->group, groups, sizeof(int32_t) * count, kind, h->stream));
+    }
     load_step_kernel<<<grid_for(h->cap, 256), 256, 0, h->stream>>>(h->fly, count, h->cap,
                                                                     h->tr_fly, h->alive);
     CK(cudaGetLastError());
