@@ -440,11 +440,20 @@ def roofline(stats, steps, walk_s, alg_gbps, hbm_peak, peak_src, clk):
 def run_ours(args):
     import torch
     rank, world, local = env_rank()
+    # BENCH_SHARE_GPU=1: every rank on cuda:0 over gloo -- a smoke test of the
+    # N > 1 path on a one-GPU box (tests/test_gpu_bench_dist.py); NCCL refuses
+    # two ranks on one GPU
+    share = os.environ.get("BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     dist = None
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 

@@ -105,6 +105,31 @@ bt_status bt_create(const double *vertices, int64_t num_vertices, const int32_t 
                     const double *bbox, const double *centroid0, int64_t num_particles,
                     int32_t num_groups, int32_t device, bt_tally **out);
 
+/*
+ * One handle over several GPUs of this process (SURVEY §8b "ndev", §8e;
+ * PAPER.md:296): `num_devices` ordinals in `devices`; particles are sharded in
+ * contiguous ranges [r*ceil(N/P), (r+1)*ceil(N/P)), the mesh is replicated,
+ * each GPU keeps a private tally, and bt_finalize_batch sums the tallies with
+ * one NCCL all-reduce over NVLink (ncclCommInitAll; peer copies when NCCL is
+ * absent or an ordinal repeats) before the on-device finalize.  Every entry
+ * point takes the multi-GPU handle and fans out on one host thread per GPU:
+ * host arrays are GLOBAL (the handle slices them), summaries are summed
+ * (sweeps: max), particle/digest readouts are gathered, BT_TALLY_BATCH is the
+ * sum over GPUs, the source weight follows the reference's rule on the whole
+ * move.  Device-memory arguments, the transport and the callback path need a
+ * one-GPU handle (BT_EINVAL otherwise); bt_shard exposes the per-GPU handles.
+ */
+bt_status bt_create_multi(const double *vertices, int64_t num_vertices, const int32_t *elements,
+                          const int32_t *adj_elem, const int8_t *adj_face, int64_t num_elements,
+                          const double *bbox, const double *centroid0, int64_t num_particles,
+                          int32_t num_groups, const int32_t *devices, int32_t num_devices,
+                          bt_tally **out);
+
+/* Number of per-GPU shards (1 for a bt_create handle) and shard `index`'s
+ * handle and particle range [lo, hi). */
+bt_status bt_num_shards(bt_tally *h, int32_t *n);
+bt_status bt_shard(bt_tally *h, int32_t index, bt_tally **shard, int64_t *lo, int64_t *hi);
+
 bt_status bt_destroy(bt_tally *h);
 
 /*
@@ -269,6 +294,56 @@ bt_status bt_read_transport_state(bt_tally *h, int64_t count, double *direction,
 /* uniform_block(seed, batch, particle, block) on the device for n keys
  * (4 x u64 each) -> 4n doubles (philox KAT hook). */
 bt_status bt_uniform_blocks(const uint64_t *keys, int64_t n, int32_t device, double *out);
+
+/* ---- standalone tally grids and scoring (tally.py:21-80) ---------------- */
+
+/* create_grid(num_elements, num_groups): a tally-only handle (no mesh, no
+ * particles) for bt_score / bt_finalize_batch / bt_read_tally / bt_flux. */
+bt_status bt_create_grid(int64_t num_elements, int32_t num_groups, int32_t device,
+                         bt_tally **out);
+/* score_track_length (kind 0: tally[e*G+g] += w * length) and
+ * score_collision (kind 1: += w / sigma_t) for n events; BT_EINDEX for an
+ * element/group out of range, BT_EINVAL for sigma_t <= 0 (nothing scored). */
+bt_status bt_score(bt_tally *h, int32_t kind, const int32_t *elements, const int32_t *groups,
+                   const double *weights, const double *values, int64_t n, int32_t mem_kind);
+/* Overwrite a tally array (E*G doubles) from host memory (the writable grid). */
+bt_status bt_write_tally(bt_tally *h, int32_t which, const double *in, int64_t n);
+bt_status bt_set_batches_completed(bt_tally *h, int64_t n);
+
+/* ---- native mesh ingest and the paper-level ABI -------- */
+
+typedef struct bt_mesh bt_mesh;
+/* read_tetmesh (mesh.py:302-331) + TetMesh.from_arrays (mesh.py:109-148):
+ * text parsed on all host threads; orientation fixed (local 2<->3 swap),
+ * degenerate elements rejected, volumes / centroids / bbox as the reference
+ * computes them (bit-identical), adjacency on GPU `device` (< 0: host sort).
+ * BT_EINVAL carries MalformedMeshError's message. */
+bt_status bt_mesh_read(const char *path, int32_t device, bt_mesh **out);
+bt_status bt_mesh_from_arrays(const double *vertices, int64_t num_vertices,
+                              const int32_t *elements, int64_t num_elements, int32_t device,
+                              bt_mesh **out);
+bt_status bt_mesh_info(const bt_mesh *m, int64_t *num_vertices, int64_t *num_elements);
+/* Copy out (any pointer may be NULL): vertices (V,3), elements (E,4),
+ * adj_elem (E,4), adj_face (E,4), volumes (E), centroids (E,3), bbox (2,3). */
+bt_status bt_mesh_arrays(const bt_mesh *m, double *vertices, int32_t *elements,
+                         int32_t *adj_elem, int8_t *adj_face, double *volumes, double *centroids,
+                         double *bbox);
+bt_status bt_mesh_destroy(bt_mesh *m);
+/* PumiTally(mesh, num_particles, ...) from a mesh object or a mesh file
+ * (tally.py:224-225: a path argument is read with read_tetmesh);
+ * the handle keeps a host copy of the mesh for bt_write_vtk. */
+bt_status bt_create_from_mesh(const bt_mesh *m, int64_t num_particles, int32_t num_groups,
+                              int32_t device, bt_tally **out);
+bt_status bt_create_from_file(const char *mesh_filename, int64_t num_particles,
+                              int32_t num_groups, int32_t device, bt_tally **out);
+/* write(filename) (tally.py:284-286 -> write_vtk, tally.py:159-189):
+ * legacy ASCII VTK of the flux, byte-identical to the reference's writer
+ * (floats as Python repr).  `volumes` may be NULL for handles made from a
+ * mesh object/file.  bt_write_flux_csv: write_flux_csv (tally.py:192-200). */
+bt_status bt_write_vtk(bt_tally *h, const char *filename, const double *volumes);
+bt_status bt_write_flux_csv(bt_tally *h, const char *filename, const double *volumes);
+/* repr(float(x)) as Python formats it (the writers' number format). */
+bt_status bt_format_double(double x, char *out, int32_t cap);
 
 const char *bt_last_error(void);
 const char *bt_version(void);

@@ -28,7 +28,8 @@ BT_LOCATE_GRID, BT_LOCATE_WALK = 0, 1
 
 # every symbol declared in include/b200tally.h (checked by tests/test_abi.py)
 EXPORTS = (
-    "bt_create", "bt_destroy", "bt_initialize_particle_location",
+    "bt_create", "bt_create_multi", "bt_num_shards", "bt_shard", "bt_destroy",
+    "bt_initialize_particle_location",
     "bt_move_to_next_location", "bt_finalize_batch", "bt_read_tally",
     "bt_tally_device_ptr", "bt_get_source_weight", "bt_set_source_weight",
     "bt_batches_completed", "bt_read_particles", "bt_read_digest", "bt_set_option",
@@ -67,6 +68,9 @@ _I32 = C.c_int32
 
 _SIGS = {
     "bt_create": [_P, _I64, _P, _P, _P, _I64, _P, _P, _I64, _I32, _I32, C.POINTER(_P)],
+    "bt_create_multi": [_P, _I64, _P, _P, _P, _I64, _P, _P, _I64, _I32, _P, _I32, C.POINTER(_P)],
+    "bt_num_shards": [_P, C.POINTER(_I32)],
+    "bt_shard": [_P, _I32, C.POINTER(_P), C.POINTER(_I64), C.POINTER(_I64)],
     "bt_destroy": [_P],
     "bt_initialize_particle_location": [_P, _P, _I64, _I32, _I32, C.POINTER(Summary)],
     "bt_move_to_next_location": [_P, _P, _P, _P, _P, _I64, _I32, C.POINTER(Summary)],

@@ -81,6 +81,7 @@ static bt_status set_err(bt_status s, const char* fmt, ...) {
 // handle
 
 struct HostStager;
+struct Multi;
 
 struct bt_tally {
     int dev = 0;
@@ -149,6 +150,8 @@ struct bt_tally {
     int locate_lanes = 0;                     // grid search lanes per particle (0 = default)
     std::vector<double> host_sel;             // host scratch: weights of flying particles
     HostStager* stager = nullptr;             // pageable host inputs (host_stage.cuh)
+    Multi* multi = nullptr;                   // non-null: a multi-GPU handle (multi.cuh)
+    bt_mesh* host_mesh = nullptr;             // owned host copy (bt_create_from_mesh / _file)
     // transport (allocated on first bt_transport_run)
     double* col_tally = nullptr;
     double* col_sum = nullptr;
@@ -234,6 +237,10 @@ static bt_status free_all(bt_tally* h) {
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->hcounters) cudaFreeHost(h->hcounters);
+    if (h->host_mesh) {
+        delete h->host_mesh;
+        h->host_mesh = nullptr;
+    }
     if (h->stager) {
         h->stager->release();
         delete h->stager;
@@ -446,6 +453,40 @@ static int64_t select_flying(const double* w, const int8_t* fly, int64_t n, doub
 }
 
 
+#include "multi.cuh"
+#include "mesh_io.cuh"
+
+// score_track_length / score_collision (tally.py:67-80) over n events:
+// tally[e*G + g] += w * x (kind 0) or w / x (kind 1); flags bit 1: a bin out
+// of range, bit 2: sigma_t <= 0 (checked before any score lands)
+__global__ void score_check_kernel(const int32_t* __restrict__ el, const int32_t* __restrict__ gr,
+                                   const double* __restrict__ x, int64_t n, int64_t ne,
+                                   int32_t ng, int kind, unsigned long long* flags) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (el[i] < 0 || el[i] >= ne || gr[i] < 0 || gr[i] >= ng) atomicOr(flags, 1ull);
+    if (kind == 1 && !(x[i] > 0.0)) atomicOr(flags, 2ull);
+}
+__global__ void score_kernel(const int32_t* __restrict__ el, const int32_t* __restrict__ gr,
+                             const double* __restrict__ w, const double* __restrict__ x,
+                             int64_t n, int32_t ng, int kind, double* __restrict__ tally) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double v = kind == 0 ? __dmul_rn(w[i], x[i]) : __ddiv_rn(w[i], x[i]);
+    atomicAdd(tally + (int64_t)el[i] * ng + gr[i], v);
+}
+
+// single-GPU-only entry points on a multi-GPU handle: forwarded to its one
+// shard, refused with several
+#define MULTI_SINGLE(h)                                                                    \
+    do {                                                                                   \
+        if ((h) && (h)->multi) {                                                           \
+            if ((h)->multi->shard.size() != 1)                                             \
+                return set_err(BT_EINVAL, "%s: not available on a multi-GPU handle", __func__); \
+            (h) = (h)->multi->shard[0];                                                    \
+        }                                                                                  \
+    } while (0)
+
 // ---------------------------------------------------------------------------
 // C ABI
 
@@ -597,7 +638,51 @@ bt_status bt_create(const double* vertices, int64_t num_vertices, const int32_t*
 #undef TRYF
 }
 
+bt_status bt_create_multi(const double* vertices, int64_t num_vertices, const int32_t* elements,
+                          const int32_t* adj_elem, const int8_t* adj_face, int64_t num_elements,
+                          const double* bbox, const double* centroid0, int64_t num_particles,
+                          int32_t num_groups, const int32_t* devices, int32_t num_devices,
+                          bt_tally** out) {
+    if (!out) return set_err(BT_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (!devices || num_devices <= 0) return set_err(BT_EINVAL, "need at least one device");
+    if (num_particles <= 0) return set_err(BT_EINVAL, "num_particles must be positive");
+    if (num_particles < num_devices)
+        return set_err(BT_EINVAL, "num_particles (%lld) < number of devices (%d)",
+                       (long long)num_particles, num_devices);
+    return multi_create(vertices, num_vertices, elements, adj_elem, adj_face, num_elements, bbox,
+                        centroid0, num_particles, num_groups, devices, num_devices, out);
+}
+
+bt_status bt_num_shards(bt_tally* h, int32_t* n) {
+    if (!h || !n) return set_err(BT_EINVAL, "NULL argument");
+    *n = h->multi ? (int32_t)h->multi->shard.size() : 1;
+    return BT_OK;
+}
+
+bt_status bt_shard(bt_tally* h, int32_t index, bt_tally** shard, int64_t* lo, int64_t* hi) {
+    if (!h) return set_err(BT_EINVAL, "NULL handle");
+    if (!h->multi) {
+        if (index != 0) return set_err(BT_EINVAL, "shard index out of range");
+        if (shard) *shard = h;
+        if (lo) *lo = 0;
+        if (hi) *hi = h->cap;
+        return BT_OK;
+    }
+    if (index < 0 || index >= (int32_t)h->multi->shard.size())
+        return set_err(BT_EINVAL, "shard index out of range");
+    if (shard) *shard = h->multi->shard[(size_t)index];
+    if (lo) *lo = h->multi->lo[(size_t)index];
+    if (hi) *hi = h->multi->hi[(size_t)index];
+    return BT_OK;
+}
+
 bt_status bt_destroy(bt_tally* h) {
+    if (h && h->multi) {
+        destroy_multi(h->multi);
+        delete h;
+        return BT_OK;
+    }
     if (!h) return BT_OK;
     cudaSetDevice(h->dev);
     cudaStreamSynchronize(h->stream);
@@ -608,6 +693,10 @@ bt_status bt_destroy(bt_tally* h) {
 }
 
 bt_status bt_set_option(bt_tally* h, int32_t key, int64_t value) {
+    if (h && h->multi) {
+        Multi* m = h->multi;
+        return fan_out(m, [&](int r) { return bt_set_option(m->shard[(size_t)r], key, value); });
+    }
     if (!h) return set_err(BT_EINVAL, "NULL handle");
     switch (key) {
         case BT_OPT_MAX_SWEEPS: h->max_sweeps = value; break;
@@ -930,6 +1019,7 @@ static LocateArgs locate_args(bt_tally* h, const double* target, int64_t count) 
 
 bt_status bt_initialize_particle_location(bt_tally* h, const double* positions, int64_t size,
                                           int32_t mem_kind, int32_t mode, bt_summary* summary) {
+    if (h && h->multi) return multi_initialize(h, positions, size, mem_kind, mode, summary);
     if (!h) return set_err(BT_EINVAL, "NULL handle");
     if (summary) memset(summary, 0, sizeof *summary);
     if (size < 0 || size % 3 != 0)
@@ -1042,6 +1132,8 @@ static bt_status device_source_weight(bt_tally* h, const int8_t* flying, const d
 bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, const int8_t* flying,
                                    const double* weights, const int32_t* groups, int64_t size,
                                    int32_t mem_kind, bt_summary* summary) {
+    if (h && h->multi)
+        return multi_move(h, destinations, flying, weights, groups, size, mem_kind, summary);
     if (!h) return set_err(BT_EINVAL, "NULL handle");
     if (summary) memset(summary, 0, sizeof *summary);
     const int64_t count = size;
@@ -1171,6 +1263,7 @@ bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, cons
 }
 
 bt_status bt_finalize_batch(bt_tally* h, double source_weight) {
+    if (h && h->multi) return multi_finalize(h, source_weight);
     if (!h) return set_err(BT_EINVAL, "NULL handle");
     double w = source_weight > 0.0 ? source_weight : h->source_weight;
     if (!(w > 0.0))
@@ -1198,6 +1291,7 @@ static double* tally_ptr(bt_tally* h, int32_t which) {
 }
 
 bt_status bt_read_tally(bt_tally* h, int32_t which, double* out, int64_t n) {
+    if (h && h->multi) return multi_read_tally(h, which, out, n);
     if (!h) return set_err(BT_EINVAL, "NULL handle");
     double* p = tally_ptr(h, which);
     if (!p) return set_err(BT_EINVAL, "unknown tally array %d", which);
@@ -1209,6 +1303,7 @@ bt_status bt_read_tally(bt_tally* h, int32_t which, double* out, int64_t n) {
 }
 
 bt_status bt_tally_device_ptr(bt_tally* h, int32_t which, void** ptr) {
+    MULTI_SINGLE(h);
     if (!h || !ptr) return set_err(BT_EINVAL, "NULL argument");
     double* p = tally_ptr(h, which);
     if (!p) return set_err(BT_EINVAL, "unknown tally array %d", which);
@@ -1220,18 +1315,28 @@ bt_status bt_tally_device_ptr(bt_tally* h, int32_t which, void** ptr) {
 }
 
 bt_status bt_get_source_weight(bt_tally* h, double* w) {
+    if (h && h->multi && w) {
+        *w = h->multi->source_weight;
+        return BT_OK;
+    }
     if (!h || !w) return set_err(BT_EINVAL, "NULL argument");
     *w = h->source_weight;
     return BT_OK;
 }
 
 bt_status bt_set_source_weight(bt_tally* h, double w) {
+    if (h && h->multi) {
+        h->multi->source_weight = w;
+        for (bt_tally* t : h->multi->shard) t->source_weight = w;
+        return BT_OK;
+    }
     if (!h) return set_err(BT_EINVAL, "NULL handle");
     h->source_weight = w;
     return BT_OK;
 }
 
 bt_status bt_batches_completed(bt_tally* h, int64_t* n) {
+    if (h && h->multi) h = h->multi->shard[0];
     if (!h || !n) return set_err(BT_EINVAL, "NULL argument");
     *n = h->batches;
     return BT_OK;
@@ -1240,6 +1345,9 @@ bt_status bt_batches_completed(bt_tally* h, int64_t* n) {
 bt_status bt_read_particles(bt_tally* h, int64_t count, double* position, int32_t* element,
                             int8_t* alive, int8_t* entry_face, int8_t* stuck, int8_t* outcome,
                             double* seg_total) {
+    if (h && h->multi)
+        return multi_read_particles(h, count, position, element, alive, entry_face, stuck, outcome,
+                                    seg_total);
     if (!h) return set_err(BT_EINVAL, "NULL handle");
     if (count < 0 || count > h->cap) return set_err(BT_EINVAL, "count out of range");
     TRY(ensure_device(h));
@@ -1259,6 +1367,7 @@ bt_status bt_read_particles(bt_tally* h, int64_t count, double* position, int32_
 }
 
 bt_status bt_read_digest(bt_tally* h, int64_t count, uint64_t* digest, int64_t* events) {
+    if (h && h->multi) return multi_read_digest(h, count, digest, events);
     if (!h) return set_err(BT_EINVAL, "NULL handle");
     if (!h->digest) return set_err(BT_EINVAL, "digests are off (BT_OPT_DIGEST)");
     if (count < 0 || count > h->cap) return set_err(BT_EINVAL, "count out of range");
@@ -1274,6 +1383,7 @@ bt_status bt_read_digest(bt_tally* h, int64_t count, uint64_t* digest, int64_t* 
 }
 
 bt_status bt_last_timing(bt_tally* h, float* walk_ms, float* call_ms, int64_t* kernels) {
+    if (h && h->multi) return multi_last_timing(h, walk_ms, call_ms, kernels);
     if (!h) return set_err(BT_EINVAL, "NULL handle");
     if (h->call_pending) {
         TRY(ensure_device(h));
@@ -1289,6 +1399,7 @@ bt_status bt_last_timing(bt_tally* h, float* walk_ms, float* call_ms, int64_t* k
 
 bt_status bt_particle_device_ptrs(bt_tally* h, double** position, int32_t** element,
                                   int8_t** alive) {
+    MULTI_SINGLE(h);
     if (!h) return set_err(BT_EINVAL, "NULL handle");
     // the localization of host positions completes asynchronously: a consumer
     // on another stream (e.g. torch's) must see its element / pos / alive
@@ -1301,6 +1412,10 @@ bt_status bt_particle_device_ptrs(bt_tally* h, double** position, int32_t** elem
 }
 
 bt_status bt_save_state(bt_tally* h) {
+    if (h && h->multi) {
+        Multi* m = h->multi;
+        return fan_out(m, [&](int r) { return bt_save_state(m->shard[(size_t)r]); });
+    }
     if (!h) return set_err(BT_EINVAL, "NULL handle");
     TRY(ensure_device(h));
     const int64_t n = h->cap;
@@ -1324,6 +1439,10 @@ bt_status bt_save_state(bt_tally* h) {
 }
 
 bt_status bt_restore_state(bt_tally* h) {
+    if (h && h->multi) {
+        Multi* m = h->multi;
+        return fan_out(m, [&](int r) { return bt_restore_state(m->shard[(size_t)r]); });
+    }
     if (!h) return set_err(BT_EINVAL, "NULL handle");
     if (!h->have_snapshot) return set_err(BT_EINVAL, "no snapshot saved");
     TRY(ensure_device(h));
@@ -1444,6 +1563,7 @@ bt_status bt_transport_run(bt_tally* h, const double* sigma_t, const double* sig
                            const double* group_cdf, int32_t num_groups, int64_t num_particles,
                            int64_t num_batches, uint64_t seed, const double* box,
                            const double* fixed_direction, bt_transport_totals* out) {
+    MULTI_SINGLE(h);
     if (!h || !sigma_t || !sigma_s_row_prob || !group_cdf || !box || !out)
         return set_err(BT_EINVAL, "NULL argument");
     if (num_groups != h->ngroups)
@@ -1581,6 +1701,7 @@ bt_status bt_transport_run(bt_tally* h, const double* sigma_t, const double* sig
 
 bt_status bt_read_transport_state(bt_tally* h, int64_t count, double* direction, int32_t* group,
                                   uint32_t* rng_block) {
+    MULTI_SINGLE(h);
     if (!h) return set_err(BT_EINVAL, "NULL handle");
     if (!h->tr_dir) return set_err(BT_EINVAL, "no transport run on this handle");
     if (count < 0 || count > h->cap) return set_err(BT_EINVAL, "count out of range");
@@ -1661,6 +1782,7 @@ static bt_status ensure_sweep_bufs(bt_tally* h) {
 bt_status bt_load_step(bt_tally* h, const double* destinations, const int8_t* flying,
                        const double* weights, const int32_t* groups, int64_t count,
                        int32_t mem_kind) {
+    MULTI_SINGLE(h);
     if (!h) return set_err(BT_EINVAL, "NULL handle");
     if (count < 0 || count > h->cap)
         return set_err(BT_EINVAL, "count %lld outside [0, %lld]", (long long)count,
@@ -1704,6 +1826,7 @@ __global__ void unlocalized_kernel(const int8_t* __restrict__ fly, const int32_t
 }
 
 bt_status bt_trace_begin(bt_tally* h, int32_t score, int64_t max_sweeps) {
+    MULTI_SINGLE(h);
     if (!h) return set_err(BT_EINVAL, "NULL handle");
     TRY(ensure_device(h));
     if (!h->tr_fly) return set_err(BT_EINVAL, "no step loaded (bt_load_step)");
@@ -1735,6 +1858,7 @@ bt_status bt_trace_begin(bt_tally* h, int32_t score, int64_t max_sweeps) {
 }
 
 bt_status bt_trace_propose(bt_tally* h, bt_sweep_events* ev, int64_t* flying) {
+    MULTI_SINGLE(h);
     if (!h || !ev || !flying) return set_err(BT_EINVAL, "NULL argument");
     TRY(ensure_device(h));
     const int64_t n = h->cap;
@@ -1780,6 +1904,7 @@ bt_status bt_trace_propose(bt_tally* h, bt_sweep_events* ev, int64_t* flying) {
 }
 
 bt_status bt_trace_commit(bt_tally* h) {
+    MULTI_SINGLE(h);
     if (!h) return set_err(BT_EINVAL, "NULL handle");
     TRY(ensure_device(h));
     const int64_t nev = h->tr_nev;
@@ -1801,6 +1926,7 @@ bt_status bt_trace_commit(bt_tally* h) {
 }
 
 bt_status bt_trace_end(bt_tally* h, bt_summary* out) {
+    MULTI_SINGLE(h);
     if (!h || !out) return set_err(BT_EINVAL, "NULL argument");
     TRY(ensure_device(h));
     CK(cudaMemcpyAsync(h->hcounters, h->dcounters, sizeof(unsigned long long) * NDCOUNTERS,
@@ -1827,6 +1953,7 @@ bt_status bt_memcpy(void* dst, const void* src, int64_t bytes, int32_t kind) {
 
 bt_status bt_flux(bt_tally* h, int32_t estimator, const double* volumes, double* mean,
                   double* rel_error) {
+    if (h && h->multi) h = h->multi->shard[0];  // finalized moments: the same on every GPU
     if (!h || !volumes || !mean || !rel_error) return set_err(BT_EINVAL, "NULL argument");
     const double* sm = estimator == 0 ? h->sum : h->col_sum;
     const double* sq = estimator == 0 ? h->sum_sq : h->col_sum_sq;
@@ -1863,11 +1990,357 @@ bt_status bt_flux(bt_tally* h, int32_t estimator, const double* volumes, double*
 
 bt_status bt_info(bt_tally* h, int32_t* device, int64_t* num_elements, int64_t* capacity,
                   int32_t* num_groups) {
+    if (h && h->multi) {
+        if (device) *device = h->multi->shard[0]->dev;
+        if (num_elements) *num_elements = h->ne;
+        if (capacity) *capacity = h->multi->cap;
+        if (num_groups) *num_groups = h->ngroups;
+        return BT_OK;
+    }
     if (!h) return set_err(BT_EINVAL, "NULL handle");
     if (device) *device = h->dev;
     if (num_elements) *num_elements = h->ne;
     if (capacity) *capacity = h->cap;
     if (num_groups) *num_groups = h->ngroups;
+    return BT_OK;
+}
+
+
+// ---- standalone tally grids and scoring (tally.py:21-80)
+
+bt_status bt_create_grid(int64_t num_elements, int32_t num_groups, int32_t device,
+                         bt_tally** out) {
+    if (!out) return set_err(BT_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (num_elements <= 0 || num_groups <= 0)
+        return set_err(BT_EINVAL, "grid sizes must be positive, got (%lld, %d)",
+                       (long long)num_elements, num_groups);
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev)
+        return set_err(BT_EINVAL, "device %d out of range (%d visible)", device, ndev);
+    bt_tally* h = new bt_tally();
+    h->dev = device;
+    h->ne = num_elements;
+    h->ngroups = num_groups;
+    h->cap = 0;  // no particles: moves of count > 0 are refused
+    auto fail = [&](bt_status st) {
+        const std::string keep = g_err;
+        free_all(h);
+        delete h;
+        g_err = keep;
+        return st;
+    };
+    bt_status st = ensure_device(h);
+    if (st) return fail(st);
+    const int64_t nb = num_elements * num_groups;
+    if ((st = dalloc(&h->tally, nb)) || (st = dalloc(&h->sum, nb)) || (st = dalloc(&h->sum_sq, nb)) ||
+        (st = dalloc(&h->dcounters, NDCOUNTERS)))
+        return fail(st);
+    if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMemset(h->tally, 0, sizeof(double) * nb) != cudaSuccess ||
+        cudaMemset(h->sum, 0, sizeof(double) * nb) != cudaSuccess ||
+        cudaMemset(h->sum_sq, 0, sizeof(double) * nb) != cudaSuccess)
+        return fail(set_err(BT_ECUDA, "bt_create_grid: %s", cudaGetErrorString(cudaGetLastError())));
+    *out = h;
+    return BT_OK;
+}
+
+bt_status bt_score(bt_tally* h, int32_t kind, const int32_t* elements, const int32_t* groups,
+                   const double* weights, const double* values, int64_t n, int32_t mem_kind) {
+    if (h && h->multi) h = h->multi->shard[0];  // BT_TALLY_BATCH is the sum over GPUs
+    if (!h) return set_err(BT_EINVAL, "NULL handle");
+    if (kind != 0 && kind != 1) return set_err(BT_EINVAL, "kind must be 0 (track) or 1 (collision)");
+    if (n < 0) return set_err(BT_EINVAL, "negative count");
+    if (n == 0) return BT_OK;
+    if (!elements || !groups || !weights || !values) return set_err(BT_EINVAL, "NULL array");
+    TRY(ensure_device(h));
+    if (mem_kind == BT_MEM_HOST) {  // _check_bin, score_collision's sigma_t check
+        for (int64_t i = 0; i < n; ++i) {
+            if (kind == 1 && !(values[i] > 0.0)) {
+                char r[48];
+                r[py_repr(values[i], r)] = 0;
+                return set_err(BT_EINVAL, "sigma_t must be positive, got %s", r);
+            }
+            if (elements[i] < 0 || elements[i] >= h->ne)
+                return set_err(BT_EINDEX, "element %d out of range [0, %lld)", elements[i],
+                               (long long)h->ne);
+            if (groups[i] < 0 || groups[i] >= h->ngroups)
+                return set_err(BT_EINDEX, "group %d out of range [0, %d)", groups[i], h->ngroups);
+        }
+    }
+    int32_t *de = nullptr, *dg = nullptr;
+    double *dw = nullptr, *dx = nullptr;
+    const int32_t* pe = elements;
+    const int32_t* pg = groups;
+    const double* pw = weights;
+    const double* px = values;
+    if (mem_kind == BT_MEM_HOST) {
+        TRY(dalloc(&de, n));
+        TRY(dalloc(&dg, n));
+        TRY(dalloc(&dw, n));
+        TRY(dalloc(&dx, n));
+        CK(cudaMemcpyAsync(de, elements, sizeof(int32_t) * n, cudaMemcpyHostToDevice, h->stream));
+        CK(cudaMemcpyAsync(dg, groups, sizeof(int32_t) * n, cudaMemcpyHostToDevice, h->stream));
+        CK(cudaMemcpyAsync(dw, weights, sizeof(double) * n, cudaMemcpyHostToDevice, h->stream));
+        CK(cudaMemcpyAsync(dx, values, sizeof(double) * n, cudaMemcpyHostToDevice, h->stream));
+        pe = de; pg = dg; pw = dw; px = dx;
+    } else {
+        CK(cudaMemsetAsync(h->dcounters + 15, 0, sizeof(unsigned long long), h->stream));
+        score_check_kernel<<<grid_for(n, 256), 256, 0, h->stream>>>(pe, pg, px, n, h->ne,
+                                                                    h->ngroups, kind,
+                                                                    h->dcounters + 15);
+        unsigned long long f = 0;
+        CK(cudaMemcpyAsync(&f, h->dcounters + 15, sizeof f, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        if (f & 2ull) return set_err(BT_EINVAL, "sigma_t must be positive");
+        if (f & 1ull) return set_err(BT_EINDEX, "element or group out of range");
+    }
+    score_kernel<<<grid_for(n, 256), 256, 0, h->stream>>>(pe, pg, pw, px, n, h->ngroups, kind,
+                                                          h->tally);
+    cudaError_t err = cudaGetLastError();
+    if (err == cudaSuccess) err = cudaStreamSynchronize(h->stream);
+    if (de) { cudaFree(de); cudaFree(dg); cudaFree(dw); cudaFree(dx); }
+    if (err != cudaSuccess) return set_err(BT_ECUDA, "bt_score: %s", cudaGetErrorString(err));
+    return BT_OK;
+}
+
+bt_status bt_write_tally(bt_tally* h, int32_t which, const double* in, int64_t n) {
+    if (h && h->multi) {  // the unfinalized batch lives on shard 0 + the others: write it to
+        Multi* m = h->multi;  // shard 0 and clear the rest; the moments are mirrored
+        if (n != h->ne * h->ngroups) return set_err(BT_EINVAL, "n must be E*G");
+        return fan_out(m, [&](int r) -> bt_status {
+            bt_tally* t = m->shard[(size_t)r];
+            if (which == BT_TALLY_BATCH && r > 0) {
+                TRY(ensure_device(t));
+                CK(cudaMemset(t->tally, 0, sizeof(double) * n));
+                return BT_OK;
+            }
+            return bt_write_tally(t, which, in, n);
+        });
+    }
+    if (!h || !in) return set_err(BT_EINVAL, "NULL argument");
+    double* p = tally_ptr(h, which);
+    if (!p) return set_err(BT_EINVAL, "unknown tally array %d", which);
+    if (n != h->ne * h->ngroups) return set_err(BT_EINVAL, "n must be E*G");
+    TRY(ensure_device(h));
+    CK(cudaMemcpyAsync(p, in, sizeof(double) * n, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return BT_OK;
+}
+
+bt_status bt_set_batches_completed(bt_tally* h, int64_t n) {
+    if (h && h->multi) {
+        for (bt_tally* t : h->multi->shard) t->batches = n;
+        return BT_OK;
+    }
+    if (!h || n < 0) return set_err(BT_EINVAL, "bad argument");
+    h->batches = n;
+    return BT_OK;
+}
+
+// ---- native mesh ingest (mesh.py:109-148, 302-331) and the paper-level ABI
+
+bt_status bt_mesh_from_arrays(const double* vertices, int64_t num_vertices,
+                              const int32_t* elements, int64_t num_elements, int32_t device,
+                              bt_mesh** out) {
+    if (!out) return set_err(BT_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (num_vertices < 0 || num_elements < 0) return set_err(BT_EINVAL, "negative size");
+    if ((num_vertices && !vertices) || (num_elements && !elements))
+        return set_err(BT_EINVAL, "NULL array");
+    bt_mesh* m = new bt_mesh();
+    m->nv = num_vertices;
+    m->ne = num_elements;
+    m->v.assign(vertices, vertices + 3 * num_vertices);
+    m->e.assign(elements, elements + 4 * num_elements);
+    const bt_status st = mesh_finish(m, device);
+    if (st != BT_OK) {
+        delete m;
+        return st;
+    }
+    *out = m;
+    return BT_OK;
+}
+
+bt_status bt_mesh_read(const char* path, int32_t device, bt_mesh** out) {
+    if (!out || !path) return set_err(BT_EINVAL, "NULL argument");
+    *out = nullptr;
+    FILE* f = fopen(path, "rb");
+    if (!f) return set_err(BT_EINVAL, "%s: cannot open", path);
+    std::string data;
+    fseek(f, 0, SEEK_END);
+    const long sz = ftell(f);
+    fseek(f, 0, SEEK_SET);
+    data.resize(sz > 0 ? (size_t)sz : 0);
+    const size_t got = sz > 0 ? fread(&data[0], 1, (size_t)sz, f) : 0;
+    fclose(f);
+    if ((long)got != sz) return set_err(BT_EINVAL, "%s: short read", path);
+    bt_mesh* m = new bt_mesh();
+    bt_status st = mesh_parse(path, data.data(), data.size(), m);
+    if (st == BT_OK) st = mesh_finish(m, device);
+    if (st != BT_OK) {
+        delete m;
+        return st;
+    }
+    *out = m;
+    return BT_OK;
+}
+
+bt_status bt_mesh_info(const bt_mesh* m, int64_t* num_vertices, int64_t* num_elements) {
+    if (!m) return set_err(BT_EINVAL, "NULL mesh");
+    if (num_vertices) *num_vertices = m->nv;
+    if (num_elements) *num_elements = m->ne;
+    return BT_OK;
+}
+
+bt_status bt_mesh_arrays(const bt_mesh* m, double* vertices, int32_t* elements, int32_t* adj_elem,
+                         int8_t* adj_face, double* volumes, double* centroids, double* bbox) {
+    if (!m) return set_err(BT_EINVAL, "NULL mesh");
+    auto cp = [](void* dst, const void* src, size_t bytes) {
+        if (dst && bytes) memcpy(dst, src, bytes);
+    };
+    cp(vertices, m->v.data(), sizeof(double) * m->v.size());
+    cp(elements, m->e.data(), sizeof(int32_t) * m->e.size());
+    cp(adj_elem, m->ae.data(), sizeof(int32_t) * m->ae.size());
+    cp(adj_face, m->af.data(), m->af.size());
+    cp(volumes, m->vol.data(), sizeof(double) * m->vol.size());
+    cp(centroids, m->cen.data(), sizeof(double) * m->cen.size());
+    cp(bbox, m->bbox, sizeof m->bbox);
+    return BT_OK;
+}
+
+bt_status bt_mesh_destroy(bt_mesh* m) {
+    delete m;
+    return BT_OK;
+}
+
+bt_status bt_create_from_mesh(const bt_mesh* m, int64_t num_particles, int32_t num_groups,
+                              int32_t device, bt_tally** out) {
+    if (!m || !out) return set_err(BT_EINVAL, "NULL argument");
+    if (m->ne == 0) return set_err(BT_EINVAL, "grid sizes must be positive");
+    TRY(bt_create(m->v.data(), m->nv, m->e.data(), m->ae.data(), m->af.data(), m->ne, m->bbox,
+                  m->cen.data(), num_particles, num_groups, device, out));
+    (*out)->host_mesh = new bt_mesh(*m);
+    return BT_OK;
+}
+
+bt_status bt_create_from_file(const char* mesh_filename, int64_t num_particles,
+                              int32_t num_groups, int32_t device, bt_tally** out) {
+    if (!out) return set_err(BT_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (num_particles <= 0) return set_err(BT_EINVAL, "num_particles must be positive");
+    bt_mesh* m = nullptr;
+    TRY(bt_mesh_read(mesh_filename, device, &m));
+    const bt_status st = bt_create_from_mesh(m, num_particles, num_groups, device, out);
+    bt_mesh_destroy(m);
+    return st;
+}
+
+// the handle's mesh on the host: its own copy, or read back from the device
+static bt_status handle_mesh(bt_tally* h, std::vector<double>& v, std::vector<int32_t>& e) {
+    if (h->host_mesh) {
+        v = h->host_mesh->v;
+        e = h->host_mesh->e;
+        return BT_OK;
+    }
+    bt_tally* s = h->multi ? h->multi->shard[0] : h;
+    if (!s->vtx || !s->rec) return set_err(BT_EINVAL, "this handle has no mesh");
+    TRY(ensure_device(s));
+    std::vector<Vtx> hv((size_t)s->nv);
+    std::vector<ElemRec> hr((size_t)s->ne);
+    CK(cudaMemcpy(hv.data(), s->vtx, sizeof(Vtx) * hv.size(), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hr.data(), s->rec, sizeof(ElemRec) * hr.size(), cudaMemcpyDeviceToHost));
+    v.resize((size_t)(3 * s->nv));
+    e.resize((size_t)(4 * s->ne));
+    for (int64_t i = 0; i < s->nv; ++i) {
+        v[(size_t)(3 * i)] = hv[(size_t)i].x;
+        v[(size_t)(3 * i + 1)] = hv[(size_t)i].y;
+        v[(size_t)(3 * i + 2)] = hv[(size_t)i].z;
+    }
+    for (int64_t i = 0; i < s->ne; ++i)
+        for (int k = 0; k < 4; ++k) e[(size_t)(4 * i + k)] = hr[(size_t)i].v[k];
+    return BT_OK;
+}
+
+static bt_status handle_flux(bt_tally* h, const double* volumes, std::vector<double>& mean,
+                             std::vector<double>& rel) {
+    const double* vol = volumes ? volumes : (h->host_mesh ? h->host_mesh->vol.data() : nullptr);
+    if (!vol) return set_err(BT_EINVAL, "volumes are required for a handle made from arrays");
+    const int64_t nb = h->ne * h->ngroups;
+    mean.resize((size_t)nb);
+    rel.resize((size_t)nb);
+    return bt_flux(h, 0, vol, mean.data(), rel.data());
+}
+
+bt_status bt_write_vtk(bt_tally* h, const char* filename, const double* volumes) {
+    if (!h || !filename) return set_err(BT_EINVAL, "NULL argument");
+    std::vector<double> mean, rel, v;
+    std::vector<int32_t> e;
+    TRY(handle_flux(h, volumes, mean, rel));
+    TRY(handle_mesh(h, v, e));
+    const int64_t nv = (int64_t)v.size() / 3, ne = (int64_t)e.size() / 4, G = h->ngroups;
+    std::string s;
+    s.reserve((size_t)(nv * 70 + ne * 60 + 2 * G * ne * 24 + 256));
+    s += "# vtk DataFile Version 3.0\ntetrahedral mesh flux tally\nASCII\nDATASET UNSTRUCTURED_GRID\n";
+    s += "POINTS " + std::to_string(nv) + " double\n";
+    {
+        char b[160];
+        for (int64_t i = 0; i < nv; ++i) {
+            int k = py_repr(v[(size_t)(3 * i)], b);
+            b[k++] = ' ';
+            k += py_repr(v[(size_t)(3 * i + 1)], b + k);
+            b[k++] = ' ';
+            k += py_repr(v[(size_t)(3 * i + 2)], b + k);
+            b[k++] = '\n';
+            s.append(b, (size_t)k);
+        }
+    }
+    s += "CELLS " + std::to_string(ne) + " " + std::to_string(5 * ne) + "\n";
+    {
+        char b[80];
+        for (int64_t i = 0; i < ne; ++i) {
+            const int k = snprintf(b, sizeof b, "4 %d %d %d %d\n", e[(size_t)(4 * i)],
+                                   e[(size_t)(4 * i + 1)], e[(size_t)(4 * i + 2)],
+                                   e[(size_t)(4 * i + 3)]);
+            s.append(b, (size_t)k);
+        }
+    }
+    s += "CELL_TYPES " + std::to_string(ne) + "\n";
+    for (int64_t i = 0; i < ne; ++i) s += "10\n";
+    s += "CELL_DATA " + std::to_string(ne) + "\n";
+    for (int64_t g = 0; g < G; ++g) {
+        s += "SCALARS flux_g" + std::to_string(g) + " double 1\nLOOKUP_TABLE default\n";
+        append_reprs(s, mean.data(), ne, G, g);
+        s += "SCALARS rel_error_g" + std::to_string(g) + " double 1\nLOOKUP_TABLE default\n";
+        append_reprs(s, rel.data(), ne, G, g);
+    }
+    return write_text(filename, s);
+}
+
+bt_status bt_write_flux_csv(bt_tally* h, const char* filename, const double* volumes) {
+    if (!h || !filename) return set_err(BT_EINVAL, "NULL argument");
+    std::vector<double> mean, rel;
+    TRY(handle_flux(h, volumes, mean, rel));
+    const int64_t ne = h->ne, G = h->ngroups;
+    std::string s = "element,group,mean,rel_error\n";
+    char b[128];
+    for (int64_t e = 0; e < ne; ++e)
+        for (int64_t g = 0; g < G; ++g) {
+            int k = snprintf(b, sizeof b, "%lld,%lld,", (long long)e, (long long)g);
+            k += py_repr(mean[(size_t)(e * G + g)], b + k);
+            b[k++] = ',';
+            k += py_repr(rel[(size_t)(e * G + g)], b + k);
+            b[k++] = '\n';
+            s.append(b, (size_t)k);
+        }
+    return write_text(filename, s);
+}
+
+bt_status bt_format_double(double x, char* out, int32_t cap) {
+    if (!out || cap < 32) return set_err(BT_EINVAL, "need a 32-byte buffer");
+    const int k = py_repr(x, out);
+    out[k] = 0;
     return BT_OK;
 }
 

@@ -218,7 +218,7 @@ class MeshTally:
     """Batched track-length tally on a tet mesh, computed on one B200."""
 
     def __init__(self, mesh, num_particles: int, num_groups: int = 1, threads: int = 1, *,
-                 device: int = 0, localize: str = "grid", digest: bool = False,
+                 device: int = 0, devices=None, localize: str = "grid", digest: bool = False,
                  sort: bool = False, warp_aggregate: bool | None = None, staged: bool | int = True,
                  move_chunks: int = 0):
         if isinstance(mesh, (str, Path)):
@@ -237,7 +237,13 @@ class MeshTally:
         self.threads = max(1, int(threads))  # accepted for API compatibility
         self.num_groups = int(num_groups)
         self.capacity = int(num_particles)
-        self.device = int(device)
+        # devices=[d0, d1, ...]: one handle over several GPUs of this process
+        # (bt_create_multi: contiguous particle shards, replicated mesh, one
+        # NCCL all-reduce of the tallies per batch)
+        self.devices = None if devices is None else [int(d) for d in devices]
+        if self.devices is not None and not self.devices:
+            raise ValueError("devices must name at least one GPU")
+        self.device = self.devices[0] if self.devices else int(device)
         self.localize = localize
         self._count = 0
         L = _lib.load()
@@ -248,9 +254,16 @@ class MeshTally:
         bbox = np.ascontiguousarray(mesh.bounding_box, dtype=np.float64)
         c0 = np.ascontiguousarray(mesh.centroids[0], dtype=np.float64)
         h = C.c_void_p()
-        _lib.check(L.bt_create(v.ctypes.data, v.shape[0], e.ctypes.data, ae.ctypes.data,
-                               af.ctypes.data, e.shape[0], bbox.ctypes.data, c0.ctypes.data,
-                               self.capacity, self.num_groups, self.device, C.byref(h)))
+        if self.devices is None:
+            _lib.check(L.bt_create(v.ctypes.data, v.shape[0], e.ctypes.data, ae.ctypes.data,
+                                   af.ctypes.data, e.shape[0], bbox.ctypes.data, c0.ctypes.data,
+                                   self.capacity, self.num_groups, self.device, C.byref(h)))
+        else:
+            dv = np.ascontiguousarray(self.devices, dtype=np.int32)
+            _lib.check(L.bt_create_multi(v.ctypes.data, v.shape[0], e.ctypes.data,
+                                         ae.ctypes.data, af.ctypes.data, e.shape[0],
+                                         bbox.ctypes.data, c0.ctypes.data, self.capacity,
+                                         self.num_groups, dv.ctypes.data, dv.size, C.byref(h)))
         self._h = h
         self._L = L
         _LIVE.add(self)
@@ -290,6 +303,18 @@ class MeshTally:
     @source_weight.setter
     def source_weight(self, w: float) -> None:
         _lib.check(self._L.bt_set_source_weight(self._h, float(w)))
+
+    @property
+    def num_shards(self) -> int:
+        n = C.c_int32()
+        _lib.check(self._L.bt_num_shards(self._h, C.byref(n)))
+        return int(n.value)
+
+    def shard_bounds(self, index: int) -> tuple[int, int]:
+        """Particle range [lo, hi) of GPU shard `index`."""
+        lo, hi = C.c_int64(), C.c_int64()
+        _lib.check(self._L.bt_shard(self._h, int(index), None, C.byref(lo), C.byref(hi)))
+        return int(lo.value), int(hi.value)
 
     def set_option(self, key: int, value: int) -> None:
         _lib.check(self._L.bt_set_option(self._h, int(key), int(value)))
