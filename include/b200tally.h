@@ -342,6 +342,8 @@ bt_status bt_create_from_file(const char *mesh_filename, int64_t num_particles,
  * mesh object/file.  bt_write_flux_csv: write_flux_csv (tally.py:192-200). */
 bt_status bt_write_vtk(bt_tally *h, const char *filename, const double *volumes);
 bt_status bt_write_flux_csv(bt_tally *h, const char *filename, const double *volumes);
+/* Number of visible CUDA devices (0 without a GPU or driver). */
+bt_status bt_device_count(int32_t *n);
 /* repr(float(x)) as Python formats it (the writers' number format). */
 bt_status bt_format_double(double x, char *out, int32_t cap);
 

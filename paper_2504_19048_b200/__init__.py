@@ -31,16 +31,22 @@ from .tally import (
     TallyGrid,
     TraceSummary,
     batch_totals,
+    create_grid,
     finalize_batch,
     flux,
+    score_collision,
+    score_track_length,
     write_flux_csv,
     write_vtk,
 )
+from .transport import CrossSections, RunConfig, RunResult, run
 
 __all__ = [
     "FACE_VERTICES", "MalformedMeshError", "TetMesh", "build_adjacency", "build_cube_mesh",
     "build_torus_shell_mesh", "element_volume", "read_tetmesh", "validate", "write_tetmesh",
     "OUTCOME_LEAKED", "OUTCOME_NONE", "OUTCOME_REACHED", "OUTCOME_STUCK_KILLED",
     "FluxResult", "MeshTally", "ParticleState", "TallyGrid", "TraceSummary", "batch_totals",
-    "finalize_batch", "flux", "write_flux_csv", "write_vtk",
+    "create_grid", "finalize_batch", "flux", "score_collision", "score_track_length",
+    "write_flux_csv", "write_vtk",
+    "CrossSections", "RunConfig", "RunResult", "run",
 ]

@@ -37,6 +37,10 @@ EXPORTS = (
     "bt_info", "bt_build_adjacency", "bt_transport_run", "bt_read_transport_state",
     "bt_uniform_blocks", "bt_load_step", "bt_trace_begin", "bt_trace_propose",
     "bt_trace_commit", "bt_trace_end", "bt_memcpy", "bt_flux",
+    "bt_create_grid", "bt_score", "bt_write_tally", "bt_set_batches_completed",
+    "bt_mesh_read", "bt_mesh_from_arrays", "bt_mesh_info", "bt_mesh_arrays", "bt_mesh_destroy",
+    "bt_create_from_mesh", "bt_create_from_file", "bt_write_vtk", "bt_write_flux_csv",
+    "bt_device_count", "bt_format_double",
     "bt_last_error", "bt_version",
 )
 
@@ -100,6 +104,21 @@ _SIGS = {
     "bt_trace_end": [_P, C.POINTER(Summary)],
     "bt_memcpy": [_P, _P, _I64, _I32],
     "bt_flux": [_P, _I32, _P, _P, _P],
+    "bt_create_grid": [_I64, _I32, _I32, C.POINTER(_P)],
+    "bt_score": [_P, _I32, _P, _P, _P, _P, _I64, _I32],
+    "bt_write_tally": [_P, _I32, _P, _I64],
+    "bt_set_batches_completed": [_P, _I64],
+    "bt_mesh_read": [C.c_char_p, _I32, C.POINTER(_P)],
+    "bt_mesh_from_arrays": [_P, _I64, _P, _I64, _I32, C.POINTER(_P)],
+    "bt_mesh_info": [_P, C.POINTER(_I64), C.POINTER(_I64)],
+    "bt_mesh_arrays": [_P, _P, _P, _P, _P, _P, _P, _P],
+    "bt_mesh_destroy": [_P],
+    "bt_create_from_mesh": [_P, _I64, _I32, _I32, C.POINTER(_P)],
+    "bt_create_from_file": [C.c_char_p, _I64, _I32, _I32, C.POINTER(_P)],
+    "bt_write_vtk": [_P, C.c_char_p, _P],
+    "bt_write_flux_csv": [_P, C.c_char_p, _P],
+    "bt_device_count": [C.POINTER(_I32)],
+    "bt_format_double": [C.c_double, C.c_char_p, _I32],
     "bt_last_error": [],
     "bt_version": [],
 }
@@ -130,6 +149,13 @@ def load(build_if_missing: bool = True):
         f.restype = C.c_char_p if name in ("bt_last_error", "bt_version") else C.c_int
     _lib = L
     return L
+
+
+def device_count() -> int:
+    """Visible CUDA devices (0 on a host without a GPU)."""
+    n = C.c_int32()
+    check(load().bt_device_count(C.byref(n)))
+    return int(n.value)
 
 
 def check(status: int) -> None:

@@ -2337,6 +2337,17 @@ bt_status bt_write_flux_csv(bt_tally* h, const char* filename, const double* vol
     return write_text(filename, s);
 }
 
+bt_status bt_device_count(int32_t* n) {
+    if (!n) return set_err(BT_EINVAL, "NULL argument");
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+        cudaGetLastError();
+        c = 0;
+    }
+    *n = c;
+    return BT_OK;
+}
+
 bt_status bt_format_double(double x, char* out, int32_t cap) {
     if (!out || cap < 32) return set_err(BT_EINVAL, "need a 32-byte buffer");
     const int k = py_repr(x, out);

@@ -99,54 +99,88 @@ static int py_repr(double x, char* out) {
     return (int)(p - out);
 }
 
-// ---- host face adjacency (build_adjacency, mesh.py:188-235) for device < 0
+// ---- host face adjacency (build_adjacency, mesh.py:188-235) for device < 0:
+// faces bucketed by their smallest vertex id (counting sort), each bucket
+// (~F/V = 24 faces on a cube mesh) sorted by the other two ids on all host
+// threads; equal neighbours pair up.  Errors report the first offending face
+// in lexicographic order, as a full sort would.
 static bt_status host_adjacency(const int32_t* el, int64_t ne, int64_t nv, int32_t* ae,
                                 int8_t* af) {
     static const int FV[4][3] = {{1, 2, 3}, {0, 2, 3}, {0, 1, 3}, {0, 1, 2}};
-    struct K {
-        int64_t a, b, c;
-        int64_t row;
-    };
-    std::vector<K> k((size_t)(4 * ne));
+    const int64_t F = 4 * ne;
+    std::vector<int32_t> fa((size_t)F), fb((size_t)F), fc((size_t)F);
     par_for(ne, [&](int64_t lo, int64_t hi) {
         for (int64_t e = lo; e < hi; ++e)
             for (int f = 0; f < 4; ++f) {
-                int64_t t[3] = {el[4 * e + FV[f][0]], el[4 * e + FV[f][1]], el[4 * e + FV[f][2]]};
-                std::sort(t, t + 3);
-                k[(size_t)(4 * e + f)] = K{t[0], t[1], t[2], 4 * e + f};
+                int32_t t[3] = {el[4 * e + FV[f][0]], el[4 * e + FV[f][1]], el[4 * e + FV[f][2]]};
+                if (t[0] > t[1]) std::swap(t[0], t[1]);
+                if (t[1] > t[2]) std::swap(t[1], t[2]);
+                if (t[0] > t[1]) std::swap(t[0], t[1]);
+                fa[(size_t)(4 * e + f)] = t[0];
+                fb[(size_t)(4 * e + f)] = t[1];
+                fc[(size_t)(4 * e + f)] = t[2];
             }
     });
-    std::stable_sort(k.begin(), k.end(), [](const K& x, const K& y) {
-        return x.a != y.a ? x.a < y.a : (x.b != y.b ? x.b < y.b : x.c < y.c);
+    std::vector<int64_t> start((size_t)nv + 1, 0);
+    for (int64_t r = 0; r < F; ++r) ++start[(size_t)fa[(size_t)r] + 1];
+    for (int64_t v = 0; v < nv; ++v) start[(size_t)v + 1] += start[(size_t)v];
+    std::vector<int64_t> fill(start.begin(), start.end() - 1);
+    std::vector<int64_t> rows((size_t)F);
+    for (int64_t r = 0; r < F; ++r) rows[(size_t)fill[(size_t)fa[(size_t)r]]++] = r;  // ascending rows
+    std::fill(ae, ae + F, -1);
+    std::fill(af, af + F, (int8_t)-1);
+    // first error per kind: (bucket, message)
+    std::mutex mu;
+    int64_t err_at = INT64_MAX;
+    std::string err_msg;
+    par_for(nv, [&](int64_t lo, int64_t hi) {
+        std::vector<int64_t> b;
+        for (int64_t v = lo; v < hi; ++v) {
+            const int64_t s0 = start[(size_t)v], s1 = start[(size_t)v + 1];
+            if (s1 - s0 < 2) continue;
+            b.assign(rows.begin() + s0, rows.begin() + s1);
+            std::stable_sort(b.begin(), b.end(), [&](int64_t x, int64_t y) {
+                return fb[(size_t)x] != fb[(size_t)y] ? fb[(size_t)x] < fb[(size_t)y]
+                                                      : fc[(size_t)x] < fc[(size_t)y];
+            });
+            auto same = [&](size_t i, size_t j) {
+                return fb[(size_t)b[i]] == fb[(size_t)b[j]] && fc[(size_t)b[i]] == fc[(size_t)b[j]];
+            };
+            for (size_t i = 0; i + 1 < b.size(); ++i) {
+                if (!same(i, i + 1)) continue;
+                char msg[200] = {0};
+                const int64_t r1 = b[i], r2 = b[i + 1];
+                if (i + 2 < b.size() && same(i + 1, i + 2))
+                    snprintf(msg, sizeof msg,
+                             "face with vertices (%d, %d, %d) is shared by more than two "
+                             "elements (duplicate or non-manifold mesh)",
+                             fa[(size_t)r1], fb[(size_t)r1], fc[(size_t)r1]);
+                else if (r1 / 4 == r2 / 4)
+                    snprintf(msg, sizeof msg,
+                             "element %lld lists the same face twice (repeated vertex id)",
+                             (long long)(r1 / 4));
+                if (msg[0]) {
+                    std::lock_guard<std::mutex> g(mu);
+                    if (v < err_at) {
+                        err_at = v;
+                        err_msg = msg;
+                    }
+                    break;
+                }
+                ae[r1] = (int32_t)(r2 / 4);
+                af[r1] = (int8_t)(r2 % 4);
+                ae[r2] = (int32_t)(r1 / 4);
+                af[r2] = (int8_t)(r1 % 4);
+                ++i;
+            }
+        }
     });
-    std::fill(ae, ae + 4 * ne, -1);
-    std::fill(af, af + 4 * ne, (int8_t)-1);
-    auto same = [&](size_t i, size_t j) {
-        return k[i].a == k[j].a && k[i].b == k[j].b && k[i].c == k[j].c;
-    };
-    for (size_t i = 0; i + 1 < k.size(); ++i) {
-        if (!same(i, i + 1)) continue;
-        if (i + 2 < k.size() && same(i + 1, i + 2))
-            return set_err(BT_EINVAL,
-                           "face with vertices (%lld, %lld, %lld) is shared by more than two "
-                           "elements (duplicate or non-manifold mesh)",
-                           (long long)k[i].a, (long long)k[i].b, (long long)k[i].c);
-        const int64_t r1 = k[i].row, r2 = k[i + 1].row;
-        if (r1 / 4 == r2 / 4)
-            return set_err(BT_EINVAL, "element %lld lists the same face twice (repeated vertex id)",
-                           (long long)(r1 / 4));
-        ae[r1] = (int32_t)(r2 / 4);
-        af[r1] = (int8_t)(r2 % 4);
-        ae[r2] = (int32_t)(r1 / 4);
-        af[r2] = (int8_t)(r1 % 4);
-        ++i;
-    }
+    if (err_at != INT64_MAX) return set_err(BT_EINVAL, "%s", err_msg.c_str());
     for (int64_t e = 0; e < ne; ++e) {  // duplicated element
         const int32_t* r = ae + 4 * e;
         if (r[0] >= 0 && r[0] == r[1] && r[0] == r[2] && r[0] == r[3])
             return set_err(BT_EINVAL, "element %lld duplicates element %d", (long long)e, r[0]);
     }
-    (void)nv;
     return BT_OK;
 }
 
@@ -159,8 +193,10 @@ static bt_status mesh_finish(bt_mesh* m, int32_t device) {
         if (E[i] < 0 || E[i] >= nv) return set_err(BT_EINVAL, "element vertex id out of range");
     m->vol.assign((size_t)ne, 0.0);
     m->cen.assign((size_t)(3 * ne), 0.0);
-    // signed_volumes6: a = v1 - v0, b = v2 - v0, c = v3 - v0;
-    // np.einsum("ij,ij->i", np.cross(a, b), c) = (x0*c0 + x1*c1) + x2*c2
+    // signed_volumes6: a = v1 - v0, b = v2 - v0, c = v3 - v0; np.cross(a, b)
+    // as numpy forms it; np.einsum("ij,ij->i", x, c) sums its three products
+    // as (x0*c0 + x2*c2) + x1*c1 (two-lane accumulation; checked against
+    // numpy on permuted torus meshes, tests/test_mesh_native.py)
     par_for(ne, [&](int64_t lo, int64_t hi) {
         for (int64_t e = lo; e < hi; ++e) {
             const double* p0 = V + 3 * (int64_t)E[4 * e];
@@ -176,8 +212,8 @@ static bt_status mesh_finish(bt_mesh* m, int32_t device) {
             const double x0 = a[1] * b[2] - a[2] * b[1];
             const double x1 = a[2] * b[0] - a[0] * b[2];
             const double x2 = a[0] * b[1] - a[1] * b[0];
-            double v6 = x0 * c[0] + x1 * c[1];
-            v6 = v6 + x2 * c[2];
+            double v6 = x0 * c[0] + x2 * c[2];
+            v6 = v6 + x1 * c[1];
             if (v6 < 0.0) {
                 std::swap(E[4 * e + 2], E[4 * e + 3]);
                 v6 = -v6;

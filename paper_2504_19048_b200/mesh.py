@@ -89,9 +89,19 @@ class TetMesh:
         return np.stack([self.adj_elem, self.adj_face.astype(np.int32)], axis=2)
 
     @classmethod
-    def from_arrays(cls, vertices, elements, device: int | None = None) -> "TetMesh":
-        """Orientation fix, degeneracy check, adjacency (on `device` when
-        given: bt_build_adjacency, else host numpy)."""
+    def from_arrays(cls, vertices, elements, device: int | str | None = "auto") -> "TetMesh":
+        """Orientation fix, degeneracy check, adjacency.
+
+        ``device="auto"`` (default): the library's native ingest
+        (bt_mesh_from_arrays: all host threads, adjacency on GPU 0 when one is
+        visible, else a host sort); an int: the same on that GPU; ``None``:
+        the host numpy path.  All three give bit-identical arrays."""
+        if device is not None:
+            return _native_from_arrays(vertices, elements, device)
+        return cls._from_arrays_numpy(vertices, elements)
+
+    @classmethod
+    def _from_arrays_numpy(cls, vertices, elements) -> "TetMesh":
         vertices = np.ascontiguousarray(vertices, dtype=np.float64)
         elements = np.array(elements, dtype=np.int32, copy=True, order="C")
         if vertices.ndim != 2 or vertices.shape[1] != 3:
@@ -117,7 +127,7 @@ class TetMesh:
             raise MalformedMeshError(
                 f"element {bad} is degenerate (volume {vol6[bad] / 6.0:g})")
 
-        adj_elem, adj_face = build_adjacency(elements, nv, device=device)
+        adj_elem, adj_face = build_adjacency(elements, nv)
         centroids = vertices[elements].mean(axis=1)
         if vertices.size:
             bbox = np.stack([vertices.min(axis=0), vertices.max(axis=0)])
@@ -129,6 +139,59 @@ class TetMesh:
                    np.ascontiguousarray(bbox))
 
 
+def _native_device(device) -> int:
+    from . import _lib
+    if device == "auto":
+        return 0 if _lib.device_count() > 0 else -1
+    return int(device)
+
+
+def _native_mesh(h, L) -> TetMesh:
+    """Copy a bt_mesh's arrays into a TetMesh and release it."""
+    import ctypes as C
+    from . import _lib
+    try:
+        nv, ne = C.c_int64(), C.c_int64()
+        _lib.check(L.bt_mesh_info(h, C.byref(nv), C.byref(ne)))
+        nv, ne = int(nv.value), int(ne.value)
+        v = np.empty((nv, 3))
+        e = np.empty((ne, 4), np.int32)
+        ae = np.empty((ne, 4), np.int32)
+        af = np.empty((ne, 4), np.int8)
+        vol = np.empty(ne)
+        cen = np.empty((ne, 3))
+        bbox = np.empty((2, 3))
+        _lib.check(L.bt_mesh_arrays(h, v.ctypes.data, e.ctypes.data, ae.ctypes.data,
+                                    af.ctypes.data, vol.ctypes.data, cen.ctypes.data,
+                                    bbox.ctypes.data))
+    finally:
+        L.bt_mesh_destroy(h)
+    return TetMesh(v, e, ae, af, vol, cen, bbox)
+
+
+def _native_call(fn, *args) -> TetMesh:
+    import ctypes as C
+    from . import _lib
+    L = _lib.load()
+    h = C.c_void_p()
+    st = getattr(L, fn)(*args, C.byref(h))
+    if st == _lib.BT_EINVAL:
+        raise MalformedMeshError(L.bt_last_error().decode())
+    _lib.check(st)
+    return _native_mesh(h, L)
+
+
+def _native_from_arrays(vertices, elements, device) -> TetMesh:
+    vertices = np.ascontiguousarray(vertices, dtype=np.float64)
+    elements = np.ascontiguousarray(elements, dtype=np.int32)
+    if vertices.ndim != 2 or vertices.shape[1] != 3:
+        raise MalformedMeshError("vertices must be (V, 3)")
+    if elements.ndim != 2 or elements.shape[1] != 4:
+        raise MalformedMeshError("elements must be (E, 4)")
+    return _native_call("bt_mesh_from_arrays", vertices.ctypes.data, vertices.shape[0],
+                        elements.ctypes.data, elements.shape[0], _native_device(device))
+
+
 def signed_volumes6(vertices: np.ndarray, elements: np.ndarray) -> np.ndarray:
     """6x signed volume: (v1-v0) x (v2-v0) . (v3-v0)."""
     p = vertices[elements]                      # (E, 4, 3)
@@ -138,7 +201,7 @@ def signed_volumes6(vertices: np.ndarray, elements: np.ndarray) -> np.ndarray:
     return np.einsum("ij,ij->i", np.cross(a, b), c)
 
 
-def build_cube_mesh(n: int, edge_length: float = 1.0, device: int | None = None) -> TetMesh:
+def build_cube_mesh(n: int, edge_length: float = 1.0, device: int | str | None = "auto") -> TetMesh:
     """[0, edge_length]^3 split into n^3 hex cells of 6 Kuhn tets each."""
     if not isinstance(n, (int, np.integer)) or isinstance(n, bool) or n < 1:
         raise ValueError(f"subdivisions must be a positive integer, got {n!r}")
@@ -166,7 +229,7 @@ def build_cube_mesh(n: int, edge_length: float = 1.0, device: int | None = None)
 
 def build_torus_shell_mesh(nr: int, ntheta: int, nphi: int, R: float = 300.0,
                            a_in: float = 100.0, a_out: float = 120.0,
-                           device: int | None = None) -> TetMesh:
+                           device: int | str | None = "auto") -> TetMesh:
     """Toroidal-shell mesh; see torus_shell_arrays."""
     return TetMesh.from_arrays(*torus_shell_arrays(nr, ntheta, nphi, R, a_in, a_out),
                                device=device)
@@ -346,7 +409,12 @@ def write_tetmesh(mesh: TetMesh, path) -> None:
             fh.write(f"{a} {b} {c} {d}\n")
 
 
-def read_tetmesh(path) -> TetMesh:
+def read_tetmesh(path, device: int | str | None = "auto") -> TetMesh:
+    """read_tetmesh (mesh.py:312-331).  ``device`` as in
+    ``TetMesh.from_arrays``: the native reader (bt_mesh_read, parsed on all
+    host threads) unless ``None`` (the host Python parser + numpy path)."""
+    if device is not None:
+        return _native_call("bt_mesh_read", str(path).encode(), _native_device(device))
     path = Path(path)
     with open(path) as fh:
         header = fh.readline().split()
@@ -370,4 +438,4 @@ def read_tetmesh(path) -> TetMesh:
             raise MalformedMeshError(f"{path}: {err}") from err
     if vertices.shape != (nv, 3) or elements.shape != (ne, 4):
         raise MalformedMeshError(f"{path}: body does not match header counts")
-    return TetMesh.from_arrays(vertices, elements)
+    return TetMesh.from_arrays(vertices, elements, device=None)

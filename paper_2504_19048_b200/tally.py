@@ -94,36 +94,193 @@ def _producer_sync(t) -> None:
     torch.cuda.current_stream(t.device).synchronize()
 
 
-class TallyGrid:
-    """Read-through view of the device tally (tally.py:21-44 field names)."""
+class _LiveArray:
+    """A device tally array seen from the host: every read returns the current
+    device contents (``np.asarray(a)``, ``a[i]``, ``a.sum()`` ...), every item
+    assignment writes through (``a[i] = x``, ``a[:] = 0``) -- the live,
+    writable arrays of the reference's jitclass grid (tally.py:21-44)."""
 
-    def __init__(self, owner: "MeshTally"):
+    def __init__(self, grid: "TallyGrid", which: int, shape):
+        self._grid = grid
+        self._which = which
+        self.shape = tuple(shape)
+        self.dtype = np.dtype(np.float64)
+        self.ndim = len(self.shape)
+        self.size = int(np.prod(self.shape))
+
+    def _read(self) -> np.ndarray:
+        return self._grid._read(self._which).reshape(self.shape)
+
+    def __array__(self, dtype=None, copy=None):
+        a = self._read()
+        return a if dtype is None else a.astype(dtype)
+
+    def __len__(self) -> int:
+        return self.shape[0]
+
+    def __getitem__(self, idx):
+        return self._read()[idx]
+
+    def __setitem__(self, idx, value):
+        a = self._read()
+        a[idx] = value
+        self._grid._write(self._which, a.reshape(-1))
+
+    def __iter__(self):
+        return iter(self._read())
+
+    def __getattr__(self, name):  # sum, max, reshape, copy, tolist, ...
+        return getattr(self._read(), name)
+
+    def __repr__(self) -> str:
+        return f"_LiveArray({self._read()!r})"
+
+
+class TallyGrid:
+    """The device tally of a MeshTally (or of ``create_grid``) with the
+    reference grid's fields (tally.py:21-44): ``partials`` (1, E*G) -- the
+    unfinalized batch, one slab --, ``batch_accum`` (vestigial in the
+    reference too: always zero), ``sum``, ``sum_sq``, ``batches_completed``.
+    The arrays are live views of the device memory (read on access, written
+    through on assignment)."""
+
+    def __init__(self, owner):
         self._owner = owner
-        self.num_elements = owner.mesh.num_elements
+        self.num_elements = owner.num_elements
         self.num_groups = owner.num_groups
+        nb = self.num_elements * self.num_groups
+        self._partials = _LiveArray(self, _lib.BT_TALLY_BATCH, (1, nb))
+        self._sum = _LiveArray(self, _lib.BT_TALLY_SUM, (nb,))
+        self._sum_sq = _LiveArray(self, _lib.BT_TALLY_SUM_SQ, (nb,))
 
     def _read(self, which):
         return self._owner._read_tally(which)
 
+    def _write(self, which, a):
+        self._owner._write_tally(which, a)
+
     @property
-    def partials(self) -> np.ndarray:
-        return self._read(_lib.BT_TALLY_BATCH)[None, :]
+    def partials(self) -> _LiveArray:
+        return self._partials
 
     @property
     def batch_accum(self) -> np.ndarray:
         return np.zeros(self.num_elements * self.num_groups)
 
     @property
-    def sum(self) -> np.ndarray:
-        return self._read(_lib.BT_TALLY_SUM)
+    def sum(self) -> _LiveArray:
+        return self._sum
+
+    @sum.setter
+    def sum(self, v):
+        self._sum[:] = v
 
     @property
-    def sum_sq(self) -> np.ndarray:
-        return self._read(_lib.BT_TALLY_SUM_SQ)
+    def sum_sq(self) -> _LiveArray:
+        return self._sum_sq
+
+    @sum_sq.setter
+    def sum_sq(self, v):
+        self._sum_sq[:] = v
 
     @property
     def batches_completed(self) -> int:
         return self._owner.batches_completed
+
+    @batches_completed.setter
+    def batches_completed(self, n: int) -> None:
+        _lib.check(self._owner._L.bt_set_batches_completed(self._owner._h, int(n)))
+
+
+class _GridHandle:
+    """A tally-only device handle (bt_create_grid) behind ``create_grid``."""
+
+    def __init__(self, num_elements: int, num_groups: int, device: int):
+        self._L = _lib.load()
+        self.num_elements = int(num_elements)
+        self.num_groups = int(num_groups)
+        self._h = C.c_void_p()
+        _lib.check(self._L.bt_create_grid(self.num_elements, self.num_groups, int(device),
+                                          C.byref(self._h)))
+        _LIVE.add(self)
+
+    @property
+    def batches_completed(self) -> int:
+        n = C.c_int64()
+        _lib.check(self._L.bt_batches_completed(self._h, C.byref(n)))
+        return int(n.value)
+
+    def finalize_batch(self, w: float) -> None:
+        _lib.check(self._L.bt_finalize_batch(self._h, float(w)))
+
+    def _read_tally(self, which) -> np.ndarray:
+        n = self.num_elements * self.num_groups
+        out = np.empty(n)
+        _lib.check(self._L.bt_read_tally(self._h, which, out.ctypes.data, n))
+        return out
+
+    def _write_tally(self, which, a) -> None:
+        a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
+        _lib.check(self._L.bt_write_tally(self._h, which, a.ctypes.data, a.size))
+
+    def close(self) -> None:
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._L.bt_destroy(h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def create_grid(num_elements: int, num_groups: int, max_threads: int = 1, *,
+                device: int = 0) -> TallyGrid:
+    """tally.py:47-55: a zeroed element x group grid, allocated once (on the
+    GPU; ``max_threads`` is accepted -- one device tally replaces the
+    per-thread slabs)."""
+    if num_elements <= 0 or num_groups <= 0:
+        raise ValueError(f"grid sizes must be positive, got ({num_elements}, {num_groups})")
+    if max_threads < 1:
+        raise ValueError(f"max_threads must be >= 1, got {max_threads}")
+    return TallyGrid(_GridHandle(num_elements, num_groups, device))
+
+
+def _score(grid: TallyGrid, kind: int, element, group, weight, value) -> None:
+    e = np.ascontiguousarray(np.atleast_1d(element), dtype=np.int64)
+    g = np.ascontiguousarray(np.atleast_1d(group), dtype=np.int64)
+    w = np.ascontiguousarray(np.atleast_1d(weight), dtype=np.float64)
+    x = np.ascontiguousarray(np.atleast_1d(value), dtype=np.float64)
+    e, g, w, x = np.broadcast_arrays(e, g, w, x)
+    # _check_bin (tally.py:58-64) / the sigma_t check, before anything lands
+    if kind == 1 and not (x > 0.0).all():
+        raise ValueError(f"sigma_t must be positive, got {float(x[~(x > 0.0)][0])!r}")
+    bad = (e < 0) | (e >= grid.num_elements)
+    if bad.any():
+        raise IndexError(f"element {int(e[bad][0])} out of range [0, {grid.num_elements})")
+    bad = (g < 0) | (g >= grid.num_groups)
+    if bad.any():
+        raise IndexError(f"group {int(g[bad][0])} out of range [0, {grid.num_groups})")
+    e32 = np.ascontiguousarray(e, dtype=np.int32)
+    g32 = np.ascontiguousarray(g, dtype=np.int32)
+    w = np.ascontiguousarray(w)
+    x = np.ascontiguousarray(x)
+    o = grid._owner
+    _lib.check(o._L.bt_score(o._h, kind, e32.ctypes.data, g32.ctypes.data, w.ctypes.data,
+                             x.ctypes.data, e32.size, _lib.BT_MEM_HOST))
+
+
+def score_track_length(grid: TallyGrid, element, group, weight, length) -> None:
+    """tally.py:67-71: batch tally[element, group] += weight * length
+    (scalars as the reference, or equal-length arrays of events)."""
+    _score(grid, 0, element, group, weight, length)
+
+
+def score_collision(grid: TallyGrid, element, group, weight, sigma_t) -> None:
+    """tally.py:74-80: batch tally[element, group] += weight / sigma_t."""
+    _score(grid, 1, element, group, weight, sigma_t)
 
 
 def batch_totals(grid: TallyGrid) -> np.ndarray:
@@ -444,6 +601,14 @@ class MeshTally:
                             f"{' or '.join(self._DEVICE_DTYPES[itemsize])}")
         if t.device.index is not None and t.device.index != self.device:
             raise ValueError(f"tensor on cuda:{t.device.index}, handle on cuda:{self.device}")
+
+    @property
+    def num_elements(self) -> int:
+        return self._mesh.num_elements
+
+    def _write_tally(self, which, a) -> None:
+        a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
+        _lib.check(self._L.bt_write_tally(self._h, which, a.ctypes.data, a.size))
 
     def _read_tally(self, which) -> np.ndarray:
         n = self._mesh.num_elements * self.num_groups

@@ -149,3 +149,148 @@ def test_device_group_error_leaves_tally_untouched():
     assert not mt.batch_totals().any()
     assert mt.source_weight == 0.0
     mt.close()
+
+
+def test_paper_abi_file_constructor_and_vtk_writer(tmp_path):
+    """PumiTally(mesh_filename, ...) and write(filename) at the C ABI
+    (PAPER.md:265-270): bt_create_from_file + moves + bt_write_vtk /
+    bt_write_flux_csv write the same bytes as the Python facade's writers
+    (which match the reference's, tests/test_writers.py)."""
+    import ctypes as C
+    from paper_2504_19048_b200 import mesh as M
+    L = _lib.load()
+    m = build_cube_mesh(6)
+    path = tmp_path / "cube6.tet"
+    M.write_tetmesh(m, path)
+    gen = np.random.default_rng(12)
+    n = 3000
+    pos = synth.uniform_box(gen, n)
+    h = C.c_void_p()
+    _lib.check(L.bt_create_from_file(str(path).encode(), n, 2, 0, C.byref(h)))
+    mt = MeshTally(str(path), n, 2)  # the facade reads the file the same way
+    s = _lib.Summary()
+    for batch in range(2):
+        _lib.check(L.bt_initialize_particle_location(h, pos.ctypes.data, pos.size,
+                                                     _lib.BT_MEM_HOST, 0, C.byref(s)))
+        mt.initialize_particle_location(pos)
+        dest = np.ascontiguousarray(synth.flight_destinations(gen, pos, 5.0))
+        fly = np.ones(n, np.int8)
+        w = np.ascontiguousarray(0.5 + gen.random(n))
+        g = np.ascontiguousarray(gen.integers(0, 2, n).astype(np.int32))
+        _lib.check(L.bt_move_to_next_location(h, dest.ctypes.data, fly.ctypes.data, w.ctypes.data,
+                                              g.ctypes.data, n, _lib.BT_MEM_HOST, C.byref(s)))
+        mt.move_to_next_location(dest, fly, w, g)
+        _lib.check(L.bt_finalize_batch(h, 0.0))
+        mt.finalize_batch()
+    # the C writers on the file-made handle vs the Python writers on its moments
+    E, G = m.num_elements, 2
+    sm, sq = np.empty(E * G), np.empty(E * G)
+    _lib.check(L.bt_read_tally(h, _lib.BT_TALLY_SUM, sm.ctypes.data, E * G))
+    _lib.check(L.bt_read_tally(h, _lib.BT_TALLY_SUM_SQ, sq.ctypes.data, E * G))
+    from paper_2504_19048_b200 import FluxResult, write_flux_csv, write_vtk
+    nb = 2
+    bm = sm.reshape(E, G) / nb
+    mean = bm / m.volumes[:, None]
+    var = np.clip((sq.reshape(E, G) - sm.reshape(E, G) ** 2 / nb) / (nb - 1), 0.0, None)
+    rel = np.zeros((E, G))
+    nz = bm > 0
+    rel[nz] = np.sqrt(var / nb)[nz] / bm[nz]
+    fr = FluxResult(mean=mean, rel_error=rel)
+    a, b = tmp_path / "c.vtk", tmp_path / "py.vtk"
+    _lib.check(L.bt_write_vtk(h, str(a).encode(), None))
+    write_vtk(m, fr, b)
+    assert a.read_bytes() == b.read_bytes()
+    a, b = tmp_path / "c.csv", tmp_path / "py.csv"
+    _lib.check(L.bt_write_flux_csv(h, str(a).encode(), None))
+    write_flux_csv(fr, b)
+    assert a.read_bytes() == b.read_bytes()
+    # a handle made from arrays (the facade's) needs the volumes; same bytes
+    # as the facade's own write()
+    assert L.bt_write_vtk(mt._h, str(a).encode(), None) == _lib.BT_EINVAL
+    vol = np.ascontiguousarray(mt.mesh.volumes)
+    _lib.check(L.bt_write_vtk(mt._h, str(a).encode(), vol.ctypes.data))
+    mt.write(b)
+    assert a.read_bytes() == b.read_bytes()
+    L.bt_destroy(h)
+    mt.close()
+
+
+def test_create_grid_and_scoring_functions():
+    """create_grid / score_track_length / score_collision / finalize_batch /
+    flux (tally.py:47-152) on a standalone device grid, against the same
+    arithmetic in numpy; the reference's argument errors."""
+    from paper_2504_19048_b200 import (batch_totals, create_grid, finalize_batch, flux,
+                                       score_collision, score_track_length)
+    E, G = 50, 3
+    grid = create_grid(E, G)
+    ref = np.zeros(E * G)
+    s = np.zeros(E * G)
+    sq = np.zeros(E * G)
+    gen = np.random.default_rng(4)
+    for batch in range(3):
+        score_track_length(grid, 7, 2, 0.5, 3.0)
+        ref[7 * G + 2] += 0.5 * 3.0
+        score_collision(grid, 8, 0, 2.0, 4.0)
+        ref[8 * G + 0] += 2.0 / 4.0
+        e = gen.integers(0, E, 1000)
+        g = gen.integers(0, G, 1000)
+        w = gen.random(1000)
+        x = gen.random(1000) + 0.1
+        score_track_length(grid, e, g, w, x)
+        np.add.at(ref, e * G + g, w * x)
+        assert np.allclose(batch_totals(grid).reshape(-1), ref, rtol=1e-12, atol=0)
+        finalize_batch(grid, 10.0)
+        s += ref / 10.0
+        sq += (ref / 10.0) ** 2
+        ref[:] = 0.0
+    assert grid.batches_completed == 3
+    assert np.allclose(grid.sum, s, rtol=1e-12) and np.allclose(grid.sum_sq, sq, rtol=1e-12)
+    vol = np.full(E, 0.25)
+    fr = flux(grid, vol)
+    assert np.allclose(fr.mean, (s / 3).reshape(E, G) / 0.25, rtol=1e-12)
+    with pytest.raises(IndexError):
+        score_track_length(grid, E, 0, 1.0, 1.0)
+    with pytest.raises(IndexError):
+        score_track_length(grid, 0, G, 1.0, 1.0)
+    with pytest.raises(ValueError):
+        score_collision(grid, 0, 0, 1.0, 0.0)
+    with pytest.raises(ValueError):
+        finalize_batch(grid, 0.0)
+    with pytest.raises(ValueError):
+        create_grid(0, 1)
+
+
+def test_grid_is_live_and_writable():
+    """MeshTally.grid reads the device arrays on every access and writes
+    through on assignment (the reference's grid is the live jitclass)."""
+    from paper_2504_19048_b200 import batch_totals, score_track_length
+    m = build_cube_mesh(5)
+    gen = np.random.default_rng(9)
+    n = 2000
+    pos = synth.uniform_box(gen, n)
+    mt = MeshTally(m, n)
+    grid = mt.grid
+    mt.initialize_particle_location(pos)
+    mt.move_to_next_location(synth.flight_destinations(gen, pos, 5.0), np.ones(n, np.int8),
+                             np.ones(n))
+    live = grid.partials
+    tot = float(np.asarray(live).sum())
+    assert tot > 0 and tot == pytest.approx(float(mt.read_particles().seg_total.sum()), rel=1e-12)
+    score_track_length(grid, 3, 0, 2.0, 0.25)
+    assert float(np.asarray(live).sum()) == pytest.approx(tot + 0.5, rel=1e-12)
+    live[0, :] = 0.0
+    assert not batch_totals(grid).any()
+    grid.sum[5] = 7.0
+    assert grid.sum[5] == 7.0 and np.asarray(grid.sum).sum() == 7.0
+    grid.batches_completed = 2
+    assert mt.batches_completed == 2
+    mt.close()
+
+
+def test_gpu_adjacency_is_the_default_with_a_gpu():
+    from paper_2504_19048_b200 import mesh as M
+    assert _lib.device_count() >= 1
+    a = M.build_cube_mesh(20, device=None)
+    b = M.build_cube_mesh(20)  # "auto": native ingest, adjacency on GPU 0
+    for f in ("elements", "adj_elem", "adj_face", "volumes", "centroids"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
