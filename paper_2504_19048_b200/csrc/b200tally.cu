@@ -2263,14 +2263,36 @@ static bt_status handle_mesh(bt_tally* h, std::vector<double>& v, std::vector<in
     return BT_OK;
 }
 
+// flux (tally.py:123-152) of the handle's track-length moments, evaluated on
+// the host in the reference's operation order (so the writers' text equals
+// the reference writers' on the same moments)
 static bt_status handle_flux(bt_tally* h, const double* volumes, std::vector<double>& mean,
                              std::vector<double>& rel) {
     const double* vol = volumes ? volumes : (h->host_mesh ? h->host_mesh->vol.data() : nullptr);
     if (!vol) return set_err(BT_EINVAL, "volumes are required for a handle made from arrays");
-    const int64_t nb = h->ne * h->ngroups;
-    mean.resize((size_t)nb);
-    rel.resize((size_t)nb);
-    return bt_flux(h, 0, vol, mean.data(), rel.data());
+    int64_t n = 0;
+    TRY(bt_batches_completed(h, &n));
+    if (n == 0) return set_err(BT_ERUNTIME, "no batches completed; nothing to normalize");
+    for (int64_t e = 0; e < h->ne; ++e)
+        if (!(vol[e] > 0.0)) return set_err(BT_EINVAL, "volumes must be positive");
+    const int64_t G = h->ngroups, nb = h->ne * G;
+    std::vector<double> s((size_t)nb), sq((size_t)nb);
+    TRY(bt_read_tally(h, BT_TALLY_SUM, s.data(), nb));
+    TRY(bt_read_tally(h, BT_TALLY_SUM_SQ, sq.data(), nb));
+    mean.assign((size_t)nb, 0.0);
+    rel.assign((size_t)nb, 0.0);
+    const double dn = (double)n;
+    for (int64_t b = 0; b < nb; ++b) {
+        const double bm = s[(size_t)b] / dn;
+        mean[(size_t)b] = bm / vol[b / G];
+        if (n >= 2) {
+            double var = (sq[(size_t)b] - s[(size_t)b] * s[(size_t)b] / dn) / (dn - 1.0);
+            if (var < 0.0) var = 0.0;  // np.clip(var, 0.0, None)
+            const double se = std::sqrt(var / dn);
+            if (bm > 0.0) rel[(size_t)b] = se / bm;
+        }
+    }
+    return BT_OK;
 }
 
 bt_status bt_write_vtk(bt_tally* h, const char* filename, const double* volumes) {

@@ -5,7 +5,15 @@ bit-exact to the reference's transport.run (tests/test_transport_oracle.py).
 * Histories: identical sequence of operations; they stay bit-identical
   until a CUDA log/sin/cos result differs from the host libm in the last
   bit.  The fraction of bit-identical particle histories is measured and
-  must be high; everything else is compared statistically.
+  must be high; everything else is compared statistically, with bounds
+  from the runs' own variance: per-history PAIRED differences (device minus
+  reference, same particle, same random stream) of the history's track
+  length, random blocks consumed (2 per collision + 2 per history) and
+  outcome.  Identical histories contribute 0; a diverged history continues
+  as an independent draw from the same process, so an unbiased device has
+  E[difference] = 0 and the mean difference must lie within K standard
+  errors of 0 -- a 1% bias in the collision rate or the scatter sampling
+  fails this at the sizes below, where a flat 5% bound would not.
 """
 
 import numpy as np
@@ -17,6 +25,27 @@ from paper_2504_19048_b200 import build_cube_mesh
 from paper_2504_19048_b200 import transport as T
 
 pytestmark = pytest.mark.gpu
+
+K = 4.0  # standard errors
+
+
+def _paired_ok(a, b, what):
+    """mean(a - b) within K standard errors of 0 (exactly 0 if all equal)."""
+    d = np.asarray(a, dtype=np.float64) - np.asarray(b, dtype=np.float64)
+    n = d.size
+    se = d.std(ddof=1) / np.sqrt(n) if n > 1 else 0.0
+    m = d.mean()
+    print(f"  {what}: mean diff {m:.4g}, se {se:.3g}, diverged {(d != 0).mean():.3f}")
+    assert abs(m) <= K * se + 1e-12 * max(1.0, float(np.abs(b).mean())), what
+    return d
+
+
+def _total_ok(total_a, total_b, d_last, nb, what):
+    """A run total (all batches) against the reference's: the paired per-
+    history differences of the last batch give its standard error."""
+    se = np.sqrt(nb * float((d_last ** 2).sum()))
+    print(f"  {what}: {total_a} vs {total_b}, K*se = {K * se:.4g}")
+    assert abs(total_a - total_b) <= K * se + 1e-9 * abs(total_b), what
 
 
 @pytest.fixture(scope="module")
@@ -68,24 +97,28 @@ def test_transport_statistical_parity(gold, name):
     assert frac > 0.5
     # balance: every source particle leaks, is absorbed or stuck-killed
     assert r.leaked_weight + r.absorbed_weight + r.stuck_weight == r.source_weight
-    tot = n * nb
-    for key in ("leaked_weight", "absorbed_weight"):
-        ref = float(gold[p + key])
-        q = ref / tot
-        sigma = np.sqrt(2 * tot * q * (1 - q)) + 1.0
-        assert abs(getattr(r, key) - ref) <= 5 * sigma, key
-    c_ref = float(gold[p + "collisions"])
-    assert abs(r.collisions - c_ref) <= 0.05 * c_ref + 50
-    # integrated flux (track length per source particle) and collision estimate
+    # per-history paired differences (last batch) and the run totals
+    d_seg = _paired_ok(fs["seg_total"], gold[p + "final_seg_total"], "track length") \
+        if p + "final_seg_total" in gold else None
+    d_blk = _paired_ok(fs["rng_block"], gold[p + "final_rng_block"], "random blocks")
+    _paired_ok(fs["outcome"] == 2, gold[p + "final_outcome"] == 2, "leaked")
+    _total_ok(r.collisions, float(gold[p + "collisions"]), d_blk / 2.0, nb, "collisions")
+    if d_seg is not None:
+        V = m.volumes[:, None]
+        a = float((r.flux_track.mean * V).sum())
+        b = float((gold[p + "flux_track_mean"] * V).sum())
+        # integrated track-length flux = track length / (batches x source weight)
+        _total_ok(a, b, d_seg / (nb * n), nb, "integrated track flux")
+    # both estimators agree with each other (same physics): the collision
+    # estimator's integral against the track-length one, within their
+    # batch-to-batch errors
     V = m.volumes[:, None]
-    for est, key in ((r.flux_track, "flux_track_mean"), (r.flux_collision, "flux_col_mean")):
-        a = float((est.mean * V).sum())
-        b = float((gold[p + key] * V).sum())
-        assert abs(a - b) <= 0.05 * abs(b), (key, a, b)
-    # both estimators agree with each other (same physics)
     a = float((r.flux_track.mean * V).sum())
-    b = float((r.flux_collision.mean * V).sum())
-    assert abs(a - b) <= 0.05 * abs(b)
+    c = float((r.flux_collision.mean * V).sum())
+    se = float((r.flux_track.rel_error * r.flux_track.mean * V).sum()
+               + (r.flux_collision.rel_error * r.flux_collision.mean * V).sum())
+    if nb >= 2:
+        assert abs(a - c) <= K * se, (a, c, se)
 
 
 def test_transport_vs_oracle_same_engine():
@@ -103,6 +136,12 @@ def test_transport_vs_oracle_same_engine():
     print("paper physics: identical histories", same.mean(), "events", r.events, o["events"],
           "collisions", r.collisions, o["collisions"])
     assert same.mean() > 0.2
-    assert abs(r.collisions - o["collisions"]) <= 0.03 * o["collisions"]
-    assert abs(r.events - o["events"]) <= 0.03 * o["events"]
-    assert abs(r.track_length_total - o["track_length_total"]) <= 0.03 * o["track_length_total"]
+    fs = r.final_state
+    n, nb = cfg.num_particles, cfg.num_batches
+    d_seg = _paired_ok(fs["seg_total"], o["seg_total"][:n], "track length")
+    d_blk = _paired_ok(fs["rng_block"], o["rng_block"][:n], "random blocks")
+    _paired_ok(fs["outcome"] == 2, o["outcome"][:n] == 2, "leaked")
+    _paired_ok(fs["outcome"] == 5, o["outcome"][:n] == 5, "absorbed")
+    _total_ok(r.collisions, o["collisions"], d_blk / 2.0, nb, "collisions")
+    _total_ok(r.events, o["events"], d_blk, nb, "events")
+    _total_ok(r.track_length_total, o["track_length_total"], d_seg, nb, "track length")
