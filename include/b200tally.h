@@ -77,9 +77,16 @@ enum {
                                  arrays, no stage kernel) */
     BT_OPT_MOVE_CHUNKS = 6,   /* host inputs: copy/walk pipeline depth (0 = auto, <= 16) */
     BT_OPT_LOCATE_LANES = 7,  /* grid localization: lanes per particle 1..32 (0 = default 2) */
-    BT_OPT_EXACT_ONLY = 8     /* 1: no fp32 pre-filters -- grid localization tests every
+    BT_OPT_EXACT_ONLY = 8,    /* 1: no fp32 pre-filters -- grid localization tests every
                                  candidate exactly, and (with BT_OPT_DIGEST) every exit search
                                  runs the reference's literal arithmetic; for validation */
+    BT_OPT_DEFER_INIT = 9     /* host positions, grid mode, >= 2^20 particles: 1 = the
+                                 initialize call returns once the DMA (from the front) and
+                                 host threads (from the back, into pinned staging) have read
+                                 the caller's buffer; the parked part is copied and localized
+                                 by the next call (the move: chunk by chunk, ahead of the walk
+                                 chunks that need it); 0 (default, measured faster end to
+                                 end): copy it all in the initialize call */
 };
 
 /* Mirrors meshtally.search.TraceSummary (search.py:150-157). */

@@ -152,6 +152,20 @@ struct bt_tally {
     HostStager* stager = nullptr;             // pageable host inputs (host_stage.cuh)
     Multi* multi = nullptr;                   // non-null: a multi-GPU handle (multi.cuh)
     bt_mesh* host_mesh = nullptr;             // owned host copy (bt_create_from_mesh / _file)
+    // Deferred localization of host positions (initialize -> the next move):
+    // positions split into chunks of di_chunk particles; a chunk is either
+    // copied and localized already (di_state 0: the DMA read it straight from
+    // the caller's pinned buffer during the initialize call) or parked in the
+    // pinned host buffer pos_stage (di_state 1) by host threads, to be copied
+    // and localized when the move reaches it.
+    cudaStream_t lstream = nullptr;           // localization of deferred chunks
+    double* pos_stage = nullptr;              // pinned, 3 * cap doubles (lazily)
+    int64_t di_count = 0, di_chunk = 0;
+    int di_nch = 0;
+    bool di_pending = false;
+    std::vector<uint8_t> di_state;
+    std::vector<cudaEvent_t> di_ev;           // per chunk: localized (on lstream)
+    std::vector<cudaEvent_t> di_cev;          // per chunk: copied (on cstream)
     // transport (allocated on first bt_transport_run)
     double* col_tally = nullptr;
     double* col_sum = nullptr;
@@ -186,6 +200,7 @@ struct bt_tally {
     bool opt_sort = false;
     int opt_wagg = WAGG_ADAPTIVE;
     bool opt_exact_only = false;
+    bool opt_no_defer = true;  // BT_OPT_DEFER_INIT = 0 (default: measured slower, see below)
     int opt_staged = 2;  // 0: v1 refill, 1: stage kernel + work list, 2: direct refill
     WorkSoA work{};
     void* work_mem = nullptr;
@@ -255,6 +270,10 @@ static bt_status free_all(bt_tally* h) {
     if (h->ev_loc) cudaEventDestroy(h->ev_loc);
     for (cudaEvent_t e : h->evchunk)
         if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : h->di_ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : h->di_cev) cudaEventDestroy(e);
+    if (h->lstream) cudaStreamDestroy(h->lstream);
+    if (h->pos_stage) cudaFreeHost(h->pos_stage);
     if (h->stream) cudaStreamDestroy(h->stream);
     if (h->cstream) cudaStreamDestroy(h->cstream);
     if (h->stream2) cudaStreamDestroy(h->stream2);
@@ -554,6 +573,14 @@ bt_status bt_create(const double* vertices, int64_t num_vertices, const int32_t*
     CKF(cudaEventCreate(&h->ev3));
     CKF(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
     CKF(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
+    {
+        // localization of parked chunks at the highest priority: the walk's
+        // persistent CTAs hold the SMs, a launch from this stream gets the
+        // SMs freed between walk chunks first
+        int lo_p = 0, hi_p = 0;
+        CKF(cudaDeviceGetStreamPriorityRange(&lo_p, &hi_p));
+        CKF(cudaStreamCreateWithPriority(&h->lstream, cudaStreamNonBlocking, hi_p));
+    }
     CKF(cudaEventCreateWithFlags(&h->ev_s1, cudaEventDisableTiming));
     CKF(cudaEventCreateWithFlags(&h->ev_s2, cudaEventDisableTiming));
     CKF(cudaEventCreateWithFlags(&h->evc0, cudaEventDisableTiming));
@@ -687,6 +714,7 @@ bt_status bt_destroy(bt_tally* h) {
     cudaSetDevice(h->dev);
     cudaStreamSynchronize(h->stream);
     cudaStreamSynchronize(h->cstream);
+    if (h->lstream) cudaStreamSynchronize(h->lstream);
     free_all(h);
     delete h;
     return BT_OK;
@@ -737,6 +765,7 @@ bt_status bt_set_option(bt_tally* h, int32_t key, int64_t value) {
             break;
         case BT_OPT_MOVE_CHUNKS: h->move_chunks = (int)value; break;
         case BT_OPT_EXACT_ONLY: h->opt_exact_only = value != 0; break;
+        case BT_OPT_DEFER_INIT: h->opt_no_defer = value == 0; break;
         case BT_OPT_LOCATE_LANES:
             if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8 &&
                 value != 16 && value != 32)
@@ -977,17 +1006,19 @@ static bt_status run_walk(bt_tally* h, const double* dest, const int8_t* fly, co
 
 // lanes per particle of the grid search (BT_OPT_LOCATE_LANES; 0 = default)
 constexpr int DEFAULT_LOCATE_LANES = 2;  // measured best on C2 and the 10M-tet cube (tools/locate_sweep.py)
-static bt_status launch_locate(bt_tally* h, const LocateArgs& la, int64_t n) {
+static bt_status launch_locate(bt_tally* h, const LocateArgs& la, int64_t n,
+                               cudaStream_t st = nullptr) {
+    if (!st) st = h->stream;
     const int g = h->locate_lanes > 0 ? h->locate_lanes : DEFAULT_LOCATE_LANES;
     const int64_t threads = n * g;
     const unsigned blocks = (unsigned)((threads + LOCATE_THREADS - 1) / LOCATE_THREADS);
     switch (g) {
-        case 1: locate_grid_kernel<1><<<blocks, LOCATE_THREADS, 0, h->stream>>>(la); break;
-        case 2: locate_grid_kernel<2><<<blocks, LOCATE_THREADS, 0, h->stream>>>(la); break;
-        case 4: locate_grid_kernel<4><<<blocks, LOCATE_THREADS, 0, h->stream>>>(la); break;
-        case 8: locate_grid_kernel<8><<<blocks, LOCATE_THREADS, 0, h->stream>>>(la); break;
-        case 16: locate_grid_kernel<16><<<blocks, LOCATE_THREADS, 0, h->stream>>>(la); break;
-        case 32: locate_grid_kernel<32><<<blocks, LOCATE_THREADS, 0, h->stream>>>(la); break;
+        case 1: locate_grid_kernel<1><<<blocks, LOCATE_THREADS, 0, st>>>(la); break;
+        case 2: locate_grid_kernel<2><<<blocks, LOCATE_THREADS, 0, st>>>(la); break;
+        case 4: locate_grid_kernel<4><<<blocks, LOCATE_THREADS, 0, st>>>(la); break;
+        case 8: locate_grid_kernel<8><<<blocks, LOCATE_THREADS, 0, st>>>(la); break;
+        case 16: locate_grid_kernel<16><<<blocks, LOCATE_THREADS, 0, st>>>(la); break;
+        case 32: locate_grid_kernel<32><<<blocks, LOCATE_THREADS, 0, st>>>(la); break;
         default: return set_err(BT_EINVAL, "locate lanes must be 1, 2, 4, 8, 16 or 32");
     }
     CK(cudaGetLastError());
@@ -1017,6 +1048,160 @@ static LocateArgs locate_args(bt_tally* h, const double* target, int64_t count) 
     return a;
 }
 
+
+// ---- deferred localization of host positions (see bt_tally::di_*)
+
+// copy chunk k of the pending initialize from pos_stage and localize it
+static bt_status di_enqueue(bt_tally* h, int k) {
+    if (h->di_state[(size_t)k] != 1) return BT_OK;
+    const int64_t lo = (int64_t)k * h->di_chunk, hi = std::min(h->di_count, lo + h->di_chunk);
+    CK(cudaMemcpyAsync(h->init_stage + 3 * lo, h->pos_stage + 3 * lo,
+                       sizeof(double) * 3 * (hi - lo), cudaMemcpyHostToDevice, h->cstream));
+    CK(cudaEventRecord(h->di_cev[(size_t)k], h->cstream));
+    CK(cudaStreamWaitEvent(h->lstream, h->di_cev[(size_t)k], 0));
+    LocateArgs la = locate_args(h, h->init_stage, hi);
+    la.lo = lo;
+    TRY(launch_locate(h, la, hi - lo, h->lstream));
+    CK(cudaEventRecord(h->di_ev[(size_t)k], h->lstream));
+    h->di_state[(size_t)k] = 0;
+    return BT_OK;
+}
+
+// stream `st` waits until particles [lo, hi) of the pending initialize are
+// localized (enqueuing the parked chunks among them first)
+static bt_status di_depend(bt_tally* h, int64_t lo, int64_t hi, cudaStream_t st) {
+    if (!h->di_pending) return BT_OK;
+    hi = std::min(hi, h->di_count);
+    if (lo >= hi) return BT_OK;
+    const int k0 = (int)(lo / h->di_chunk), k1 = (int)((hi - 1) / h->di_chunk);
+    for (int k = k0; k <= k1; ++k) {
+        TRY(di_enqueue(h, k));
+        CK(cudaStreamWaitEvent(st, h->di_ev[(size_t)k], 0));
+    }
+    return BT_OK;
+}
+
+// finish the pending initialize: every parked chunk copied and localized,
+// the main stream ordered after all of it
+static bt_status settle_init(bt_tally* h) {
+    if (!h->di_pending) return BT_OK;
+    for (int k = 0; k < h->di_nch; ++k) TRY(di_enqueue(h, k));
+    CK(cudaEventRecord(h->ev_loc, h->lstream));
+    CK(cudaStreamWaitEvent(h->stream, h->ev_loc, 0));
+    h->di_pending = false;
+    return BT_OK;
+}
+
+// initialize_particle_location with host positions, grid mode, count >=
+// DEFER_MIN: the caller's buffer is consumed from both ends at once -- the
+// DMA engine copies chunks from the front straight out of a pinned buffer
+// (each localized as soon as it lands), host threads copy chunks from the
+// back into the pinned pos_stage -- and the call returns when they meet
+// (PCIe + host memcpy bandwidth, ~90 GB/s on the GPU box instead of the DMA's
+// 53: tools/micro/hostcopy.cu).  The parked chunks are copied and localized
+// by the next move, interleaved with its own input copies, right before the
+// walk chunks that need them.  A pageable buffer is all parked.
+// Opt-in (BT_OPT_DEFER_INIT = 1): the call returns 1.3 ms sooner (C2, 1e7
+// pinned positions: 3.1 vs 4.5 ms), but the parked half's localization then
+// runs while the move's persistent walk CTAs hold every SM, so it waits for
+// a walk chunk to drain and the walk chunk after it waits for it: the move
+// takes 2.4 ms longer (tools/e2e_breakdown.py, profiles/r02_e2e_breakdown.txt).
+constexpr int64_t DEFER_MIN = 1 << 20;
+constexpr int64_t DI_CHUNK_BYTES = 8 << 20;
+static bt_status init_host_deferred(bt_tally* h, const double* positions, int64_t count,
+                                    bool pageable) {
+    if (!h->init_stage) TRY(dalloc(&h->init_stage, 3 * h->cap));
+    if (!h->pos_stage) CK(cudaMallocHost((void**)&h->pos_stage, sizeof(double) * 3 * h->cap));
+    if (!h->stager) h->stager = new HostStager();
+    TRY(h->stager->init());
+    // the previous localization (and its reads of init_stage) is complete
+    CK(cudaStreamWaitEvent(h->cstream, h->ev_loc, 0));
+    CK(cudaStreamWaitEvent(h->lstream, h->ev_loc, 0));
+    const int64_t P = std::max<int64_t>(1, DI_CHUNK_BYTES / 24);
+    const int nch = (int)((count + P - 1) / P);
+    h->di_count = count;
+    h->di_chunk = P;
+    h->di_nch = nch;
+    h->di_state.assign((size_t)nch, 0);
+    while ((int)h->di_ev.size() < nch) {
+        cudaEvent_t a, b;
+        CK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+        h->di_ev.push_back(a);
+        h->di_cev.push_back(b);
+    }
+    std::mutex mu;
+    int front = 0, back = nch - 1;  // next chunk for the DMA / for the host threads
+    int last_dma = -1;
+    bt_status st_dma = BT_OK;
+    std::string err_dma;
+    HostPool* pool = h->stager->pool;
+    pool->run([&](int i) {
+        if (i == 0 && !pageable) {  // the calling thread feeds the DMA engine
+            std::vector<int> inflight;
+            for (;;) {
+                int k;
+                {
+                    std::lock_guard<std::mutex> g(mu);
+                    if (front > back) break;
+                    k = front++;
+                }
+                const int64_t lo = (int64_t)k * P, hi = std::min(count, lo + P);
+                cudaError_t e = cudaMemcpyAsync(h->init_stage + 3 * lo, positions + 3 * lo,
+                                                sizeof(double) * 3 * (hi - lo),
+                                                cudaMemcpyHostToDevice, h->cstream);
+                if (e == cudaSuccess) e = cudaEventRecord(h->di_cev[(size_t)k], h->cstream);
+                if (e == cudaSuccess) e = cudaStreamWaitEvent(h->lstream, h->di_cev[(size_t)k], 0);
+                if (e != cudaSuccess) {
+                    st_dma = set_err(BT_ECUDA, "deferred initialize: %s", cudaGetErrorString(e));
+                    err_dma = g_err;
+                    std::lock_guard<std::mutex> g(mu);
+                    front = back + 1;
+                    break;
+                }
+                LocateArgs la = locate_args(h, h->init_stage, hi);
+                la.lo = lo;
+                const bt_status ls = launch_locate(h, la, hi - lo, h->lstream);
+                if (ls != BT_OK || cudaEventRecord(h->di_ev[(size_t)k], h->lstream) != cudaSuccess) {
+                    st_dma = ls != BT_OK ? ls : set_err(BT_ECUDA, "deferred initialize: event");
+                    err_dma = g_err;
+                    std::lock_guard<std::mutex> g(mu);
+                    front = back + 1;
+                    break;
+                }
+                last_dma = k;
+                // keep two copies queued: enough to keep the engine busy, few
+                // enough that the meeting point follows the actual rates
+                inflight.push_back(k);
+                if (inflight.size() > 2) {
+                    cudaEventSynchronize(h->di_cev[(size_t)inflight.front()]);
+                    inflight.erase(inflight.begin());
+                }
+            }
+            return;
+        }
+        for (;;) {  // host threads park chunks from the back
+            int k;
+            {
+                std::lock_guard<std::mutex> g(mu);
+                if (back < front) break;
+                k = back--;
+            }
+            const int64_t lo = (int64_t)k * P, hi = std::min(count, lo + P);
+            memcpy(h->pos_stage + 3 * lo, positions + 3 * lo, sizeof(double) * 3 * (hi - lo));
+            h->di_state[(size_t)k] = 1;
+        }
+    });
+    if (st_dma != BT_OK) {
+        g_err = err_dma;
+        return st_dma;
+    }
+    // the caller's buffer must be read before returning: the last front copy
+    if (last_dma >= 0) CK(cudaEventSynchronize(h->di_cev[(size_t)last_dma]));
+    h->di_pending = true;
+    return BT_OK;
+}
+
 bt_status bt_initialize_particle_location(bt_tally* h, const double* positions, int64_t size,
                                           int32_t mem_kind, int32_t mode, bt_summary* summary) {
     if (h && h->multi) return multi_initialize(h, positions, size, mem_kind, mode, summary);
@@ -1040,6 +1225,13 @@ bt_status bt_initialize_particle_location(bt_tally* h, const double* positions, 
     CK(cudaEventRecord(h->ev2, h->stream));
     const double* target = positions;
     const bool host = mem_kind == BT_MEM_HOST;
+    TRY(settle_init(h));  // a previous initialize's parked chunks
+    if (host && mode == BT_LOCATE_GRID && count >= DEFER_MIN && !h->opt_no_defer) {
+        TRY(init_host_deferred(h, positions, count, is_pageable(positions)));
+        CK(cudaEventRecord(h->ev3, h->stream));
+        h->call_pending = true;
+        return BT_OK;
+    }
     if (host && mode == BT_LOCATE_GRID) {
         // Copy on the copy stream into a dedicated staging buffer, then
         // return as soon as the caller's buffer has been read: the
@@ -1049,7 +1241,9 @@ bt_status bt_initialize_particle_location(bt_tally* h, const double* positions, 
         // have landed, while the next chunks are still being copied.
         if (!h->init_stage) TRY(dalloc(&h->init_stage, 3 * h->cap));
         CK(cudaStreamWaitEvent(h->cstream, h->ev_loc, 0));  // previous localization done
-        const int nch = (int)std::min<int64_t>(count >= (4 << 20) ? 4 : 1, count);
+        int nch_big = 4;
+        if (const char* env = getenv("B200TALLY_INIT_CHUNKS")) nch_big = std::max(1, std::min(MAX_CHUNKS, atoi(env)));
+        const int nch = (int)std::min<int64_t>(count >= (4 << 20) ? nch_big : 1, count);
         const bool pageable = is_pageable(positions);
         LocateArgs la = locate_args(h, h->init_stage, count);
         for (int c = 0; c < nch; ++c) {
@@ -1209,6 +1403,9 @@ bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, cons
             const int64_t n = hi - lo;
             if (n <= 0) continue;
             cudaStream_t st = (c & 1) ? h->stream2 : h->stream;
+            // the pending initialize's chunks under [lo, hi): copied and
+            // localized now, ahead of this chunk's own inputs
+            TRY(di_depend(h, lo, hi, st));
             TRY(h2d(h, h->dest + 3 * lo, destinations + 3 * lo, sizeof(double) * 3 * n,
                     h->cstream, pg_dest));
             TRY(h2d(h, h->fly + lo, flying + lo, n, h->cstream, pg_fly));
@@ -1217,16 +1414,18 @@ bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, cons
                 TRY(h2d(h, h->group + lo, groups + lo, sizeof(int32_t) * n, h->cstream, pg_g));
             CK(cudaEventRecord(h->evchunk[c], h->cstream));
             CK(cudaStreamWaitEvent(st, h->evchunk[c], 0));
-            TRY(walk_enqueue(h, a, lo, hi, c, nullptr, st));
+            TRY(walk_enqueue(h, a, lo, hi, c, st));
         }
         CK(cudaEventRecord(h->ev_s2, h->stream2));
         CK(cudaStreamWaitEvent(h->stream, h->ev_s2, 0));
+        TRY(settle_init(h));  // particles beyond this move's count
         s = walk_end(h, a.max_sweeps, summary, ov);
         if (need_w) h->source_weight = job.out;
     } else {
         // Device inputs: one host synchronisation per move.  The group range
         // check, the refill choice and the recorded source weight are all
         // decided on the device, and come back with the counters in one copy.
+        TRY(settle_init(h));
         WalkArgs a = walk_args(h, destinations, flying, weights, true);
         TRY(walk_begin(h));
         a.gate = h->dcounters + 14;  // [14] walkable, [15] prepare_kernel's flags
@@ -1351,6 +1550,7 @@ bt_status bt_read_particles(bt_tally* h, int64_t count, double* position, int32_
     if (!h) return set_err(BT_EINVAL, "NULL handle");
     if (count < 0 || count > h->cap) return set_err(BT_EINVAL, "count out of range");
     TRY(ensure_device(h));
+    TRY(settle_init(h));
     auto cp = [&](void* dst, const void* src, size_t bytes) -> bt_status {
         if (dst && bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, h->stream));
         return BT_OK;
@@ -1372,6 +1572,7 @@ bt_status bt_read_digest(bt_tally* h, int64_t count, uint64_t* digest, int64_t* 
     if (!h->digest) return set_err(BT_EINVAL, "digests are off (BT_OPT_DIGEST)");
     if (count < 0 || count > h->cap) return set_err(BT_EINVAL, "count out of range");
     TRY(ensure_device(h));
+    TRY(settle_init(h));
     if (digest)
         CK(cudaMemcpyAsync(digest, h->digest, sizeof(uint64_t) * count, cudaMemcpyDeviceToHost,
                            h->stream));
@@ -1404,6 +1605,7 @@ bt_status bt_particle_device_ptrs(bt_tally* h, double** position, int32_t** elem
     // the localization of host positions completes asynchronously: a consumer
     // on another stream (e.g. torch's) must see its element / pos / alive
     TRY(ensure_device(h));
+    TRY(settle_init(h));
     CK(cudaStreamSynchronize(h->stream));
     if (position) *position = h->pos;
     if (element) *element = h->element;
@@ -1418,6 +1620,7 @@ bt_status bt_save_state(bt_tally* h) {
     }
     if (!h) return set_err(BT_EINVAL, "NULL handle");
     TRY(ensure_device(h));
+    TRY(settle_init(h));
     const int64_t n = h->cap;
     if (!h->snap_pos) {
         TRY(dalloc(&h->snap_pos, 3 * n));
@@ -1446,6 +1649,7 @@ bt_status bt_restore_state(bt_tally* h) {
     if (!h) return set_err(BT_EINVAL, "NULL handle");
     if (!h->have_snapshot) return set_err(BT_EINVAL, "no snapshot saved");
     TRY(ensure_device(h));
+    TRY(settle_init(h));
     const int64_t n = h->cap;
     auto d2d = cudaMemcpyDeviceToDevice;
     CK(cudaMemcpyAsync(h->pos, h->snap_pos, sizeof(double) * 3 * n, d2d, h->stream));
@@ -1574,6 +1778,7 @@ bt_status bt_transport_run(bt_tally* h, const double* sigma_t, const double* sig
     if (num_batches <= 0) return set_err(BT_EINVAL, "num_batches must be positive");
     memset(out, 0, sizeof *out);
     TRY(ensure_device(h));
+    TRY(settle_init(h));
     const int64_t n = num_particles, nb = h->ne * h->ngroups, G = num_groups;
     if (!h->col_tally) {
         TRY(dalloc(&h->col_tally, nb));
@@ -1788,6 +1993,7 @@ bt_status bt_load_step(bt_tally* h, const double* destinations, const int8_t* fl
         return set_err(BT_EINVAL, "count %lld outside [0, %lld]", (long long)count,
                        (long long)h->cap);
     TRY(ensure_device(h));
+    TRY(settle_init(h));
     if (count == 0) return BT_OK;
     if (!destinations || !flying || !weights) return set_err(BT_EINVAL, "NULL array");
     if (!h->tr_fly) TRY(dalloc(&h->tr_fly, h->cap));
@@ -1829,6 +2035,7 @@ bt_status bt_trace_begin(bt_tally* h, int32_t score, int64_t max_sweeps) {
     MULTI_SINGLE(h);
     if (!h) return set_err(BT_EINVAL, "NULL handle");
     TRY(ensure_device(h));
+    TRY(settle_init(h));
     if (!h->tr_fly) return set_err(BT_EINVAL, "no step loaded (bt_load_step)");
     TRY(ensure_sweep_bufs(h));
     // _check_localized (search.py:440-446)

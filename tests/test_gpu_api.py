@@ -183,6 +183,9 @@ def test_paper_abi_file_constructor_and_vtk_writer(tmp_path):
         _lib.check(L.bt_finalize_batch(h, 0.0))
         mt.finalize_batch()
     # the C writers on the file-made handle vs the Python writers on its moments
+    # (volumes of the mesh as read back: the file holds the oriented rows, whose
+    # recomputed volumes may differ in the last bit, as in the reference)
+    m = M.read_tetmesh(path)
     E, G = m.num_elements, 2
     sm, sq = np.empty(E * G), np.empty(E * G)
     _lib.check(L.bt_read_tally(h, _lib.BT_TALLY_SUM, sm.ctypes.data, E * G))
@@ -294,3 +297,57 @@ def test_gpu_adjacency_is_the_default_with_a_gpu():
     b = M.build_cube_mesh(20)  # "auto": native ingest, adjacency on GPU 0
     for f in ("elements", "adj_elem", "adj_face", "volumes", "centroids"):
         assert np.array_equal(getattr(a, f), getattr(b, f)), f
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_deferred_initialize_paths(pinned):
+    """Host positions of >= 2^20 particles with BT_OPT_DEFER_INIT = 1: the
+    initialize call parks part of them in pinned staging and the next call
+    localizes them.  Every way the parked part can be consumed -- a move over all
+    particles, a move over fewer (the rest settled after the walk), a readout
+    in between, a second initialize on top -- must equal the undeferred path
+    bit for bit."""
+    torch = pytest.importorskip("torch")
+    m = build_cube_mesh(14)
+    gen = np.random.default_rng(55)
+    n = 3_000_000
+    pos = synth.uniform_box(gen, n)
+    dest = synth.flight_destinations(gen, pos, 4.0)
+    fly = (gen.random(n) < 0.9).astype(np.int8)
+    w = 0.5 + gen.random(n)
+
+    def host(a):
+        return torch.from_numpy(a).pin_memory().numpy() if pinned else a
+
+    hp, hd, hf, hw = host(pos), host(dest), host(fly), host(w)
+    runs = []
+    for defer in (0, 1):
+        mt = MeshTally(m, n)
+        mt.set_option(_lib.BT_OPT_DEFER_INIT, defer)
+        out = []
+        mt.initialize_particle_location(hp)                 # then a full move
+        out.append(mt.move_to_next_location(hd, hf, hw))
+        out.append(mt.read_particles())
+        mt.initialize_particle_location(hp)                 # then a short move
+        k = n - 777_777
+        out.append(mt.move_to_next_location(hd[:k], hf[:k], hw[:k]))
+        out.append(mt.read_particles())
+        mt.initialize_particle_location(hp)                 # then a readout
+        out.append(mt.read_particles())
+        mt.initialize_particle_location(hp[: n // 2])
+        mt.initialize_particle_location(hp)                 # init on top of init
+        out.append(mt.move_to_next_location(hd, hf, hw))
+        out.append(mt.read_particles())
+        out.append(mt.batch_totals().copy())
+        runs.append(out)
+        mt.close()
+    a, b = runs
+    for x, y in zip(a, b):
+        if hasattr(x, "position"):
+            for key in ("position", "element", "alive", "entry_face", "stuck", "outcome",
+                        "seg_total"):
+                assert np.array_equal(getattr(x, key), getattr(y, key)), key
+        elif isinstance(x, np.ndarray):
+            assert np.allclose(x, y, rtol=1e-9, atol=0)
+        else:
+            assert x == y

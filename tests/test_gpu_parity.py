@@ -349,15 +349,24 @@ def test_pipelined_host_inputs_match_device_inputs():
     dev = MeshTally(m, n)
     host.initialize_particle_location(pos)
     dev.initialize_particle_location(torch.from_numpy(pos).cuda())
-    s1 = host.move_to_next_location(dest, fly, w)
-    s2 = dev.move_to_next_location(torch.from_numpy(dest).cuda(), torch.from_numpy(fly).cuda(),
-                                   torch.from_numpy(w).cuda())
-    assert s1 == s2
-    a, b = host.read_particles(), dev.read_particles()
-    for k in ("position", "element", "alive", "entry_face", "stuck", "outcome", "seg_total"):
-        assert np.array_equal(getattr(a, k), getattr(b, k)), k
-    assert rel_close(host.batch_totals(), dev.batch_totals(), TALLY_RTOL)[0]
-    assert host.source_weight == w[fly != 0].sum()
+    # two chained moves: the second one's input buffers on the device still
+    # hold the first move's values, so a walk chunk that started before its
+    # own inputs landed would show up as a mismatch
+    for move in range(2):
+        s1 = host.move_to_next_location(dest, fly, w)
+        s2 = dev.move_to_next_location(torch.from_numpy(dest).cuda(),
+                                       torch.from_numpy(fly).cuda(), torch.from_numpy(w).cuda())
+        assert s1 == s2
+        a, b = host.read_particles(), dev.read_particles()
+        for k in ("position", "element", "alive", "entry_face", "stuck", "outcome", "seg_total"):
+            assert np.array_equal(getattr(a, k), getattr(b, k)), (move, k)
+        assert rel_close(host.batch_totals(), dev.batch_totals(), TALLY_RTOL)[0]
+        assert host.source_weight == w[fly != 0].sum()
+        if move == 0:
+            dest = synth.flight_destinations(gen, a.position, 5.0)
+            fly = a.alive.astype(np.int8)
+            w = 0.5 + gen.random(n)
+            host.source_weight = dev.source_weight = 0.0  # record the second move too
     host.close()
     dev.close()
 
