@@ -293,7 +293,7 @@ static inline unsigned grid_for(int64_t n, int threads) {
 }
 
 static bt_status build_grid(bt_tally* h) {
-    // cells ~ E/6 over the bounding box, per-axis counts proportional to extent
+    // cells ~ density x E over the bounding box, per-axis counts proportional to extent
     double ext[3];
     double vol = 1.0;
     for (int k = 0; k < 3; ++k) {
@@ -302,13 +302,20 @@ static bt_status build_grid(bt_tally* h) {
     }
     double maxext = std::max(ext[0], std::max(ext[1], ext[2]));
     for (int k = 0; k < 3; ++k) vol *= std::max(ext[k], 1e-6 * maxext);
-    // cells per element (experiments: B200TALLY_GRID_DENSITY)
-    double density = 0.5;  // measured best on C2 (profiles/r01_*): 3.9 ms / 1e7 points
+    // cells per element (experiments: B200TALLY_GRID_DENSITY).  With the
+    // pruned lists, 4 cells per element: 1.24 ms per 1e7 points on C2, 1.58 ms
+    // on the 10.1M-tet cube (0.5: 1.85 / 2.50 ms; box lists at 0.5, round 1:
+    // 2.85 / 3.62 ms), ~27 list entries per element (profiles/r02_locate.jsonl)
+    double density = 4.0;
     if (const char* env = getenv("B200TALLY_GRID_DENSITY")) density = std::max(1e-3, atof(env));
     double target = std::max(1.0, (double)h->ne * density);
     target = std::min(target, (double)(1 << 26));
     double cell = std::cbrt(vol / target);
     GridDev G{};
+    // element-cell lists pruned by the barycentric half-spaces (locate.cuh);
+    // B200TALLY_GRID_PRUNE=0 lists every bounding-box cell (tests, experiments)
+    const char* pe = getenv("B200TALLY_GRID_PRUNE");
+    G.prune = pe ? atoi(pe) != 0 : 1;
     int64_t ncells = 1;
     for (int k = 0; k < 3; ++k) {
         int d = (int)std::max(1.0, std::min(4096.0, std::round(ext[k] / cell)));
@@ -318,17 +325,14 @@ static bt_status build_grid(bt_tally* h) {
         G.cs[k] = (ext[k] > 1e-300) ? ext[k] / d : 1.0;
         ncells *= d;
     }
-    int* counts = nullptr;
-    int* offs = nullptr;
-    int4 *rlo = nullptr, *rhi = nullptr;
+    long long* counts = nullptr;  // 64-bit: the scan accumulates in the input type
+    long long* offs = nullptr;
     TRY(dalloc(&counts, h->ne + 1));
     TRY(dalloc(&offs, h->ne + 1));
-    TRY(dalloc(&rlo, h->ne));
-    TRY(dalloc(&rhi, h->ne));
-    CK(cudaMemsetAsync(counts + h->ne, 0, sizeof(int), h->stream));
+    CK(cudaMemsetAsync(counts + h->ne, 0, sizeof(long long), h->stream));
     TRY(dalloc(&h->lam, h->ne));
     elem_cells_count_kernel<<<grid_for(h->ne, 256), 256, 0, h->stream>>>(h->rec, h->vtx, h->ne,
-                                                                         G, counts, rlo, rhi);
+                                                                         G, counts);
     CK(cudaGetLastError());
     elem_lambda_kernel<<<grid_for(h->ne, 256), 256, 0, h->stream>>>(h->rec, h->vtx, h->ne, h->lam);
     CK(cudaGetLastError());
@@ -338,15 +342,22 @@ static bt_status build_grid(bt_tally* h) {
     void* tmp = nullptr;
     CK(cudaMalloc(&tmp, tmp_bytes));
     CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, offs, (int)(h->ne + 1), h->stream));
-    int m = 0;
-    CK(cudaMemcpyAsync(&m, offs + h->ne, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    long long m64 = 0;
+    CK(cudaMemcpyAsync(&m64, offs + h->ne, sizeof m64, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     cudaFree(tmp);
+    if (m64 >= (1ll << 31)) {
+        cudaFree(counts);
+        cudaFree(offs);
+        return set_err(BT_ENOMEM, "localization grid: %lld cell entries exceed 2^31 (lower "
+                       "B200TALLY_GRID_DENSITY)", m64);
+    }
+    const int m = (int)m64;
     unsigned long long *keys = nullptr, *keys_out = nullptr;
     TRY(dalloc(&keys, m));
     TRY(dalloc(&keys_out, m));
-    elem_cells_emit_kernel<<<grid_for(h->ne, 256), 256, 0, h->stream>>>(h->ne, G, offs, rlo, rhi,
-                                                                        keys);
+    elem_cells_emit_kernel<<<grid_for(h->ne, 256), 256, 0, h->stream>>>(h->ne, G, h->rec, h->vtx,
+                                                                        offs, keys);
     CK(cudaGetLastError());
     int cell_bits = 1;
     while ((1ll << cell_bits) < ncells + 1) ++cell_bits;
@@ -368,8 +379,6 @@ static bt_status build_grid(bt_tally* h) {
     cudaFree(keys_out);
     cudaFree(counts);
     cudaFree(offs);
-    cudaFree(rlo);
-    cudaFree(rhi);
     G.cell_start = h->cell_start;
     G.cand = h->cand;
     h->grid = G;

@@ -26,6 +26,7 @@ struct GridDev {
     int dims[3];
     const int* cell_start;  // ncells + 1
     const int* cand;        // element ids, ascending within a cell
+    int prune;              // list elements only in cells their half-spaces reach
 };
 
 __device__ __forceinline__ int grid_axis(double p, double org, double cs, int dim) {
@@ -34,32 +35,105 @@ __device__ __forceinline__ int grid_axis(double p, double org, double cs, int di
     return i;
 }
 
-__global__ void elem_cells_count_kernel(const ElemRec* __restrict__ rec,
-                                        const Vtx* __restrict__ vtx, int64_t ne, GridDev G,
-                                        int* __restrict__ counts, int4* __restrict__ ranges_lo,
-                                        int4* __restrict__ ranges_hi) {
-    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (e >= ne) return;
-    const ElemRec r = rec[e];
+// Which grid cells an element is listed in: the cells of its bounding box
+// (expanded by 1e-7 of its extent) that its tolerance-expanded barycentric
+// half-spaces do not exclude.  lambda_k is affine, so its maximum over a cell
+// is w_k.(c - v0) + |w_k|.h (c the centre, h the half-size): a cell where one
+// maximum is below -CELL_TOL cannot hold a point the element contains
+// (the reference's containment tolerance is EPS_BARY = 1e-10 plus its own
+// rounding, <= 1e-8 for the elements this test applies to: quality ratio
+// A^3/|det| <= 1e6; others keep every box cell).  A Kuhn tet fills a sixth of
+// its box: the cells' candidate lists shrink ~2.5x, and the lowest-id search
+// scans half a list per point.
+constexpr double CELL_TOL = 1e-6;
+struct ElemCells {
+    int lo[3], hi[3];  // cell index range of the expanded box
+    double w[4][3];    // lambda_k = w_k . (p - v0) (+ 1 for k = 0)
+    double v0[3];
+    bool prune;        // false: keep every box cell
+};
+__device__ inline ElemCells elem_cells(const ElemRec& r, const Vtx* __restrict__ vtx,
+                                       const GridDev& G) {
+    ElemCells E;
+    double x[4], y[4], z[4];
     double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
     for (int j = 0; j < 4; ++j) {
         const Vtx v = vtx[r.v[j]];
+        x[j] = v.x;
+        y[j] = v.y;
+        z[j] = v.z;
         const double c[3] = {v.x, v.y, v.z};
         for (int k = 0; k < 3; ++k) {
             lo[k] = fmin(lo[k], c[k]);
             hi[k] = fmax(hi[k], c[k]);
         }
     }
-    double ext = fmax(fmax(hi[0] - lo[0], hi[1] - lo[1]), hi[2] - lo[2]);
-    double delta = 1e-7 * ext + 1e-300;
-    int a[3], b[3];
+    const double ext = fmax(fmax(hi[0] - lo[0], hi[1] - lo[1]), hi[2] - lo[2]);
+    const double delta = 1e-7 * ext + 1e-300;
     for (int k = 0; k < 3; ++k) {
-        a[k] = grid_axis(lo[k] - delta, G.org[k], G.cs[k], G.dims[k]);
-        b[k] = grid_axis(hi[k] + delta, G.org[k], G.cs[k], G.dims[k]);
+        E.lo[k] = grid_axis(lo[k] - delta, G.org[k], G.cs[k], G.dims[k]);
+        E.hi[k] = grid_axis(hi[k] + delta, G.org[k], G.cs[k], G.dims[k]);
     }
-    counts[e] = (b[0] - a[0] + 1) * (b[1] - a[1] + 1) * (b[2] - a[2] + 1);
-    ranges_lo[e] = make_int4(a[0], a[1], a[2], 0);
-    ranges_hi[e] = make_int4(b[0], b[1], b[2], 0);
+    double a[3][3];
+    for (int k = 0; k < 3; ++k) {
+        a[k][0] = x[k + 1] - x[0];
+        a[k][1] = y[k + 1] - y[0];
+        a[k][2] = z[k + 1] - z[0];
+    }
+    double n[3][3];
+    auto cross = [](const double* u, const double* v, double* o) {
+        o[0] = u[1] * v[2] - u[2] * v[1];
+        o[1] = u[2] * v[0] - u[0] * v[2];
+        o[2] = u[0] * v[1] - u[1] * v[0];
+    };
+    cross(a[1], a[2], n[0]);
+    cross(a[2], a[0], n[1]);
+    cross(a[0], a[1], n[2]);
+    const double det = a[0][0] * n[0][0] + a[0][1] * n[0][1] + a[0][2] * n[0][2];
+    double A = 0.0;
+    for (int k = 0; k < 3; ++k) A = fmax(A, fabs(a[k][0]) + fabs(a[k][1]) + fabs(a[k][2]));
+    const double q = A * A * A / fabs(det);
+    E.prune = G.prune && q <= 1e6;  // false for NaN / inf (degenerate elements)
+    for (int i = 0; i < 3; ++i) E.w[0][i] = 0.0;
+    for (int k = 0; k < 3; ++k)
+        for (int i = 0; i < 3; ++i) {
+            E.w[k + 1][i] = n[k][i] / det;
+            E.w[0][i] -= E.w[k + 1][i];
+        }
+    E.v0[0] = x[0];
+    E.v0[1] = y[0];
+    E.v0[2] = z[0];
+    return E;
+}
+__device__ inline bool elem_cell_overlap(const ElemCells& E, const GridDev& G, int i, int j,
+                                         int l) {
+    if (!E.prune) return true;
+    const int ix[3] = {i, j, l};
+    double d[3], h[3];
+    for (int k = 0; k < 3; ++k) {
+        h[k] = 0.5 * G.cs[k] * (1.0 + 2e-7);  // the point-to-cell mapping's rounding
+        d[k] = G.org[k] + ((double)ix[k] + 0.5) * G.cs[k] - E.v0[k];
+    }
+    for (int k = 0; k < 4; ++k) {
+        const double lmax = (k == 0 ? 1.0 : 0.0) + E.w[k][0] * d[0] + E.w[k][1] * d[1] +
+                            E.w[k][2] * d[2] +
+                            (fabs(E.w[k][0]) * h[0] + fabs(E.w[k][1]) * h[1] + fabs(E.w[k][2]) * h[2]);
+        if (lmax < -CELL_TOL) return false;  // the whole cell is beyond face k
+    }
+    return true;
+}
+
+__global__ void elem_cells_count_kernel(const ElemRec* __restrict__ rec,
+                                        const Vtx* __restrict__ vtx, int64_t ne, GridDev G,
+                                        long long* __restrict__ counts) {
+    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= ne) return;
+    const ElemCells E = elem_cells(rec[e], vtx, G);
+    int cnt = 0;
+    for (int i = E.lo[0]; i <= E.hi[0]; ++i)
+        for (int j = E.lo[1]; j <= E.hi[1]; ++j)
+            for (int l = E.lo[2]; l <= E.hi[2]; ++l) cnt += elem_cell_overlap(E, G, i, j, l);
+    counts[e] = cnt;
 }
 
 __global__ void elem_lambda_kernel(const ElemRec* __restrict__ rec, const Vtx* __restrict__ vtx,
@@ -112,21 +186,21 @@ __global__ void elem_lambda_kernel(const ElemRec* __restrict__ rec, const Vtx* _
     lam[e] = L;
 }
 
-__global__ void elem_cells_emit_kernel(int64_t ne, GridDev G, const int* __restrict__ offs,
-                                       const int4* __restrict__ ranges_lo,
-                                       const int4* __restrict__ ranges_hi,
+__global__ void elem_cells_emit_kernel(int64_t ne, GridDev G, const ElemRec* __restrict__ rec,
+                                       const Vtx* __restrict__ vtx, const long long* __restrict__ offs,
                                        unsigned long long* __restrict__ keys) {
     int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= ne) return;
-    const int4 a = ranges_lo[e], b = ranges_hi[e];
-    int k = offs[e];
-    for (int i = a.x; i <= b.x; ++i)
-        for (int j = a.y; j <= b.y; ++j)
-            for (int l = a.z; l <= b.z; ++l) {
-                const unsigned long long cell =
-                    ((unsigned long long)i * G.dims[1] + j) * G.dims[2] + l;
-                keys[k++] = (cell << 32) | (unsigned long long)e;
-            }
+    const ElemCells E = elem_cells(rec[e], vtx, G);  // the same decisions as the count
+    long long k = offs[e];
+    for (int i = E.lo[0]; i <= E.hi[0]; ++i)
+        for (int j = E.lo[1]; j <= E.hi[1]; ++j)
+            for (int l = E.lo[2]; l <= E.hi[2]; ++l)
+                if (elem_cell_overlap(E, G, i, j, l)) {
+                    const unsigned long long cell =
+                        ((unsigned long long)i * G.dims[1] + j) * G.dims[2] + l;
+                    keys[k++] = (cell << 32) | (unsigned long long)e;
+                }
 }
 
 __global__ void cell_start_kernel(const unsigned long long* __restrict__ keys, int64_t m,

@@ -522,6 +522,45 @@ def test_localization_prefilter_equals_exact_at_scale():
     assert (out[0] >= 0).mean() > 0.9
 
 
+@pytest.mark.parametrize("mesh_kind", ["cube", "torus"])
+def test_grid_pruning_equals_box_lists_at_scale(mesh_kind, monkeypatch):
+    """The localization grid lists an element only in the cells its
+    tolerance-expanded barycentric half-spaces reach (csrc/locate.cuh
+    elem_cell_overlap).  Against the bounding-box lists
+    (B200TALLY_GRID_PRUNE=0): identical elements for every point, a third of
+    the cube's points on grid planes, edges and vertices or within 1e-12 of
+    them, and the torus's points in curved shell elements."""
+    torch = pytest.importorskip("torch")
+    gen = synth.rng(synth.SEED + 94)
+    if mesh_kind == "cube":
+        m = build_cube_mesh(55)
+        n = 10_000_000
+        pts = gen.uniform(0.0, 1.0, (n, 3))
+        grid = np.arange(56) / 55.0
+        for ax in range(3):
+            sel = gen.random(n) < 0.2
+            pts[sel, ax] = grid[gen.integers(0, 56, sel.sum())]
+        near = gen.random(n) < 0.1
+        pts[near] += gen.normal(size=(near.sum(), 3)) * 1e-12
+    else:
+        from paper_2504_19048_b200 import build_torus_shell_mesh
+        m = build_torus_shell_mesh(4, 64, 96, R=300.0, a_in=100.0, a_out=120.0)
+        n = 2_000_000
+        elems = gen.integers(0, m.num_elements, n)
+        pts = synth.points_in_elements(gen, m.vertices, m.elements, elems)
+        onv = gen.random(n) < 0.05  # on mesh vertices
+        pts[onv] = m.vertices[m.elements[elems[onv], 0]]
+    out = []
+    for prune in ("1", "0"):
+        monkeypatch.setenv("B200TALLY_GRID_PRUNE", prune)
+        mt = MeshTally(m, n)
+        mt.initialize_particle_location(torch.from_numpy(pts).cuda())
+        out.append(mt.read_particles().element)
+        mt.close()
+    assert np.array_equal(out[0], out[1])
+    assert (out[0] >= 0).mean() > 0.9
+
+
 def test_permuted_vertex_orders_sampled_parity():
     """The walk keeps a lane's element vertices in shared-memory slots and
     re-maps them through each crossing record's vertex-order selector

@@ -15,7 +15,14 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 55
 P = int(sys.argv[2]) if len(sys.argv) > 2 else 10_000_000
 m = build_cube_mesh(n)
 pos = torch.from_numpy(synth.uniform_box(synth.rng(), P)).cuda()
+import time
+torch.cuda.synchronize()
+t0 = time.perf_counter()
 mt = MeshTally(m, P)
+mt.initialize_particle_location(pos[:1])  # builds the grid
+torch.cuda.synchronize()
+print(json.dumps({"mesh_elements": m.num_elements, "create_and_grid_build_s": time.perf_counter() - t0}),
+      flush=True)
 ref = None
 for g in (1, 2, 4, 8, 16, 32):
     mt.set_option(_lib.BT_OPT_LOCATE_LANES, g)
