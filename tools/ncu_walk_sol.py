@@ -2,7 +2,10 @@
 --set full report of the bench's walk kernel -> profiles/walk_sol.json (read
 by bench.py to build its `roofline` block from the live kernel time).
 
-    python tools/ncu_walk_sol.py gpurun_out/walk_full.ncu-rep CROSSINGS_PER_LAUNCH [NOTE]
+    python tools/ncu_walk_sol.py gpurun_out/walk_full.ncu-rep CROSSINGS_PER_LAUNCH [NOTE] [OUT]
+
+OUT (default walk_sol.json) names the file under profiles/; the transport
+kernel's capture goes to transport_sol.json (CROSSINGS = the batch's events).
 
 CROSSINGS_PER_LAUNCH is the TraceSummary.events of the captured move (the
 bench move: 569,602,285 on C2 with 1e7 particles, sigma_t = 2).
@@ -21,7 +24,7 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "":
          "ns": 1e-9, "s": 1, "Ghz": 1e9, "Mhz": 1e6, "Khz": 1e3, "hz": 1}
 
 
-def main(rep, crossings, note=""):
+def main(rep, crossings, note="", out_name="walk_sol.json"):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -61,7 +64,7 @@ def main(rep, crossings, note=""):
         "occupancy_warps_per_sm": get("sm__warps_active.avg.per_cycle_active"),
         "registers": get("launch__registers_per_thread"),
     }
-    (ROOT / "profiles" / "walk_sol.json").write_text(json.dumps(out, indent=1) + "\n")
+    (ROOT / "profiles" / out_name).write_text(json.dumps(out, indent=1) + "\n")
     print(json.dumps(out, indent=1))
 
 

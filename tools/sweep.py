@@ -7,7 +7,8 @@
       multi-move batches chained on the device (dest = pos + l*dir, flying = alive)
 
 Timing: CUDA events around each move on the library stream (walk kernel) and
-around the whole batch on the torch stream; inputs device-resident.
+around the whole batch (localization + moves + finalize) on the torch stream;
+inputs device-resident and generated before the timed region.
 """
 
 from __future__ import annotations
@@ -38,7 +39,11 @@ def flights_torch(torch, n, gen, dev, sigma_t):
 
 
 def run_point(mesh, positions, sigma_t, moves, label, warm=1, chain=False, **mt_kw):
-    """positions: device tensor (N,3).  One batch = init + `moves` moves."""
+    """positions: device tensor (N,3).  One batch = init + `moves` moves.  The
+    moves' destinations are generated before the timed region (a chained
+    move continues from the previous destination, which is where a particle
+    that reached it stands, bit for bit; `flying` = the library's alive flags),
+    so the batch time is the library's alone."""
     import torch
     from paper_2504_19048_b200 import MeshTally
     dev = positions.device
@@ -48,24 +53,29 @@ def run_point(mesh, positions, sigma_t, moves, label, warm=1, chain=False, **mt_
     gen.manual_seed(20261017)
     fly = torch.ones(n, dtype=torch.int8, device=dev)
     w = torch.ones(n, dtype=torch.float64, device=dev)
+    dests = []
+    cur = positions
+    for k in range(moves):
+        d = (cur + flights_torch(torch, n, gen, dev, sigma_t)[:, None] *
+             iso_dirs_torch(torch, n, gen, dev)).contiguous()
+        dests.append(d)
+        if chain:
+            cur = d
 
-    def batch(record):
-        mt.initialize_particle_location(positions)
-        pos_t, _, alive_t = mt.particle_tensors()
-        ev = mv = 0
-        walk = 0.0
+    def batch():
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         t0.record()
+        mt.initialize_particle_location(positions)
+        _, _, alive_t = mt.particle_tensors()
+        ev = mv = 0
+        walk = 0.0
         for k in range(moves):
-            dest = pos_t + flights_torch(torch, n, gen, dev, sigma_t)[:, None] * \
-                iso_dirs_torch(torch, n, gen, dev)
             f = alive_t.clone() if chain else fly
-            nf = int(f.sum().item())  # also in the warm-up batch (first-use kernel loads)
-            s = mt.move_to_next_location(dest.contiguous(), f, w)
+            s = mt.move_to_next_location(dests[k], f, w)
             ev += s.events
-            mv += nf
+            mv += s.reached + s.boundary_exits + s.stuck_terminations  # the flying count
             walk += mt.last_timing()[0]
         mt.finalize_batch()
         t1.record()
@@ -73,8 +83,8 @@ def run_point(mesh, positions, sigma_t, moves, label, warm=1, chain=False, **mt_
         return ev, mv, walk, t0.elapsed_time(t1)
 
     for _ in range(warm):
-        batch(False)
-    ev, mv, walk_ms, batch_ms = batch(True)
+        batch()
+    ev, mv, walk_ms, batch_ms = batch()
     out = {"point": label, "elements": mesh.num_elements, "particles": n, "moves": moves,
            "sigma_t": sigma_t, "crossings": ev, "particle_moves": mv,
            "crossings_per_move": ev / max(mv, 1),
