@@ -302,6 +302,12 @@ bt_status bt_read_transport_state(bt_tally *h, int64_t count, double *direction,
  * (4 x u64 each) -> 4n doubles (philox KAT hook). */
 bt_status bt_uniform_blocks(const uint64_t *keys, int64_t n, int32_t device, double *out);
 
+/* The transport's log (fn 0), sin (1), cos (2) on the device for n arguments:
+ * the restatement of the host libm the reference calls (csrc/glibc_math.cuh;
+ * self-test hook).  BT_EINVAL when the library was built without the host
+ * libm tables. */
+bt_status bt_glibc_math(const double *x, int64_t n, int32_t fn, int32_t device, double *out);
+
 /* ---- standalone tally grids and scoring (tally.py:21-80) ---------------- */
 
 /* create_grid(num_elements, num_groups): a tally-only handle (no mesh, no

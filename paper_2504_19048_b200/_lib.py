@@ -35,7 +35,7 @@ EXPORTS = (
     "bt_batches_completed", "bt_read_particles", "bt_read_digest", "bt_set_option",
     "bt_last_timing", "bt_particle_device_ptrs", "bt_save_state", "bt_restore_state",
     "bt_info", "bt_build_adjacency", "bt_transport_run", "bt_read_transport_state",
-    "bt_uniform_blocks", "bt_load_step", "bt_trace_begin", "bt_trace_propose",
+    "bt_uniform_blocks", "bt_glibc_math", "bt_load_step", "bt_trace_begin", "bt_trace_propose",
     "bt_trace_commit", "bt_trace_end", "bt_memcpy", "bt_flux",
     "bt_create_grid", "bt_score", "bt_write_tally", "bt_set_batches_completed",
     "bt_mesh_read", "bt_mesh_from_arrays", "bt_mesh_info", "bt_mesh_arrays", "bt_mesh_destroy",
@@ -97,6 +97,7 @@ _SIGS = {
                          C.POINTER(TransportTotals)],
     "bt_read_transport_state": [_P, _I64, _P, _P, _P],
     "bt_uniform_blocks": [_P, _I64, _I32, _P],
+    "bt_glibc_math": [_P, _I64, _I32, _I32, _P],
     "bt_load_step": [_P, _P, _P, _P, _P, _I64, _I32],
     "bt_trace_begin": [_P, _I32, _I64],
     "bt_trace_propose": [_P, C.POINTER(SweepEventsC), C.POINTER(_I64)],

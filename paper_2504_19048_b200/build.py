@@ -15,7 +15,8 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 SRC = PKG / "csrc" / "b200tally.cu"
-DEPS = [SRC, *sorted((PKG / "csrc").glob("*.cuh")), ROOT / "include" / "b200tally.h"]
+DEPS = [SRC, *sorted((PKG / "csrc").glob("*.cuh")), PKG / "csrc" / "glibc_tables.inc",
+        ROOT / "include" / "b200tally.h"]
 LIB = PKG / "libb200tally.so"
 
 NVCC_FLAGS = [
@@ -40,7 +41,18 @@ def needs_build() -> bool:
     return any(d.stat().st_mtime > t for d in DEPS)
 
 
+TABLES = PKG / "csrc" / "glibc_tables.inc"
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
+    # the host libm's log / sin / cos tables for the transport (not committed;
+    # rewritten only when they change, so an unchanged build stays up to date)
+    try:
+        from . import glibc_tables
+    except ImportError:  # run as a script
+        sys.path.insert(0, str(PKG))
+        import glibc_tables
+    glibc_tables.generate(TABLES)
     if not force and not needs_build():
         return LIB
     cmd = [nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), "-o", str(LIB), str(SRC)]

@@ -71,6 +71,7 @@ static bt_status set_err(bt_status s, const char* fmt, ...) {
 
 #include "layout.cuh"
 #include "walk.cuh"
+#include "glibc_math.cuh"
 #include "transport.cuh"
 #include "sweep.cuh"
 #include "locate.cuh"
@@ -1948,6 +1949,40 @@ bt_status bt_uniform_blocks(const uint64_t* keys, int64_t n, int32_t device, dou
     cudaFree(dk);
     cudaFree(dout);
     if (e != cudaSuccess) return set_err(BT_ECUDA, "philox: %s", cudaGetErrorString(e));
+    return BT_OK;
+}
+
+__global__ void glibc_math_kernel(const double* __restrict__ x, int64_t n, int fn,
+                                  double* __restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+#if BT_GLIBC_MATH
+    if (i >= n) return;
+    out[i] = fn == 0 ? gm_log(x[i]) : fn == 1 ? gm_sin(x[i]) : gm_cos(x[i]);
+#else
+    if (i >= n) return;
+    out[i] = fn == 0 ? log(x[i]) : fn == 1 ? sin(x[i]) : cos(x[i]);
+#endif
+}
+
+bt_status bt_glibc_math(const double* x, int64_t n, int32_t fn, int32_t device, double* out) {
+    if (!BT_GLIBC_MATH)
+        return set_err(BT_EINVAL, "built without the host libm tables (BT_GLIBC_MATH 0)");
+    if (fn < 0 || fn > 2) return set_err(BT_EINVAL, "fn must be 0 (log), 1 (sin) or 2 (cos)");
+    if (n <= 0) return BT_OK;
+    if (!x || !out) return set_err(BT_EINVAL, "NULL argument");
+    CK(cudaSetDevice(device));
+    double *dx = nullptr, *dout = nullptr;
+    CK(cudaMalloc(&dx, sizeof(double) * n));
+    CK(cudaMalloc(&dout, sizeof(double) * n));
+    cudaError_t e = cudaMemcpy(dx, x, sizeof(double) * n, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        glibc_math_kernel<<<grid_for(n, 256), 256>>>(dx, n, fn, dout);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(out, dout, sizeof(double) * n, cudaMemcpyDeviceToHost);
+    cudaFree(dx);
+    cudaFree(dout);
+    if (e != cudaSuccess) return set_err(BT_ECUDA, "glibc math: %s", cudaGetErrorString(e));
     return BT_OK;
 }
 

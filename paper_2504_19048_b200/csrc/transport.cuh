@@ -46,6 +46,25 @@ __global__ void philox_kat_kernel(const uint64_t* __restrict__ keys, int64_t n,
     uniform_block(keys[4 * i], keys[4 * i + 1], keys[4 * i + 2], keys[4 * i + 3], out + 4 * i);
 }
 
+// The reference's np.log / np.cos / np.sin are the host libm's: with its
+// tables available (BT_GLIBC_MATH, glibc_math.cuh) the device evaluates the
+// same operation sequences and every history is the reference's bit for bit;
+// otherwise CUDA's functions (last-bit differences: statistical parity only).
+__device__ __forceinline__ double tr_log(double x) {
+#if BT_GLIBC_MATH
+    return gm_log(x);
+#else
+    return log(x);
+#endif
+}
+__device__ __forceinline__ void tr_sincos(double phi, double* sp, double* cp) {
+#if BT_GLIBC_MATH
+    gm_sincos_simt(phi, sp, cp);
+#else
+    sincos(phi, sp, cp);
+#endif
+}
+
 // isotropic direction from two uniforms (transport.py:172-178, 255-261)
 __device__ __forceinline__ void iso_dir(double ua, double ub, double& x, double& y, double& z) {
     const double mu = __dsub_rn(__dmul_rn(2.0, ua), 1.0);
@@ -53,7 +72,7 @@ __device__ __forceinline__ void iso_dir(double ua, double ub, double& x, double&
     const double t = __dsub_rn(1.0, __dmul_rn(mu, mu));
     const double s = __dsqrt_rn(t > 0.0 ? t : 0.0);
     double sp, cp;
-    sincos(phi, &sp, &cp);
+    tr_sincos(phi, &sp, &cp);
     x = __dmul_rn(s, cp);
     y = __dmul_rn(s, sp);
     z = mu;
@@ -192,7 +211,7 @@ __global__ void __launch_bounds__(THREADS, MINB) transport_kernel(const Transpor
                 double u[4];
                 uniform_block(t.seed, t.batch, (uint64_t)L.idx(), rb, u);
                 ++rb;
-                const double lc = __ddiv_rn(-log(u[0]), t.xs.sigma_t[L.g()]);
+                const double lc = __ddiv_rn(-tr_log(u[0]), t.xs.sigma_t[L.g()]);
                 L.dx() = __dadd_rn(L.px, __dmul_rn(lc, ux));
                 L.dy() = __dadd_rn(L.py, __dmul_rn(lc, uy));
                 L.dz() = __dadd_rn(L.pz, __dmul_rn(lc, uz));

@@ -351,3 +351,33 @@ def test_deferred_initialize_paths(pinned):
             assert np.allclose(x, y, rtol=1e-9, atol=0)
         else:
             assert x == y
+
+
+def test_device_libm_restatement_equals_host_libm():
+    """bt_glibc_math (csrc/glibc_math.cuh on the device) against the host
+    libm the reference calls, bit for bit: 3e5 transport arguments per
+    function plus the branch thresholds' neighbourhoods."""
+    import ctypes
+    from paper_2504_19048_b200 import _lib
+    L = _lib.load()
+    libm = ctypes.CDLL("libm.so.6")
+    fns = []
+    for name in ("log", "sin", "cos"):
+        f = getattr(libm, name)
+        f.restype, f.argtypes = ctypes.c_double, [ctypes.c_double]
+        fns.append(f)
+    gen = np.random.default_rng(77)
+    u = (np.floor(gen.random(300_000) * 2.0**53) + 1.0) / 2.0**53
+    edges = np.array([0.126, 0.855469, 2.426265, np.pi / 2, np.pi, 1.5 * np.pi, 2 * np.pi])
+    near = (edges[:, None] * (1.0 + np.linspace(-1e-9, 1e-9, 2001))[None, :]).reshape(-1)
+    args = {0: np.concatenate([u, 0.9375 + 0.125 * u[:50_000], [1.0]]),
+            1: np.concatenate([2 * np.pi * u, near]), 2: np.concatenate([2 * np.pi * u, near])}
+    for fn, x in args.items():
+        x = np.ascontiguousarray(x)
+        out = np.empty_like(x)
+        st = L.bt_glibc_math(x.ctypes.data, x.size, fn, 0, out.ctypes.data)
+        if st != 0:
+            pytest.skip("library built without the host libm tables")
+        want = np.array([fns[fn](float(v)) for v in x])
+        bad = np.nonzero(out.view(np.uint64) != want.view(np.uint64))[0]
+        assert bad.size == 0, (fn, x[bad[:5]], out[bad[:5]], want[bad[:5]])

@@ -1,19 +1,21 @@
-"""Device transport (bt_transport_run) vs the CPU oracle, which is pinned
-bit-exact to the reference's transport.run (tests/test_transport_oracle.py).
+"""Device transport (bt_transport_run) vs the reference's transport.run
+(golden fixtures) and the CPU oracle, which is pinned bit-exact to it
+(tests/test_transport_oracle.py).
 
 * philox4x64-10 uniforms: bit-exact.
-* Histories: identical sequence of operations; they stay bit-identical
-  until a CUDA log/sin/cos result differs from the host libm in the last
-  bit.  The fraction of bit-identical particle histories is measured and
-  must be high; everything else is compared statistically, with bounds
-  from the runs' own variance: per-history PAIRED differences (device minus
-  reference, same particle, same random stream) of the history's track
-  length, random blocks consumed (2 per collision + 2 per history) and
-  outcome.  Identical histories contribute 0; a diverged history continues
-  as an independent draw from the same process, so an unbiased device has
-  E[difference] = 0 and the mean difference must lie within K standard
-  errors of 0 -- a 1% bias in the collision rate or the scatter sampling
-  fails this at the sizes below, where a flat 5% bound would not.
+* Histories: the same sequence of operations, and -- with the host libm's
+  log / sin / cos restated on the device (csrc/glibc_math.cuh, tables read
+  from this image's glibc at build time) -- the same bits:
+  test_transport_bit_exact_vs_reference requires every particle's final
+  state, the event / collision / sweep counts and the balance weights to be
+  the reference's exactly, the fluxes within 1e-9.
+* A build without those tables (another libm) falls back to CUDA's
+  functions; histories then diverge after a last-bit difference, and the
+  statistical tests below carry the parity: per-history PAIRED differences
+  (device minus reference, same particle, same random stream) of track
+  length, random blocks consumed and outcome must have mean 0 within K
+  standard errors (a 1% bias in the collision rate or the scatter sampling
+  fails this at the sizes below).  With the tables they see 0 differences.
 """
 
 import numpy as np
@@ -27,6 +29,13 @@ from paper_2504_19048_b200 import transport as T
 pytestmark = pytest.mark.gpu
 
 K = 4.0  # standard errors
+
+
+def _exact_math():
+    """The library carries the host libm restatement (bit-exact histories)."""
+    from paper_2504_19048_b200 import _lib
+    x = np.array([0.5])
+    return _lib.load().bt_glibc_math(x.ctypes.data, 1, 0, 0, x.ctypes.data) == 0
 
 
 def _paired_ok(a, b, what):
@@ -94,7 +103,7 @@ def test_transport_statistical_parity(gold, name):
     print(f"{name}: bit-identical histories {frac:.4f}; collisions {r.collisions} vs "
           f"{int(gold[p + 'collisions'])}; leaked {r.leaked_weight} vs "
           f"{float(gold[p + 'leaked_weight'])}")
-    assert frac > 0.5
+    assert frac == 1.0 if _exact_math() else frac > 0.5
     # balance: every source particle leaks, is absorbed or stuck-killed
     assert r.leaked_weight + r.absorbed_weight + r.stuck_weight == r.source_weight
     # per-history paired differences (last batch) and the run totals
@@ -121,6 +130,39 @@ def test_transport_statistical_parity(gold, name):
         assert abs(a - c) <= K * se, (a, c, se)
 
 
+@pytest.mark.parametrize("name", ["t1g", "t2g", "tdir"])
+def test_transport_bit_exact_vs_reference(gold, name):
+    """With the host libm's log / sin / cos restated on the device
+    (csrc/glibc_math.cuh) every history is the reference's: final state of
+    every particle (position, direction, element, group, outcome, RNG block
+    counter, track length) bit for bit, the same collision and event counts,
+    balance weights equal, flux of both estimators within 1e-9 (atomic
+    summation order)."""
+    if not _exact_math():
+        pytest.skip("library built without the host libm tables")
+    p = name + "_"
+    cfg = _cfg(gold, name)
+    m = build_cube_mesh(cfg.mesh_n)
+    r = T.run(cfg, m)
+    fs = r.final_state
+    for key in ("position", "direction", "element", "group", "outcome", "alive", "rng_block"):
+        a, b = fs[key], gold[p + "final_" + key]
+        assert np.array_equal(a, b), key
+    if p + "final_seg_total" in gold:
+        assert np.array_equal(fs["seg_total"], gold[p + "final_seg_total"])
+    for k in ("collisions", "events", "sweeps"):
+        assert getattr(r, k) == int(gold[p + k]), k
+    for k in ("source_weight", "leaked_weight", "absorbed_weight", "stuck_weight"):
+        assert getattr(r, k) == float(gold[p + k]), k  # sums of unit weights: exact
+    tl = float(gold[p + "track_length_total"])
+    assert abs(r.track_length_total - tl) <= 1e-12 * tl
+    for est, key in (("flux_track", "flux_track_mean"), ("flux_collision", "flux_col_mean")):
+        a = getattr(r, est).mean.reshape(-1)
+        b = gold[p + key].reshape(-1)
+        den = np.maximum(np.abs(a), np.abs(b))
+        assert (np.abs(a - b) <= 1e-9 * den).all(), est
+
+
 def test_transport_vs_oracle_same_engine():
     """The oracle restatement and the device run side by side on a bigger
     paper-physics case (sigma_t = sigma_s = 100, n = 10 cube)."""
@@ -135,7 +177,7 @@ def test_transport_vs_oracle_same_engine():
         (r.final_state["position"] == o["position"][:cfg.num_particles]).all(axis=1)
     print("paper physics: identical histories", same.mean(), "events", r.events, o["events"],
           "collisions", r.collisions, o["collisions"])
-    assert same.mean() > 0.2
+    assert same.mean() == 1.0 if _exact_math() else same.mean() > 0.2
     fs = r.final_state
     n, nb = cfg.num_particles, cfg.num_batches
     d_seg = _paired_ok(fs["seg_total"], o["seg_total"][:n], "track length")
