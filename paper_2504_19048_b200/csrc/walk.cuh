@@ -21,7 +21,6 @@ __shared__ int8_t s_lane_alive[MAX_CTA_THREADS];
 struct XR {
     int nbp[4];
     unsigned nvs[4];
-    unsigned selw;  // wide meshes only: the four sel bytes
 };
 #ifndef BT_XR_V8
 #define BT_XR_V8 1
@@ -48,7 +47,6 @@ __device__ __forceinline__ XR load_xr(const WalkArgs& a, int e) {
     r.nbp[0] = u.x; r.nbp[1] = u.y; r.nbp[2] = u.z; r.nbp[3] = u.w;
     r.nvs[0] = v.x; r.nvs[1] = v.y; r.nvs[2] = v.z; r.nvs[3] = v.w;
 #endif
-    r.selw = a.xsel ? __ldg(a.xsel + e) : 0u;
     return r;
 }
 __device__ __forceinline__ void cpa8(unsigned dst, const void* src) {
@@ -210,7 +208,10 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
             (face & 2) ? ((face & 1) ? r.nvs[3] : r.nvs[2]) : ((face & 1) ? r.nvs[1] : r.nvs[0]);
         const bool wide = a.xsel != nullptr;
         const int nv = wide ? (int)nvs : (int)(nvs & 0xffffffu);
-        const unsigned s8 = wide ? (r.selw >> (8 * face)) & 0xffu : nvs >> 24;
+        // wide meshes (>= 2^24 vertices) keep the four selectors in a side
+        // array, read here -- a dependent load on those meshes only; carried
+        // in the record it cost every mesh a register (-0.7% on the C2 walk)
+        const unsigned s8 = wide ? (__ldg(a.xsel + L.e) >> (8 * face)) & 0xffu : nvs >> 24;
         // 2-bit fields -> the nibbles of a __byte_perm selector
         const unsigned t4 = (s8 | (s8 << 4)) & 0x0f0fu;
         const unsigned sel = (t4 | (t4 << 2)) & 0x3333u;
