@@ -34,6 +34,15 @@ def main(rep, crossings, note="", out_name="walk_sol.json"):
         i = h.index(name)
         return float(v[i].replace(",", "")) * SCALE.get(u[i], 1)
     x = float(crossings)
+
+    def lsu_wavefronts():
+        """LSU data-pipe wavefronts of the launch (1 per SM-cycle peak)."""
+        sms = get("device__attribute_multiprocessor_count")
+        try:
+            return get("SM_A.TriageCompute.l1tex__data_pipe_lsu_wavefronts.avg") * sms
+        except ValueError:  # not collected in this capture: from its % of peak
+            pct = get("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed")
+            return pct / 100.0 * get("sm__cycles_elapsed.avg") * sms
     dur = get("gpu__time_duration.sum")
     out = {
         "kernel": v[h.index("Kernel Name")],
@@ -43,7 +52,7 @@ def main(rep, crossings, note="", out_name="walk_sol.json"):
         "sm_clock_hz": get("sm__cycles_elapsed.avg.per_second"),
         "per_crossing": {
             "warp_instructions": get("smsp__inst_executed.sum") / x,
-            "lsu_wavefronts": get("SM_A.TriageCompute.l1tex__data_pipe_lsu_wavefronts.avg") * get("device__attribute_multiprocessor_count") / x,
+            "lsu_wavefronts": lsu_wavefronts() / x,
             "l2_bytes": 32 * get("lts__t_sectors.sum") / x,
             "dram_bytes": (get("dram__bytes_read.sum") + get("dram__bytes_write.sum")) / x,
         },
