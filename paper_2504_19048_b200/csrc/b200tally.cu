@@ -201,6 +201,12 @@ struct bt_tally {
     bool opt_sort = false;
     int opt_wagg = WAGG_ADAPTIVE;
     bool opt_exact_only = false;
+    struct Occ {
+        const void* k;
+        size_t dyn;
+        int bps;
+    };
+    std::vector<Occ> occ;  // launch_walk's occupancy per (kernel, dynamic shared size)
     bool opt_no_defer = true;  // BT_OPT_DEFER_INIT = 0 (default: measured slower, see below)
     int opt_staged = 2;  // 0: v1 refill, 1: stage kernel + work list, 2: direct refill
     WorkSoA work{};
@@ -910,10 +916,19 @@ static bt_status launch_walk(bt_tally* h, WalkArgs a, int64_t lo, int64_t count,
     auto* staged_k = V.staged[direct ? 1 : 0][a.digest ? 1 : 0];
     const void* kptr = staged ? (const void*)staged_k : (const void*)V.plain;
     const size_t dyn = staged ? sizeof(WarpStage) * (direct ? 1 : 2) * (V.threads / 32) : 0;
-    if (staged) CK(cudaFuncSetAttribute(kptr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    // the attribute and the occupancy of a (kernel, shared size) pair are
+    // fixed: resolved on first use, then cached (two driver calls per launch
+    // less: ~10 us of a 0.6-ms move of 1e5 particles)
     int bps = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kptr, V.threads, dyn));
-    bps = std::max(1, bps);
+    for (const auto& c : h->occ)
+        if (c.k == kptr && c.dyn == dyn) bps = c.bps;
+    if (!bps) {
+        if (staged)
+            CK(cudaFuncSetAttribute(kptr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kptr, V.threads, dyn));
+        bps = std::max(1, bps);
+        h->occ.push_back({kptr, dyn, bps});
+    }
     const int64_t want = (count + V.threads - 1) / V.threads;
     const unsigned blocks =
         (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)bps * h->num_sms));

@@ -68,7 +68,7 @@ def run_point(mesh, positions, sigma_t, moves, label, warm=1, chain=False, **mt_
         torch.cuda.synchronize()
         t0.record()
         mt.initialize_particle_location(positions)
-        _, _, alive_t = mt.particle_tensors()
+        alive_t = mt.particle_tensors()[2] if chain else None  # (a host sync: chains only)
         ev = mv = 0
         walk = 0.0
         for k in range(moves):
