@@ -222,6 +222,7 @@ __global__ void __launch_bounds__(THREADS, MINB) transport_kernel(const Transpor
                 need_flight = false;
             }
             if (walk_step<false>(a, L, C, P, DS)) {
+                sweep_guard_hit(a, L, C);
                 // flight over: its walk took L.iters sweeps in round `rounds`
                 if (rounds <= MAX_ROUNDS_TRACKED) atomicMax(t.round_max + rounds - 1, (unsigned)L.iters);
                 bool stop = true;

@@ -227,11 +227,13 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
     // exit filter, so its latency is hidden; the current element's again on
     // the paths where the particle stays (one definition, no register copies)
     L.nr = load_xr(a, (kind == 1 && nbp >= 0) ? (nbp >> 2) : L.e);
-    if (kind == 1) {
-        if (need_t)
-            // a face the fp32 filter decided: t in (1e-12, 1], division in range
-            t = exact_t<true>(T, face, ox, oy, oz, rn_sub(L.dx(), ox), rn_sub(L.dy(), oy),
-                              rn_sub(L.dz(), oz));
+    {   // the exact t of the chosen face, evaluated by every lane without a
+        // branch (-0.9% on the C2 walk): used where the fp32 filter decided a
+        // crossing (t in (1e-12, 1], division in range); exact_t selects the
+        // face's vertices, so any face value is safe for the other lanes
+        const double tt = exact_t<true>(T, face, ox, oy, oz, rn_sub(L.dx(), ox),
+                                        rn_sub(L.dy(), oy), rn_sub(L.dz(), oz));
+        if (kind == 1 && need_t) t = tt;
     }
     bool done = false;
     bool event = true;
@@ -326,12 +328,15 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
     ++L.iters;
     // sweep guard (search.py:513-516): the reference raises once its sweep
     // count exceeds the limit, even when the last particle finished in that
-    // very sweep -- so a lane finishing on step limit + 1 raises too
-    if (L.iters > a.max_sweeps32) {
-        atomicOr(C.sh + SC_ERR, 1u);
-        done = true;
-    }
-    return done;
+    // very sweep -- so a lane finishing on step limit + 1 raises too.  The
+    // walk just ends here (no branch per step); the error is flagged where a
+    // walk ends (finish(), the transport's flight end: sweep_guard_hit)
+    return done || L.iters > a.max_sweeps32;
+}
+
+// a walk ended: flag the sweep guard if it was the guard that ended it
+__device__ __forceinline__ void sweep_guard_hit(const WalkArgs& a, const Lane& L, Counters& C) {
+    if (L.iters > a.max_sweeps32) atomicOr(C.sh + SC_ERR, 1u);
 }
 
 template <bool DIG = true>
@@ -352,6 +357,7 @@ __device__ __forceinline__ void finish(const WalkArgs& a, Lane& L, Counters& C,
         a.dcount[i] = *DS.c;
     }
     C.maxit = max(C.maxit, (unsigned)L.iters);
+    sweep_guard_hit(a, L, C);
     L.busy = false;
 }
 
@@ -763,7 +769,9 @@ __global__ void __launch_bounds__(THREADS, MINB)
         if (L.busy) {
             if (walk_step<DIG>(a, L, C, P, DS)) finish<DIG>(a, L, C, DS);
         }
-        flush_pending(a, P, !L.busy);
+        // (a finished lane's pending score is issued by its next walk_step,
+        // after the refill, or by the flush at the loop's exit: no idle flush)
+        flush_pending(a, P, false);
     }
     cp_async_wait_all();
     flush_counters(a, C);
