@@ -141,10 +141,12 @@ struct Pending {
     double val = 0.0;
     int probe = 0;      // loop iterations to the next contention probe
     bool agg = false;   // warp-uniform: aggregate the pending scores
-    bool adaptive = false;  // probe for contention (WAGG_ADAPTIVE)
     __device__ __forceinline__ void init(const WalkArgs& a) {
-        adaptive = a.wagg == WAGG_ADAPTIVE;
         agg = a.wagg == WAGG_ALWAYS;
+        // one counter test per loop iteration in every mode: adaptive probes
+        // on its first iteration, the fixed modes never (-1% against a mode
+        // flag tested first)
+        probe = a.wagg == WAGG_ADAPTIVE ? 0 : 0x7fffffff;
     }
 };
 
@@ -408,7 +410,7 @@ __device__ __forceinline__ void flush_pending(const WalkArgs& a, Pending& P, boo
     constexpr unsigned FULL = 0xffffffffu;
     // mode flags resolved once per kernel (Pending::init); P.agg is the
     // current decision in every mode
-    if (P.adaptive && --P.probe <= 0) {  // probe every 4th iteration (warp-uniform)
+    if (--P.probe <= 0) {  // probe every 4th iteration (warp-uniform; adaptive mode only)
         const int lane = threadIdx.x & 31;
         const unsigned hm = __ballot_sync(FULL, P.has);
         const int nxt = __shfl_down_sync(FULL, (int)P.bin, 1);
