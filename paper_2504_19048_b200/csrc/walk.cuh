@@ -5,7 +5,10 @@
 // ---------------------------------------------------------------------------
 // walk kernels: the fused sweep (search.py:169-275) run to completion per lane
 
-constexpr int DEFAULT_VARIANT = 6;  // 192 x 2 CTAs/SM: see the launch variant table (b200tally.cu)
+constexpr int DEFAULT_VARIANT = 6;
+// vertex slots per lane: the element's four, plus a scratch slot that the
+// non-crossing lanes' zero-size copies land in (walk_step)
+constexpr int NSLOT = 5;  // 192 x 2 CTAs/SM: see the launch variant table (b200tally.cu)
 
 // Cold per-lane state (read only at the refill and at the end of a walk)
 // lives in shared memory, one slot per thread.
@@ -52,6 +55,10 @@ __device__ __forceinline__ XR load_xr(const WalkArgs& a, int e) {
 __device__ __forceinline__ void cpa8(unsigned dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src));
 }
+// cp.async of n (0 or 8) of 8 bytes: n = 0 zero-fills without reading global memory
+__device__ __forceinline__ void cpa8n(unsigned dst, const void* src, unsigned n) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(n));
+}
 __device__ __forceinline__ double lds64(unsigned ad) {
     double v;
     asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(ad));
@@ -96,8 +103,8 @@ __device__ __forceinline__ void vslots_fill(const WalkArgs& a, Lane& L, int e, c
         const double* g = &a.vtx[vid[k]].x;
         const unsigned ad = L.vsb + k * L.vss;
         cpa8(ad, g);
-        cpa8(ad + 4 * L.vss, g + 1);
-        cpa8(ad + 8 * L.vss, g + 2);
+        cpa8(ad + NSLOT * L.vss, g + 1);
+        cpa8(ad + 2 * NSLOT * L.vss, g + 2);
     }
     asm volatile("cp.async.commit_group;\n" ::);
     L.pm = 0x03020100u;
@@ -108,7 +115,7 @@ __device__ __forceinline__ int4 elem_vids(const WalkArgs& a, int e) {
 }
 // shared-memory vertex slots of a kernel with THREADS threads
 #define VSLOTS_DECL(THREADS)                                                   \
-    __shared__ double s_vslots[3 * 4 * (THREADS)];                                \
+    __shared__ double s_vslots[3 * NSLOT * (THREADS)];                                \
     const unsigned vsb0 = (unsigned)__cvta_generic_to_shared(s_vslots + threadIdx.x); \
     constexpr unsigned VSS = 8u * (THREADS);
 #define VSLOTS_INIT(L) \
@@ -187,8 +194,8 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
     for (int k = 0; k < 4; ++k) {
         const unsigned ad = L.vsb + ((L.pm >> (8 * k)) & 0xffu) * L.vss;
         T.x[k] = lds64(ad);
-        T.y[k] = lds64(ad + 4 * L.vss);
-        T.z[k] = lds64(ad + 8 * L.vss);
+        T.y[k] = lds64(ad + NSLOT * L.vss);
+        T.z[k] = lds64(ad + 2 * NSLOT * L.vss);
     }
     int face;
     double t;
@@ -203,27 +210,28 @@ __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& 
     }
     // (neighbour << 2) | its face across the exit face, -1 on the boundary
     const int nbp = (face & 2) ? ((face & 1) ? r.nbp[3] : r.nbp[2]) : ((face & 1) ? r.nbp[1] : r.nbp[0]);
-    if (kind == 1 && nbp >= 0) {
-        // crossing: the neighbour's one new vertex replaces local vertex
-        // `face` in its slot, and the slot map follows the neighbour's order
+    {   // crossing: the neighbour's one new vertex replaces local vertex
+        // `face` in its slot, and the slot map follows the neighbour's order.
+        // Every lane issues the three copies (no branch: -1.4% on the C2
+        // walk); the others copy zero bytes into their scratch slot
+        const bool cross = kind == 1 && nbp >= 0;
+        const int fc = face & 3;
         const unsigned nvs =
-            (face & 2) ? ((face & 1) ? r.nvs[3] : r.nvs[2]) : ((face & 1) ? r.nvs[1] : r.nvs[0]);
+            (fc & 2) ? ((fc & 1) ? r.nvs[3] : r.nvs[2]) : ((fc & 1) ? r.nvs[1] : r.nvs[0]);
         const bool wide = a.xsel != nullptr;
         const int nv = wide ? (int)nvs : (int)(nvs & 0xffffffu);
-        // wide meshes (>= 2^24 vertices) keep the four selectors in a side
-        // array, read here -- a dependent load on those meshes only; carried
-        // in the record it cost every mesh a register (-0.7% on the C2 walk)
-        const unsigned s8 = wide ? (__ldg(a.xsel + L.e) >> (8 * face)) & 0xffu : nvs >> 24;
-        // 2-bit fields -> the nibbles of a __byte_perm selector
+        const unsigned s8 = wide ? (__ldg(a.xsel + L.e) >> (8 * fc)) & 0xffu : nvs >> 24;
         const unsigned t4 = (s8 | (s8 << 4)) & 0x0f0fu;
         const unsigned sel = (t4 | (t4 << 2)) & 0x3333u;
-        const unsigned ad = L.vsb + ((L.pm >> (8 * face)) & 0xffu) * L.vss;
-        const double* g = &a.vtx[nv].x;
-        cpa8(ad, g);
-        cpa8(ad + 4 * L.vss, g + 1);
-        cpa8(ad + 8 * L.vss, g + 2);
+        const unsigned slot = cross ? (L.pm >> (8 * fc)) & 0xffu : 4u;
+        const unsigned ad = L.vsb + slot * L.vss;
+        const double* g = cross ? &a.vtx[nv].x : &a.vtx[0].x;
+        const unsigned n = cross ? 8u : 0u;
+        cpa8n(ad, g, n);
+        cpa8n(ad + NSLOT * L.vss, g + 1, n);
+        cpa8n(ad + 2 * NSLOT * L.vss, g + 2, n);
         asm volatile("cp.async.commit_group;\n" ::);
-        L.pm = __byte_perm(L.pm, 0u, sel);
+        L.pm = cross ? __byte_perm(L.pm, 0u, sel) : L.pm;
     }
     // the next step's crossing record: needed only after the next step's
     // exit filter, so its latency is hidden; the current element's again on
