@@ -54,6 +54,8 @@ def parse():
                    help="target CPU work for the bounded baseline sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-transport", action="store_true",
+                   help="skip the device-transport line (SURVEY §8f row 1) added on rank 0")
     p.add_argument("--sort", type=int, default=0)
     p.add_argument("--warp-agg", type=int, default=-1,
                    help="tally atomics: -1 adaptive aggregation (default), 0 never, 1 always")
@@ -597,6 +599,26 @@ def run_ours(args):
                                           "ring by host threads)"}
 
     cpu = None
+    # SURVEY §8f row 1 beside the headline: the device transport on the
+    # paper's verification physics, device time of the
+    # transport launches (tools/transport_line.py has the reference arm)
+    transport = None
+    if rank == 0 and not args.no_transport:
+        from paper_2504_19048_b200 import transport as T
+        tm = build_cube_mesh(10)
+        T.run(T.RunConfig(mesh_n=10, num_particles=20_000, num_batches=1), tm, device=local)
+        tr = T.run(T.RunConfig(mesh_n=10, num_particles=1_000_000, num_batches=2, seed=42), tm,
+                   device=local)
+        x = np.array([0.5])
+        exact = _lib.load().bt_glibc_math(x.ctypes.data, 1, 0, local, x.ctypes.data) == 0
+        transport = {"metric": "tet-crossings/s", "value": tr.events / tr.t_batch,
+                     "unit": "crossings/s", "collisions_per_s": tr.collisions / tr.t_batch,
+                     "histories_per_s": 2_000_000 / tr.t_batch, "events": tr.events,
+                     "collisions": tr.collisions, "t_transport_s": tr.t_batch,
+                     "bit_exact_histories": bool(exact),
+                     "config": "paper verification physics: cube n=10 (6,000 tets), sigma_t = "
+                               "sigma_s = 100/cm, 1e6 histories x 2 batches, seed 42"}
+
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, mrate, detail, _, _ = cpu_sample_rate(mesh, pos, dest, args.cpu_seconds)
         cpu = {"value": rate, "unit": "crossings/s", "cores": detail["cores"], "kind": "port",
@@ -617,6 +639,7 @@ def run_ours(args):
             "roofline": roofline(stats, args.steps, walk_s, alg_gbps, hbm_peak, peak_src,
                                  clocks.summary()),
             "cpu_baseline": cpu,
+            "transport": transport,
             "clocks": clocks.summary(),
             "gpu_launches": stats["kernels"],
             "lost_at_localization": lost,
