@@ -28,7 +28,8 @@ def test_bench_two_ranks_smoke():
     env = dict(os.environ, BENCH_SHARE_GPU="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", "bench.py", "--gpus", "2",
-           "--steps", "3", "--warmup", "3", "--particles", "300000", "--no-cpu-baseline"]
+           "--steps", "3", "--warmup", "3", "--particles", "300000", "--no-cpu-baseline",
+           "--no-transport"]
     out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
