@@ -159,17 +159,18 @@ struct Pending {
 
 // One step of search.py:183-274 for a flying lane.  Returns true when the
 // particle stops (reached, leaked, stuck-killed or sweep guard).  The step's
-// segment is left in P: scored at the start of the lane's next step (after its
-// loads) or by the loop-level flush.  DIG = false compiles the per-particle
-// digest bookkeeping out of the loop.
+// segment is left in P: scored at the start of the lane's next step -- the
+// next step of the same particle or, after a refill, of the lane's next one --
+// or by the loop-level flush.  DIG = false compiles the per-particle digest
+// bookkeeping out of the loop.
 template <bool DIG = true>
 __device__ __forceinline__ bool walk_step(const WalkArgs& a, Lane& L, Counters& C, Pending& P,
                                           const DigestSlot& DS) {
     const XR r = L.nr;
     Tet T;
-    // the previous step's score (warp-aggregated mode scores at loop level),
-    // as a predicated reduction: no branch (the
-    // address is formed either way; -0.35% on the C2 walk)
+    // the previous step's score (warp-aggregated mode scores at loop level)
+    // as a predicated reduction: no branch, the address is formed either way
+    // (-0.35% on the C2 walk)
     asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p red.global.add.f64 [%0], %1;\n}"
                  ::"l"(a.tally + P.bin), "d"(P.val), "r"((unsigned)P.has) : "memory");
     P.has = false;
