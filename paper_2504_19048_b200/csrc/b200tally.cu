@@ -647,14 +647,14 @@ bt_status bt_create(const double* vertices, int64_t num_vertices, const int32_t*
     const int64_t n = num_particles;
     TRYF(dalloc(&h->pos, 3 * n));
     TRYF(dalloc(&h->element, n));
-    TRYF(dalloc(&h->alive, n + FLAG_PAD));
-    TRYF(dalloc(&h->entry, n + FLAG_PAD));
-    TRYF(dalloc(&h->stuck, n + FLAG_PAD));
-    TRYF(dalloc(&h->outcome, n + FLAG_PAD));
+    TRYF(dalloc(&h->alive, n));
+    TRYF(dalloc(&h->entry, n));
+    TRYF(dalloc(&h->stuck, n));
+    TRYF(dalloc(&h->outcome, n));
     TRYF(dalloc(&h->seg_total, n));
     TRYF(dalloc(&h->group, n));
     TRYF(dalloc(&h->dest, 3 * n));
-    TRYF(dalloc(&h->fly, n + FLAG_PAD));
+    TRYF(dalloc(&h->fly, n));
     TRYF(dalloc(&h->weight, n));
     const int64_t nbins = num_elements * num_groups;
     TRYF(dalloc(&h->tally, nbins));
@@ -664,10 +664,10 @@ bt_status bt_create(const double* vertices, int64_t num_vertices, const int32_t*
     CKF(cudaMallocHost((void**)&h->hcounters, NDCOUNTERS * sizeof(unsigned long long)));
     CKF(cudaMemset(h->pos, 0, sizeof(double) * 3 * n));
     CKF(cudaMemset(h->element, 0xff, sizeof(int32_t) * n));  // -1: unlocalized
-    CKF(cudaMemset(h->alive, 0, n + FLAG_PAD));
-    CKF(cudaMemset(h->entry, 0xff, n + FLAG_PAD));  // -1
-    CKF(cudaMemset(h->stuck, 0, n + FLAG_PAD));
-    CKF(cudaMemset(h->outcome, 0, n + FLAG_PAD));
+    CKF(cudaMemset(h->alive, 0, n));
+    CKF(cudaMemset(h->entry, 0xff, n));  // -1
+    CKF(cudaMemset(h->stuck, 0, n));
+    CKF(cudaMemset(h->outcome, 0, n));
     CKF(cudaMemset(h->seg_total, 0, sizeof(double) * n));
     CKF(cudaMemset(h->group, 0, sizeof(int32_t) * n));
     CKF(cudaMemset(h->tally, 0, sizeof(double) * nbins));
@@ -915,7 +915,7 @@ static bt_status launch_walk(bt_tally* h, WalkArgs a, int64_t lo, int64_t count,
     const Variant& V = kVariants[vi];
     auto* staged_k = V.staged[direct ? 1 : 0][a.digest ? 1 : 0];
     const void* kptr = staged ? (const void*)staged_k : (const void*)V.plain;
-    const size_t dyn = staged ? sizeof(WarpStage) * (direct ? 3 : 2) * (V.threads / 32) : 0;
+    const size_t dyn = staged ? sizeof(WarpStage) * (direct ? 1 : 2) * (V.threads / 32) : 0;
     // the attribute and the occupancy of a (kernel, shared size) pair are
     // fixed: resolved on first use, then cached (two driver calls per launch
     // less: ~10 us of a 0.6-ms move of 1e5 particles)
@@ -1411,10 +1411,10 @@ bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, cons
             nch = h->move_chunks > 0 ? h->move_chunks : (count >= (4 << 20) ? 4 : 1);
             nch = (int)std::min<int64_t>(std::min(nch, MAX_CHUNKS), count);
         }
-        auto bound = [&](int c) -> int64_t {  // end of chunk c (a multiple of 32)
+        auto bound = [&](int c) -> int64_t {  // end of chunk c
             if (c + 1 >= nch) return count;
             const int sh = c == 0 ? nch : nch - 1 - c;
-            return (int64_t)((double)count / (double)(1ll << sh)) & ~(int64_t)31;
+            return (int64_t)((double)count / (double)(1ll << sh));
         };
         const bool pg_dest = is_pageable(destinations), pg_fly = is_pageable(flying),
                    pg_w = is_pageable(weights), pg_g = groups && is_pageable(groups);
@@ -1451,14 +1451,6 @@ bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, cons
         // check, the refill choice and the recorded source weight are all
         // decided on the device, and come back with the counters in one copy.
         TRY(settle_init(h));
-        // the walk's refill copies the flag bytes 4 at a time (cp.async),
-        // reading up to 3 bytes past the last particle: the library's flag
-        // arrays carry FLAG_PAD bytes of padding, a caller buffer does not,
-        // so the caller's flags go through the library's own first
-        if (flying != h->fly) {
-            CK(cudaMemcpyAsync(h->fly, flying, (size_t)count, cudaMemcpyDeviceToDevice, h->stream));
-            flying = h->fly;
-        }
         WalkArgs a = walk_args(h, destinations, flying, weights, true);
         TRY(walk_begin(h));
         a.gate = h->dcounters + 14;  // [14] walkable, [15] prepare_kernel's flags

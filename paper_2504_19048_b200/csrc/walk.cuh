@@ -547,9 +547,6 @@ struct WorkSoA {
 #define BT_STAGE_N 32
 #endif
 constexpr int STAGE_N = BT_STAGE_N;
-// bytes of padding past the particles in the int8 flag arrays: the direct
-// refill copies a stage's flags in 4-byte words
-constexpr int FLAG_PAD = 32;
 #ifndef BT_REFILL_MIN
 #define BT_REFILL_MIN 2
 #endif
@@ -561,10 +558,6 @@ struct __align__(16) WarpStage {
         w[STAGE_N], seg[STAGE_N];
     int4 r0[STAGE_N];
     int idx[STAGE_N], e[STAGE_N], g[STAGE_N], fl[STAGE_N];
-    // direct refill: the chunk's fly / alive / entry / stuck bytes and its
-    // first particle index
-    unsigned char fb[4][STAGE_N];
-    long long i0;
 };
 
 
@@ -613,79 +606,56 @@ __device__ __forceinline__ int claim_chunk(const WalkArgs& a, const WorkSoA& W, 
     return n;
 }
 
+// Direct refill (no stage kernel, no work list): a warp claims 32 consecutive
+// slots of the move and reads its particles straight from the particle
+// arrays into a stage (plain loads: one latency per 32 particles; measured
+// faster than splitting them into cp.async groups), including the starting
+// element's record.  Flags: bit 24 = walkable (flying and localized), bit 25
+// = flying.
 struct DirectArgs {
     int64_t lo, hi;  // particles [lo, hi) of this launch (slots through a.order if set)
 };
 
-// Direct refill (no stage kernel, no work list): a warp claims 32
-// consecutive particles of the move with one atomicAdd and copies them straight
-// from the particle arrays -- asynchronously, three stages per warp.  A chunk's fields are
-// copied from the particle arrays with cp.async (claim_direct_async); when
-// they have landed its flags are composed and its starting records copied
-// (stage_records, also cp.async); one stage later it becomes current.  Every
-// wait happens a full stage after the copies it waits for were issued.
-__device__ __forceinline__ void cp_async16n(void* smem, const void* gmem, unsigned n) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
-}
-__device__ __forceinline__ bool b0_live(int lane, int n) { return (lane & 7) * 4 < n; }
-__device__ __forceinline__ int claim_direct_async(const WalkArgs& a, const DirectArgs& d,
-                                                  WarpStage& st) {
+__device__ __forceinline__ int claim_direct(const WalkArgs& a, const DirectArgs& d, WarpStage& st) {
+    constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(a.queue, (unsigned long long)STAGE_N);
-    base = __shfl_sync(0xffffffffu, base, 0);
+    base = __shfl_sync(FULL, base, 0);
     const int64_t left = (d.hi - d.lo) - (int64_t)base;
     const int n = left <= 0 ? 0 : (left >= STAGE_N ? STAGE_N : (int)left);
-    const int64_t i0 = d.lo + (int64_t)base;
     if (lane < n) {
-        const int64_t i = i0 + lane;
-        cp_async8(&st.px[lane], a.pos + 3 * i);
-        cp_async8(&st.py[lane], a.pos + 3 * i + 1);
-        cp_async8(&st.pz[lane], a.pos + 3 * i + 2);
-        cp_async8(&st.dx[lane], a.dest + 3 * i);
-        cp_async8(&st.dy[lane], a.dest + 3 * i + 1);
-        cp_async8(&st.dz[lane], a.dest + 3 * i + 2);
-        cp_async8(&st.seg[lane], a.seg_total + i);
-        cp_async4(&st.e[lane], a.element + i);
-        if (a.score) {
-            cp_async8(&st.w[lane], a.weight + i);
-            cp_async4(&st.g[lane], a.group + i);
+        const int64_t t = (int64_t)base + lane;
+        const int64_t i = a.order ? (int64_t)a.order[t] : d.lo + t;
+        const int fly = a.fly_in[i] != 0;
+        const int el = a.element[i];
+        const bool walk = fly && el >= 0;
+        st.idx[lane] = (int)i;
+        st.px[lane] = a.pos[3 * i];
+        st.py[lane] = a.pos[3 * i + 1];
+        st.pz[lane] = a.pos[3 * i + 2];
+        st.dx[lane] = a.dest[3 * i];
+        st.dy[lane] = a.dest[3 * i + 1];
+        st.dz[lane] = a.dest[3 * i + 2];
+        const double w = a.score ? a.weight[i] : 0.0;
+        st.w[lane] = w;
+        st.seg[lane] = a.seg_total[i];
+        st.e[lane] = el;
+        st.g[lane] = a.score ? a.group[i] : 0;
+        st.fl[lane] = ((int)(unsigned char)a.entry[i]) | ((int)(unsigned char)a.stuck[i] << 8) |
+                      ((int)(unsigned char)(a.alive[i] | a.fly_in[i]) << 16) |  // load_step
+                      (walk ? 1 << 24 : 0) | (fly ? 1 << 25 : 0);
+        if (walk) {
+            const int4* rp = reinterpret_cast<const int4*>(a.rec + el);
+            st.r0[lane] = ldg_mesh(rp);
         }
     }
-    if (b0_live(lane, n)) {  // 8 lanes per int8 array, 4 bytes each: the last word
-        // may reach up to 3 bytes past the particles, into the arrays' FLAG_PAD
-        const int arr = lane >> 3, b0 = (lane & 7) * 4;
-        const int8_t* src = arr == 0 ? a.fly_in : arr == 1 ? a.alive : arr == 2 ? a.entry : a.stuck;
-        cp_async4(&st.fb[arr][b0], src + i0 + b0);
-    }
-    if (lane == 0) st.i0 = i0;
-    cp_async_commit();
+    __syncwarp();
     return n;
 }
-// the chunk's fields have landed: compose its flags, copy its starting records
-__device__ __forceinline__ void stage_records(const WalkArgs& a, WarpStage& st, int n) {
-    const int lane = threadIdx.x & 31;
-    __syncwarp();
-    if (lane < n) {
-        const int fly = st.fb[0][lane] != 0;
-        const int el = st.e[lane];
-        const bool walk = fly && el >= 0;
-        st.idx[lane] = (int)(st.i0 + lane);
-        if (!a.score) {
-            st.w[lane] = 0.0;
-            st.g[lane] = 0;
-        }
-        st.fl[lane] = (int)st.fb[2][lane] | ((int)st.fb[3][lane] << 8) |
-                      ((int)(unsigned char)(st.fb[1][lane] | st.fb[0][lane]) << 16) |  // load_step
-                      (walk ? 1 << 24 : 0) | (fly ? 1 << 25 : 0);
-        cp_async16n(&st.r0[lane], a.rec + (walk ? el : 0), walk ? 16u : 0u);
-    }
-    cp_async_commit();
-}
 
-// DIRECT: stages filled by claim_direct_async from the particle arrays;
-// otherwise from the stage kernel's work list with cp.async (claim_chunk).
+// DIRECT: stages filled by claim_direct from the particle arrays; otherwise
+// from the stage kernel's work list with cp.async (claim_chunk).
 template <int THREADS, int MINB, bool DIG, bool DIRECT>
 __global__ void __launch_bounds__(THREADS, MINB)
     walk_staged_kernel(const WalkArgs a, const WorkSoA W, const int64_t* __restrict__ nwork_p,
@@ -694,7 +664,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     constexpr unsigned FULL = 0xffffffffu;
     if (!gate_open(a, DIRECT)) return;
     // the warps' stages in dynamic shared memory: double-buffered for the
-    // stage kernel's cp.async prefetch, three per warp for the direct refill (claim_direct_async)
+    // stage kernel's cp.async prefetch, one per warp for the direct refill
     extern __shared__ __align__(16) unsigned char dyn_smem[];
     WarpStage(*stages)[2] = reinterpret_cast<WarpStage(*)[2]>(dyn_smem);
     __shared__ unsigned shc[SC_N];
@@ -706,7 +676,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     const int wid = threadIdx.x >> 5;
     const int64_t nwork = DIRECT ? 0 : *nwork_p;
     auto claim = [&](WarpStage& st) -> int {
-        return claim_chunk(a, W, st, nwork);  // (the stage kernel's work list)
+        return DIRECT ? claim_direct(a, D, st) : claim_chunk(a, W, st, nwork);
     };
     Lane L;
     L.busy = false;
@@ -717,24 +687,16 @@ __global__ void __launch_bounds__(THREADS, MINB)
     P.init(a);
     int cur = 0;
     int head = 0;
-    WarpStage* const st3 = reinterpret_cast<WarpStage*>(dyn_smem) + 3 * wid;
-    int s_cur = 0, s_nxt = 1, s_nn = 2, nnn = 0;
-    int ncur, nnext;
-    if (DIRECT) {
-        ncur = claim_direct_async(a, D, st3[0]);
-        nnext = ncur == STAGE_N ? claim_direct_async(a, D, st3[1]) : 0;
-        cp_async_wait_all();
-        stage_records(a, st3[0], ncur);
-        stage_records(a, st3[1], nnext);
-        nnn = nnext == STAGE_N ? claim_direct_async(a, D, st3[2]) : 0;
-        cp_async_wait_all();
-        __syncwarp();
-    } else {
-        ncur = claim(stages[wid][0]);
-        nnext = ncur == STAGE_N ? claim(stages[wid][1]) : 0;
-        cp_async_wait_all();
-        __syncwarp();
-    }
+    // direct refill: claim_direct's loads block anyway, so one stage per warp
+    // (claimed when the previous one is used up) -- the second buffer's
+    // shared memory goes to L1
+    WarpStage* const st1 = reinterpret_cast<WarpStage*>(dyn_smem) + wid;
+    int ncur = DIRECT ? claim(*st1) : claim(stages[wid][0]);
+    int nnext = (!DIRECT && ncur == STAGE_N) ? claim(stages[wid][1]) : 0;
+    // only the first group must have landed; wait_group 1 would do, but the
+    // second claim may be empty -- a full wait costs one DRAM latency once
+    cp_async_wait_all();
+    __syncwarp();
     while (true) {
         unsigned idle = __ballot_sync(FULL, !L.busy);
         // Refill only once two lanes are idle (or none is busy): the refill is a
@@ -746,18 +708,11 @@ __global__ void __launch_bounds__(THREADS, MINB)
         while (idle) {
             if (head == ncur) {  // current stage used up: switch to the prefetched one
                 if (DIRECT) {
-                    if (nnext == 0) break;
-                    cp_async_wait_all();  // nxt's records, nn's fields (issued a stage ago)
-                    __syncwarp();
-                    const int freed = s_cur;
-                    s_cur = s_nxt;
-                    ncur = nnext;
+                    if (ncur < STAGE_N) break;  // the last chunk was partial: no more work
+                    __syncwarp();               // every lane is done reading the stage
+                    ncur = claim(*st1);
                     head = 0;
-                    s_nxt = s_nn;
-                    nnext = nnn;
-                    if (nnext) stage_records(a, st3[s_nxt], nnext);
-                    s_nn = freed;
-                    nnn = nnext == STAGE_N ? claim_direct_async(a, D, st3[s_nn]) : 0;
+                    if (ncur == 0) break;
                 } else {
                     if (nnext == 0) break;
                     cp_async_wait_all();
@@ -772,7 +727,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
             const int take = min((int)__popc(idle), ncur - head);
             if (!L.busy) {
                 const int rk = __popc(idle & lanemask_lt());
-                const WarpStage& s = DIRECT ? st3[s_cur] : stages[wid][cur];
+                const WarpStage& s = DIRECT ? *st1 : stages[wid][cur];
                 const int j = head + rk;
                 const int fl0 = rk < take ? s.fl[j] : 0;
                 if (DIRECT && rk < take && !(fl0 & (1 << 24))) {
