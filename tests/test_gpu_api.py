@@ -381,3 +381,37 @@ def test_device_libm_restatement_equals_host_libm():
         want = np.array([fns[fn](float(v)) for v in x])
         bad = np.nonzero(out.view(np.uint64) != want.view(np.uint64))[0]
         assert bad.size == 0, (fn, x[bad[:5]], out[bad[:5]], want[bad[:5]])
+
+
+def test_misaligned_device_flying_buffer():
+    """A caller's int8 flying tensor that starts at an odd address (a view)
+    is read in place by the walk's refill: the same results as an aligned
+    one (a refill that copies the flags in 4-byte words must not change
+    that)."""
+    torch = pytest.importorskip("torch")
+    m = build_cube_mesh(12)
+    gen = np.random.default_rng(202)
+    n = 50_001
+    pos = synth.uniform_box(gen, n)
+    dest = synth.flight_destinations(gen, pos, 3.0)
+    fly = (gen.random(n) < 0.8).astype(np.int8)
+    w = 0.5 + gen.random(n)
+    out = []
+    for offset in (0, 1, 3):
+        mt = MeshTally(m, n, digest=True)
+        mt.initialize_particle_location(torch.from_numpy(pos).cuda())
+        big = torch.zeros(n + 8, dtype=torch.int8, device="cuda")
+        f = big[offset:offset + n]
+        f.copy_(torch.from_numpy(fly).cuda())
+        s = mt.move_to_next_location(torch.from_numpy(dest).cuda(), f, torch.from_numpy(w).cuda())
+        out.append(((s.sweeps, s.events, s.reached, s.boundary_exits, s.stuck_recoveries,
+                     s.stuck_terminations), mt.read_particles(), mt.read_digest(),
+                    mt.batch_totals().copy()))
+        mt.close()
+    for s, st, (d, c), t in out[1:]:
+        assert s == out[0][0]
+        for k in ("position", "element", "alive", "outcome", "seg_total"):
+            assert np.array_equal(getattr(st, k), getattr(out[0][1], k)), k
+        assert np.array_equal(d, out[0][2][0])
+        den = np.maximum(np.abs(t), np.abs(out[0][3]))
+        assert (np.abs(t - out[0][3]) <= 1e-9 * den).all()  # atomic summation order
