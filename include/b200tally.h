@@ -80,13 +80,17 @@ enum {
     BT_OPT_EXACT_ONLY = 8,    /* 1: no fp32 pre-filters -- grid localization tests every
                                  candidate exactly, and (with BT_OPT_DIGEST) every exit search
                                  runs the reference's literal arithmetic; for validation */
-    BT_OPT_DEFER_INIT = 9     /* host positions, grid mode, >= 2^20 particles: 1 = the
+    BT_OPT_DEFER_INIT = 9,    /* host positions, grid mode, >= 2^20 particles: 1 = the
                                  initialize call returns once the DMA (from the front) and
                                  host threads (from the back, into pinned staging) have read
                                  the caller's buffer; the parked part is copied and localized
                                  by the next call (the move: chunk by chunk, ahead of the walk
                                  chunks that need it); 0 (default, measured faster end to
                                  end): copy it all in the initialize call */
+    BT_OPT_STREAM_MOVE = 10   /* host inputs, direct refill, >= 2^22 particles: 1 (default) =
+                                 ONE walk launch consumes the move's input chunks as the copy
+                                 stream lands them (a stream memory write after each chunk);
+                                 0 = one walk launch per chunk */
 };
 
 /* Mirrors meshtally.search.TraceSummary (search.py:150-157). */

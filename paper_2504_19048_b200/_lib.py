@@ -24,7 +24,7 @@ BT_LOCATE_GRID, BT_LOCATE_WALK = 0, 1
  BT_TALLY_COL_SUM_SQ) = range(6)
 (BT_OPT_MAX_SWEEPS, BT_OPT_DIGEST, BT_OPT_SORT, BT_OPT_WARP_AGG,
  BT_OPT_BLOCKS_PER_SM, BT_OPT_STAGED, BT_OPT_MOVE_CHUNKS, BT_OPT_LOCATE_LANES,
- BT_OPT_EXACT_ONLY, BT_OPT_DEFER_INIT) = range(10)
+ BT_OPT_EXACT_ONLY, BT_OPT_DEFER_INIT, BT_OPT_STREAM_MOVE) = range(11)
 
 # every symbol declared in include/b200tally.h (checked by tests/test_abi.py)
 EXPORTS = (

@@ -29,6 +29,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -209,6 +210,9 @@ struct bt_tally {
     std::vector<Occ> occ;  // launch_walk's occupancy per (kernel, dynamic shared size)
     bool opt_no_defer = true;  // BT_OPT_DEFER_INIT = 0 (default: measured slower, see below)
     int opt_staged = 2;  // 0: v1 refill, 1: stage kernel + work list, 2: direct refill
+    bool opt_stream_move = true;        // BT_OPT_STREAM_MOVE
+    unsigned long long* ready = nullptr;  // streamed move: particles landed so far
+    int stream_ops = -1;                // stream memory writes usable: -1 unknown, 0 no, 1 yes
     WorkSoA work{};
     void* work_mem = nullptr;
     int blocks_per_sm = 0;
@@ -235,6 +239,29 @@ static bt_status ensure_device(bt_tally* h) {
 // host -> device copy of a caller buffer on `st`: DMA straight from pinned
 // memory, through the pinned ring + host threads from pageable memory.
 // Returns once `src` has been read.
+// cuStreamWriteValue64 through the runtime's driver entry point (no link
+// against libcuda): the copy engine's front end writes the value once the
+// stream's earlier copies are complete, with no SM involved -- the walk that
+// waits for it holds every SM.
+typedef int (*WriteValue64Fn)(cudaStream_t, unsigned long long, unsigned long long, unsigned);
+static WriteValue64Fn write_value64() {
+    static WriteValue64Fn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &p, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<WriteValue64Fn>(p);
+    }();
+    return fn;
+}
+static bool stream_write(bt_tally* h, unsigned long long* where, unsigned long long v,
+                         cudaStream_t st) {
+    WriteValue64Fn fn = write_value64();
+    return fn && fn(st, (unsigned long long)(uintptr_t)where, v, 0) == 0;
+}
+
 static bt_status h2d(bt_tally* h, void* dst, const void* src, size_t bytes, cudaStream_t st,
                      bool pageable) {
     if (!bytes) return BT_OK;
@@ -255,7 +282,7 @@ static bt_status free_all(bt_tally* h) {
                     h->snap_flags, h->snap_seg, h->work_mem, h->init_stage,
                     h->col_tally, h->col_sum, h->col_sum_sq, h->tr_dir, h->tr_weight,
                     h->tr_rng, h->tr_round_max, h->tr_count, h->tr_wsum, h->tr_xs,
-                    h->sb_mem, h->tr_fly, h->sb_flag, h->sb_tmp};
+                    h->sb_mem, h->tr_fly, h->sb_flag, h->sb_tmp, h->ready};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->hcounters) cudaFreeHost(h->hcounters);
@@ -782,6 +809,7 @@ bt_status bt_set_option(bt_tally* h, int32_t key, int64_t value) {
         case BT_OPT_MOVE_CHUNKS: h->move_chunks = (int)value; break;
         case BT_OPT_EXACT_ONLY: h->opt_exact_only = value != 0; break;
         case BT_OPT_DEFER_INIT: h->opt_no_defer = value == 0; break;
+        case BT_OPT_STREAM_MOVE: h->opt_stream_move = value != 0; break;
         case BT_OPT_LOCATE_LANES:
             if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8 &&
                 value != 16 && value != 32)
@@ -884,6 +912,7 @@ static WalkArgs walk_args(bt_tally* h, const double* dest, const int8_t* fly, co
     a.exact_only = h->opt_exact_only ? 1 : 0;
     a.gate = nullptr;
     a.gate_pick = 0;
+    a.ready = nullptr;
     return a;
 }
 
@@ -1009,6 +1038,9 @@ static bt_status walk_end(bt_tally* h, int64_t max_sweeps, bt_summary* summary,
         summary->stuck_recoveries = (int64_t)c[C_RECOV];
         summary->stuck_terminations = (int64_t)c[C_KILLED];
     }
+    if (c[C_ERR] & 2ull)
+        return set_err(BT_ERUNTIME, "streamed move: inputs did not arrive within 5 s "
+                                    "(set BT_OPT_STREAM_MOVE = 0 under tools that serialise launches)");
     if (c[C_ERR])
         return set_err(BT_ERUNTIME, "trace did not terminate within %lld sweeps",
                        (long long)max_sweeps);
@@ -1411,8 +1443,42 @@ bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, cons
             nch = h->move_chunks > 0 ? h->move_chunks : (count >= (4 << 20) ? 4 : 1);
             nch = (int)std::min<int64_t>(std::min(nch, MAX_CHUNKS), count);
         }
+        // Streamed: one direct-refill launch over the whole move; its warps wait
+        // for each chunk's inputs (WalkArgs::ready) instead of one launch per
+        // chunk, whose tails cost ~1 ms of the C2 move.  Chunk ends are
+        // multiples of 128 particles, so no L1 line of a landed chunk holds
+        // bytes of one still in flight.
+        const bool any_pageable = is_pageable(destinations) || is_pageable(flying) ||
+                                  is_pageable(weights) || (groups && is_pageable(groups));
+        // Pinned (or registered) inputs only: every copy and mark is enqueued
+        // before the walk is launched, so nothing the walk waits for depends on
+        // the host after the launch -- a tool that runs the launch alone (ncu)
+        // or to completion (CUDA_LAUNCH_BLOCKING) cannot deadlock it.
+        // Pageable inputs are staged by host threads while the walk runs and
+        // keep one launch per chunk.
+        bool streamed = h->opt_stream_move && nch > 1 && h->opt_staged == 2 && !h->di_pending &&
+                        !any_pageable;
+        if (streamed && h->stream_ops != 0) {
+            if (!h->ready) TRY(dalloc(&h->ready, 1));
+            streamed = stream_write(h, h->ready, 0, h->cstream);
+            if (h->stream_ops < 0) h->stream_ops = streamed ? 1 : 0;
+            if (!streamed) cudaGetLastError();
+        } else {
+            streamed = false;
+        }
+        // Streamed marks: the walk starts after 1/64 of the inputs and the
+        // copies (~1600 particles/us pinned) outrun the walk (~700/us on C2)
+        // from there, so the marks only need to come often: 1/64, 1/32,
+        // 1/16, 1/8, then every 1/8 (or move_chunks equal parts if set).
+        static const double kMarks[] = {1 / 64., 1 / 32., 1 / 16., 1 / 8., 2 / 8., 3 / 8.,
+                                        4 / 8.,  5 / 8.,  6 / 8.,  7 / 8., 1.0};
+        if (streamed && h->move_chunks <= 0) nch = (int)(sizeof kMarks / sizeof kMarks[0]);
         auto bound = [&](int c) -> int64_t {  // end of chunk c
             if (c + 1 >= nch) return count;
+            if (streamed) {
+                const double f = h->move_chunks > 0 ? (double)(c + 1) / nch : kMarks[c];
+                return (int64_t)((double)count * f) & ~(int64_t)127;
+            }
             const int sh = c == 0 ? nch : nch - 1 - c;
             return (int64_t)((double)count / (double)(1ll << sh));
         };
@@ -1423,7 +1489,31 @@ bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, cons
         // that chunk c's tail frees instead of waiting for its last walk
         CK(cudaEventRecord(h->ev_s1, h->stream));
         CK(cudaStreamWaitEvent(h->stream2, h->ev_s1, 0));
-        for (int c = 0; c < nch; ++c) {
+        if (streamed) {
+            for (int c = 0; c < nch; ++c) {
+                const int64_t lo = c == 0 ? 0 : bound(c - 1), hi = bound(c);
+                const int64_t n = hi - lo;  // (the first chunk may round to empty)
+                TRY(h2d(h, h->dest + 3 * lo, destinations + 3 * lo, sizeof(double) * 3 * n,
+                        h->cstream, pg_dest));
+                TRY(h2d(h, h->fly + lo, flying + lo, n, h->cstream, pg_fly));
+                TRY(h2d(h, h->weight + lo, weights + lo, sizeof(double) * n, h->cstream, pg_w));
+                if (groups)
+                    TRY(h2d(h, h->group + lo, groups + lo, sizeof(int32_t) * n, h->cstream, pg_g));
+                if (!stream_write(h, h->ready, (unsigned long long)hi, h->cstream))
+                    return set_err(BT_ECUDA, "stream memory write failed");
+                if (c == 0) {  // the walk starts once the first chunk has landed
+                    CK(cudaEventRecord(h->evchunk[0], h->cstream));
+                    CK(cudaStreamWaitEvent(h->stream, h->evchunk[0], 0));
+                }
+            }
+            WalkArgs sa = a;
+            sa.ready = h->ready;
+            TRY(walk_enqueue(h, sa, 0, count, 0, h->stream));
+            // the move ends after the copy stream's last write
+            CK(cudaEventRecord(h->evchunk[1], h->cstream));
+            CK(cudaStreamWaitEvent(h->stream, h->evchunk[1], 0));
+        }
+        for (int c = 0; c < (streamed ? 0 : nch); ++c) {
             const int64_t lo = c == 0 ? 0 : bound(c - 1), hi = bound(c);
             const int64_t n = hi - lo;
             if (n <= 0) continue;

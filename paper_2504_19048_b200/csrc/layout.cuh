@@ -82,6 +82,11 @@ struct WalkArgs {
     // choice.
     const unsigned long long* gate;
     int32_t gate_pick;
+    // Host-input move streamed into one direct-refill launch (nullable): the
+    // particles below *ready have landed; a warp claiming beyond it waits.
+    // Written by the copy stream (a stream memory operation after each chunk's
+    // copies), so the walk starts after the first chunk, not the last.
+    const unsigned long long* ready;
 };
 
 // the launch runs (see WalkArgs::gate); DIRECT: the direct-refill walk

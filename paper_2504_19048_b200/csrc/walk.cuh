@@ -612,6 +612,8 @@ __device__ __forceinline__ int claim_chunk(const WalkArgs& a, const WorkSoA& W, 
 // faster than splitting them into cp.async groups), including the starting
 // element's record.  Flags: bit 24 = walkable (flying and localized), bit 25
 // = flying.
+// a streamed move's warp gives up on inputs that have not landed after 5 s
+constexpr unsigned long long STREAM_STALL_NS = 5000000000ull;
 struct DirectArgs {
     int64_t lo, hi;  // particles [lo, hi) of this launch (slots through a.order if set)
 };
@@ -624,6 +626,28 @@ __device__ __forceinline__ int claim_direct(const WalkArgs& a, const DirectArgs&
     base = __shfl_sync(FULL, base, 0);
     const int64_t left = (d.hi - d.lo) - (int64_t)base;
     const int n = left <= 0 ? 0 : (left >= STAGE_N ? STAGE_N : (int)left);
+    if (a.ready && n > 0) {  // streamed host-input move: wait for this chunk's inputs
+        int stalled = 0;
+        if (lane == 0) {
+            const unsigned long long need = (unsigned long long)(d.lo + (int64_t)base + n);
+            unsigned long long r, t0, t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            while (true) {
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(r) : "l"(a.ready) : "memory");
+                if (r >= need) break;
+                __nanosleep(256);
+                // inputs that never arrive (a tool that runs this launch alone,
+                // say) end the walk with an error instead of a hung GPU
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                if (t - t0 > STREAM_STALL_NS) {
+                    atomicOr(a.counters + C_ERR, 2ull);
+                    stalled = 1;
+                    break;
+                }
+            }
+        }
+        if (__shfl_sync(FULL, stalled, 0)) return 0;
+    }
     if (lane < n) {
         const int64_t t = (int64_t)base + lane;
         const int64_t i = a.order ? (int64_t)a.order[t] : d.lo + t;

@@ -377,7 +377,7 @@ class MeshTally:
     def __init__(self, mesh, num_particles: int, num_groups: int = 1, threads: int = 1, *,
                  device: int = 0, devices=None, localize: str = "grid", digest: bool = False,
                  sort: bool = False, warp_aggregate: bool | None = None, staged: bool | int = True,
-                 move_chunks: int = 0):
+                 move_chunks: int = 0, stream_move: bool = True):
         if isinstance(mesh, (str, Path)):
             mesh = read_tetmesh(mesh)
         if not all(hasattr(mesh, a) for a in ("vertices", "elements", "adj_elem", "adj_face",
@@ -434,6 +434,7 @@ class MeshTally:
         if staged is not True:
             self.set_option(_lib.BT_OPT_STAGED, int(staged))
         self.set_option(_lib.BT_OPT_MOVE_CHUNKS, int(move_chunks))
+        self.set_option(_lib.BT_OPT_STREAM_MOVE, int(stream_move))
         self._grid = TallyGrid(self)
 
     # ------------------------------------------------------------------ props

@@ -102,7 +102,8 @@ def test_wide_crossing_records_keep_parity(name, monkeypatch):
                                                            warp_aggregate=True),
                                   dict(move_chunks=3), dict(move_chunks=16, warp_aggregate=True),
                                   dict(warp_aggregate=False), dict(staged=1), dict(staged=2),
-                                  dict(staged=2, sort=True), dict(staged=2, move_chunks=5)])
+                                  dict(staged=2, sort=True), dict(staged=2, move_chunks=5),
+                                  dict(move_chunks=5, stream_move=False)])
 def test_walk_options_keep_parity(opts):
     _check_case(load_walk_case("c1_point_s2"), "grid", **opts)
     _check_case(load_walk_case("n6_uniform_g3"), "grid", **opts)
@@ -410,10 +411,14 @@ def test_recorded_source_weight_is_numpy_sum(frac_flying):
     mt.close()
 
 
-def test_pipelined_host_inputs_match_device_inputs():
+@pytest.mark.parametrize("stream_move,pinned", [(True, False), (True, True), (False, False)])
+def test_pipelined_host_inputs_match_device_inputs(stream_move, pinned):
     """>= 4M particles: host positions are copied and localized in chunks, host
-    move inputs are walked in geometric chunks on two streams -- the result
-    must equal the single-launch device-input path bit for bit."""
+    move inputs are copied in chunks and walked either by ONE launch that
+    waits for each chunk (stream_move, the default, with pinned inputs) or by
+    one launch per chunk on two streams (pageable inputs, or stream_move off)
+    -- the result must equal the single-launch device-input path bit for
+    bit."""
     torch = pytest.importorskip("torch")
     m = build_cube_mesh(12)
     gen = np.random.default_rng(21)
@@ -422,15 +427,18 @@ def test_pipelined_host_inputs_match_device_inputs():
     dest = synth.flight_destinations(gen, pos, 5.0)
     fly = (gen.random(n) < 0.9).astype(np.int8)
     w = 0.5 + gen.random(n)
-    host = MeshTally(m, n)
+    host = MeshTally(m, n, stream_move=stream_move)
     dev = MeshTally(m, n)
+
+    def h(x):  # pageable numpy, or a numpy view of pinned host memory
+        return torch.from_numpy(x).pin_memory().numpy() if pinned else x
     host.initialize_particle_location(pos)
     dev.initialize_particle_location(torch.from_numpy(pos).cuda())
     # two chained moves: the second one's input buffers on the device still
     # hold the first move's values, so a walk chunk that started before its
     # own inputs landed would show up as a mismatch
     for move in range(2):
-        s1 = host.move_to_next_location(dest, fly, w)
+        s1 = host.move_to_next_location(h(dest), h(fly), h(w))
         s2 = dev.move_to_next_location(torch.from_numpy(dest).cuda(),
                                        torch.from_numpy(fly).cuda(), torch.from_numpy(w).cuda())
         assert s1 == s2

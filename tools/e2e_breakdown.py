@@ -3,7 +3,7 @@ initialize_particle_location (host positions), move_to_next_location (host
 inputs) and finalize, plus the library's own event timings, for pinned and
 pageable inputs with and without the deferred initialize (BT_OPT_DEFER_INIT).
 
-    python tools/e2e_breakdown.py [move_chunks]
+    python tools/e2e_breakdown.py [move_chunks] [stream_move 0/1]
 """
 import sys
 import time
@@ -23,7 +23,8 @@ pinned = (torch.from_numpy(pos).pin_memory().numpy(), torch.from_numpy(dest).pin
           torch.ones(P, dtype=torch.int8).pin_memory().numpy(),
           torch.ones(P, dtype=torch.float64).pin_memory().numpy())
 pageable = (pos, dest, np.ones(P, np.int8), np.ones(P))
-mt = MeshTally(m, P, move_chunks=int(sys.argv[1]) if len(sys.argv) > 1 else 0)
+SM = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+mt = MeshTally(m, P, move_chunks=int(sys.argv[1]) if len(sys.argv) > 1 else 0, stream_move=bool(SM))
 import os
 for label, (h_pos, h_dest, h_fly, h_w) in (("pinned", pinned), ("pageable", pageable)):
     for defer in (1, 0):
@@ -43,5 +44,5 @@ for label, (h_pos, h_dest, h_fly, h_w) in (("pinned", pinned), ("pageable", page
                 tot.append((1e3 * (t1 - t0), 1e3 * (t2 - t1), walk_ms, 1e3 * (t3 - t2),
                             1e3 * (t3 - t0)))
         a = np.mean(tot, axis=0)
-        print(f"{label:8s} defer={defer} init_chunks={os.environ.get('B200TALLY_INIT_CHUNKS', 4)}: init {a[0]:.2f} ms, move {a[1]:.2f} ms (walk kernels "
+        print(f"{label:8s} stream_move={SM} defer={defer} init_chunks={os.environ.get('B200TALLY_INIT_CHUNKS', 4)}: init {a[0]:.2f} ms, move {a[1]:.2f} ms (walk kernels "
               f"{a[2]:.2f}), finalize {a[3]:.2f} ms, total {a[4]:.2f} ms", flush=True)
