@@ -236,9 +236,6 @@ static bt_status ensure_device(bt_tally* h) {
 
 #include "host_stage.cuh"
 
-// host -> device copy of a caller buffer on `st`: DMA straight from pinned
-// memory, through the pinned ring + host threads from pageable memory.
-// Returns once `src` has been read.
 // cuStreamWriteValue64 through the runtime's driver entry point (no link
 // against libcuda): the copy engine's front end writes the value once the
 // stream's earlier copies are complete, with no SM involved -- the walk that
@@ -262,6 +259,9 @@ static bool stream_write(bt_tally* h, unsigned long long* where, unsigned long l
     return fn && fn(st, (unsigned long long)(uintptr_t)where, v, 0) == 0;
 }
 
+// host -> device copy of a caller buffer on `st`: DMA straight from pinned
+// memory, through the pinned ring + host threads from pageable memory.
+// Returns once `src` has been read.
 static bt_status h2d(bt_tally* h, void* dst, const void* src, size_t bytes, cudaStream_t st,
                      bool pageable) {
     if (!bytes) return BT_OK;
@@ -1040,7 +1040,7 @@ static bt_status walk_end(bt_tally* h, int64_t max_sweeps, bt_summary* summary,
     }
     if (c[C_ERR] & 2ull)
         return set_err(BT_ERUNTIME, "streamed move: inputs did not arrive within 5 s "
-                                    "(set BT_OPT_STREAM_MOVE = 0 under tools that serialise launches)");
+                                    "(BT_OPT_STREAM_MOVE = 0 walks chunk by chunk)");
     if (c[C_ERR])
         return set_err(BT_ERUNTIME, "trace did not terminate within %lld sweeps",
                        (long long)max_sweeps);
