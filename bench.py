@@ -62,6 +62,8 @@ def parse():
     p.add_argument("--blocks-per-sm", type=int, default=0)
     p.add_argument("--staged", type=int, default=-1,
                    help="refill: -1 library default, 0 v1, 1 stage kernel, 2 direct")
+    p.add_argument("--no-stream-move", action="store_true",
+                   help="e2e: one walk launch per input chunk instead of one streamed launch")
     return p.parse_args()
 
 
@@ -94,7 +96,8 @@ def config(args, world, ne):
         "options": {"sort": bool(args.sort),
                     "warp_agg": ("adaptive" if args.warp_agg < 0 else bool(args.warp_agg)),
                     "staged": "default" if args.staged < 0 else args.staged,
-                    "blocks_per_sm": args.blocks_per_sm or "default"},
+                    "blocks_per_sm": args.blocks_per_sm or "default",
+                    "stream_move": not args.no_stream_move},
     }
 
 
@@ -468,7 +471,8 @@ def run_ours(args):
 
     mt = MeshTally(mesh, P, device=local, sort=bool(args.sort),
                    warp_aggregate=None if args.warp_agg < 0 else bool(args.warp_agg),
-                   staged=True if args.staged < 0 else args.staged)
+                   staged=True if args.staged < 0 else args.staged,
+                   stream_move=not args.no_stream_move)
     if args.blocks_per_sm:
         mt.set_option(_lib.BT_OPT_BLOCKS_PER_SM, args.blocks_per_sm)
     d_pos = torch.from_numpy(pos).to(dev)
