@@ -404,6 +404,10 @@ __device__ __forceinline__ void score_aggregated(const WalkArgs& a, bool has_sco
 // pending bin against the next lane's) finds a duplicate, which is what a point
 // source with short flights produces (6x fewer contended atomics, measured in
 // profiles/r01_options.jsonl).  Idle lanes flush their pending score.
+#ifndef BT_AGG_HOLD
+#define BT_AGG_HOLD 128
+#endif
+constexpr int AGG_HOLD = BT_AGG_HOLD;  // iterations aggregation stays on once a probe finds contention
 __device__ __forceinline__ void flush_pending(const WalkArgs& a, Pending& P, bool idle) {
     constexpr unsigned FULL = 0xffffffffu;
     // mode flags resolved once per kernel (Pending::init); P.agg is the
@@ -415,7 +419,7 @@ __device__ __forceinline__ void flush_pending(const WalkArgs& a, Pending& P, boo
         // low 32 bits: a false match only aggregates, which stays exact
         const bool dup = P.has && lane < 31 && ((hm >> (lane + 1)) & 1u) && nxt == (int)P.bin;
         P.agg = __any_sync(FULL, dup);
-        P.probe = 4;
+        P.probe = P.agg ? AGG_HOLD : 4;
     }
     const bool agg = P.agg;
     if (agg) {

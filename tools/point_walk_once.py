@@ -23,8 +23,9 @@ d = torch.stack([s * torch.cos(phi), s * torch.sin(phi), mu], 1)
 dest = (pos - torch.log(torch.rand(n, generator=g, device=dev, dtype=torch.float64))[:, None] / sig * d).contiguous()
 fly = torch.ones(n, dtype=torch.int8, device=dev)
 w = torch.ones(n, dtype=torch.float64, device=dev)
-mt = MeshTally(build_cube_mesh(55), n)
+wa = int(sys.argv[2]) if len(sys.argv) > 2 else -1  # -1 adaptive, 0 never, 1 always
+mt = MeshTally(build_cube_mesh(55), n, warp_aggregate=None if wa < 0 else bool(wa))
 for _ in range(3):
     mt.initialize_particle_location(pos)
     r = mt.move_to_next_location(dest, fly, w)
-print(sig, r.events, round(mt.last_timing()[0], 3))
+print('point', sig, 'wagg', wa, r.events, round(mt.last_timing()[0], 3))
