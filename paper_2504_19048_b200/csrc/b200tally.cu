@@ -1456,8 +1456,10 @@ bt_status bt_move_to_next_location(bt_tally* h, const double* destinations, cons
         // or to completion (CUDA_LAUNCH_BLOCKING) cannot deadlock it.
         // Pageable inputs are staged by host threads while the walk runs and
         // keep one launch per chunk.
-        bool streamed = h->opt_stream_move && nch > 1 && h->opt_staged == 2 && !h->di_pending &&
-                        !any_pageable;
+        // (From 2^18 particles: below that the copies are a few tens of us.)
+        bool streamed = h->opt_stream_move && h->opt_staged == 2 && !h->opt_sort &&
+                        !h->di_pending && !any_pageable &&
+                        (h->move_chunks > 1 || (h->move_chunks <= 0 && count >= (1 << 18)));
         if (streamed && h->stream_ops != 0) {
             if (!h->ready) TRY(dalloc(&h->ready, 1));
             streamed = stream_write(h, h->ready, 0, h->cstream);

@@ -411,10 +411,12 @@ def test_recorded_source_weight_is_numpy_sum(frac_flying):
     mt.close()
 
 
-@pytest.mark.parametrize("stream_move,pinned", [(True, False), (True, True), (False, False)])
-def test_pipelined_host_inputs_match_device_inputs(stream_move, pinned):
-    """>= 4M particles: host positions are copied and localized in chunks, host
-    move inputs are copied in chunks and walked either by ONE launch that
+@pytest.mark.parametrize("n,stream_move,pinned", [(5_000_000, True, False), (5_000_000, True, True),
+                                                   (5_000_000, False, False), (300_001, True, True)])
+def test_pipelined_host_inputs_match_device_inputs(n, stream_move, pinned):
+    """Host positions are copied and localized in chunks (>= 4M particles),
+    host move inputs are copied in chunks (from 2^18 particles when streamed)
+    and walked either by ONE launch that
     waits for each chunk (stream_move, the default, with pinned inputs) or by
     one launch per chunk on two streams (pageable inputs, or stream_move off)
     -- the result must equal the single-launch device-input path bit for
@@ -422,7 +424,6 @@ def test_pipelined_host_inputs_match_device_inputs(stream_move, pinned):
     torch = pytest.importorskip("torch")
     m = build_cube_mesh(12)
     gen = np.random.default_rng(21)
-    n = 5_000_000
     pos = synth.uniform_box(gen, n)
     dest = synth.flight_destinations(gen, pos, 5.0)
     fly = (gen.random(n) < 0.9).astype(np.int8)
